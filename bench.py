@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""bench.py -- BLR prefill forward on B200: tokens/s, speedup vs cuBLAS dense bf16, roofline.
+
+Default workload = BASELINE.json configs[1] (C2): the GPT2-S MLP (c_fc 768->3072, then
+c_proj 3072->768) over batch 8 x seq 1024 = 8192 tokens, run in each BLR format of PAPER.md
+Table 3 (low-rank r=192; Monarch r=192 b=4; BLAST r=192 b=6).  One *step* = one pass of the
+whole hot path over the batch: the three MLPs back to back (6 BLR layer calls, 12 kernels).
+value = tokens/s counting one token through one BLR MLP as one token (3 * 8192 per step).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2|C1|C3|C4|C4M]
+
+Multi-GPU (torchrun, one process per GPU): every rank runs the full batch on its own GPU
+(token-sharded weak scaling, factors replicated, no collective on the data path); the step
+time is the max over ranks; value = tokens of all ranks / that time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2512_20861_b200 import configs, roofline, synth  # noqa: E402
+
+METRIC = "BLR layer tokens/s & speedup vs cuBLAS dense bf16; % of B200 HBM/TC roofline"
+
+
+# ------------------------------------------------------------------------------- helpers -------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def factors_for(L, layer_id, device):
+    if L.method == "lowrank":
+        return synth.lowrank_factors(L.i, L.o, L.r, 0, layer_id, device)
+    if L.method == "monarch":
+        return synth.monarch_factors(L.i, L.o, L.b1, L.b2, L.r_blk, 0, layer_id, device)
+    return synth.blast_factors(L.i, L.o, L.b1, L.b2, L.r, 0, layer_id, device)
+
+
+def build_chains(w):
+    """Group the workload's layers into chains (one per method): c_fc -> c_proj style MLPs when
+    consecutive layers connect (o == next i), else single layers."""
+    by_method = {}
+    for j, L in enumerate(w.layers):
+        by_method.setdefault(L.method, []).append((j, L))
+    chains = []
+    for m, items in by_method.items():
+        cur = []
+        for j, L in items:
+            if cur and cur[-1][1].o != L.i:
+                chains.append(cur)
+                cur = []
+            cur.append((j, L))
+        chains.append(cur)
+    return chains
+
+
+class Sampler:
+    """nvml clock / throttle-reason sampler running during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.ok = False
+        self.samples = []
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        mhz = [s[0] for s in self.samples]
+        mask = 0
+        for _, rs in self.samples:
+            mask |= rs
+        reasons = [v for k, v in self.REASONS.items() if mask & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(mhz)}
+
+
+# ------------------------------------------------------------------------------- reference ----
+def run_reference(args, w):
+    """--impl reference: the fp64 oracle as it stands, on this host's cores, on a bounded sample
+    of the same workload (each step = `rows` token rows through every layer of the workload)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    from oracle import oracle as orc
+    rows = args.ref_rows
+    chains = build_chains(w)
+    facs = {j: [t.float().numpy().astype(np.float64) for t in factors_for(L, j, "cpu")] for j, L in enumerate(w.layers)}
+    X = synth.make_x(rows, w.layers[0].i, seed=0).float().numpy().astype(np.float64)
+
+    def step():
+        for chain in chains:
+            h = X if chain[0][1].i == X.shape[1] else synth.make_x(rows, chain[0][1].i, seed=1).double().numpy()
+            for j, L in chain:
+                f = facs[j]
+                if L.method == "lowrank":
+                    h = orc.lowrank_forward(h, *f)
+                elif L.method == "monarch":
+                    h = orc.monarch_forward(h, *f, L.b1, L.b2)
+                else:
+                    h = orc.blast_forward(h, *f)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = rows * len(chains) / dt
+    cores = orc.num_threads()
+    sample = f"{rows} token rows of {w.key} through all {len(w.layers)} layers per step (fp64 oracle)"
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{w.key}: {w.desc}", "rows_per_step": rows},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(w, target_s=10.0):
+    """Time the oracle (as it stands) on a bounded token sample of the same workload."""
+    import numpy as np
+
+    from oracle import oracle as orc
+    chains = build_chains(w)
+    facs = {j: [t.float().numpy().astype(np.float64) for t in factors_for(L, j, "cpu")] for j, L in enumerate(w.layers)}
+
+    def run(rows):
+        t0 = time.perf_counter()
+        for chain in chains:
+            h = synth.make_x(rows, chain[0][1].i, seed=0).double().numpy()
+            for j, L in chain:
+                f = facs[j]
+                if L.method == "lowrank":
+                    h = orc.lowrank_forward(h, *f)
+                elif L.method == "monarch":
+                    h = orc.monarch_forward(h, *f, L.b1, L.b2)
+                else:
+                    h = orc.blast_forward(h, *f)
+        return time.perf_counter() - t0
+
+    rows = 16
+    dt = run(rows)
+    rows = int(max(16, min(w.n, rows * target_s / max(dt, 1e-3))))
+    dt = run(rows)
+    return {"value": rows * len(chains) / dt, "unit": "tokens/s", "cores": orc.num_threads(), "kind": "oracle",
+            "sample": f"{rows} token rows of {w.key} through every layer ({dt:.1f} s fp64 on host)"}
+
+
+# ------------------------------------------------------------------------------- main bench ---
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    args = ap.parse_args()
+    w = configs.WORKLOADS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    import paper_2512_20861_b200 as blr
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    lib = blr.load()
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- inputs (seeded, synthetic; rank offset in the seed so shards differ)
+    chains = build_chains(w)
+    n = w.n
+    facs = {j: [t.to(dev) for t in factors_for(L, j, "cpu")] for j, L in enumerate(w.layers)}
+    xs = {}
+    for ci, chain in enumerate(chains):
+        xs[ci] = synth.make_x(n, chain[0][1].i, seed=rank, layer_id=ci, device=dev)
+
+    def call(L, j, h):
+        f = facs[j]
+        if L.method == "lowrank":
+            return blr.lowrank_matmul(h, *f, out=outs[j], workspace=wss[j])
+        if L.method == "monarch":
+            return blr.monarch_matmul(h, *f, L.b1, L.b2, out=outs[j], workspace=wss[j])
+        return blr.blast_matmul(h, *f, out=outs[j], workspace=wss[j])
+
+    outs, wss = {}, {}
+    for j, L in enumerate(w.layers):
+        outs[j] = torch.empty((n, L.o), dtype=torch.bfloat16, device=dev)
+        if L.method == "lowrank":
+            nb = lib.blr_lowrank_workspace_size(n, L.i, L.o, L.r)
+        elif L.method == "monarch":
+            nb = lib.blr_monarch_workspace_size(n, L.i, L.o, L.b1, L.b2, L.r_blk)
+        else:
+            nb = lib.blr_blast_workspace_size(n, L.i, L.o, L.b1, L.b2, L.r)
+        wss[j] = torch.empty(nb, dtype=torch.uint8, device=dev)
+
+    def step(x_by_chain):
+        for ci, chain in enumerate(chains):
+            h = x_by_chain[ci]
+            for j, L in chain:
+                h = call(L, j, h)
+        return h
+
+    # ---- per-launch events (C-ABI profiling hook) and L2 flush buffer
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
+    n_launch = 2 * len(w.layers)
+    K, W = args.steps, args.warmup
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * n_launch)] for _ in range(K)]
+    for row in ev:
+        for e in row:
+            e.record(stream)  # forces creation of the underlying cudaEvent_t
+    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+
+    for _ in range(W):
+        flush.zero_()
+        step(xs)
+    torch.cuda.synchronize()
+
+    import ctypes
+    launches = 0
+    sampler = Sampler(dev.index)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for s in range(K):
+            flush.zero_()  # L2 flush between timed steps (outside the step events)
+            arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in ev[s]])
+            lib.blr_profile_begin(arr, 2 * n_launch)
+            step_ev[s][0].record(stream)
+            step(xs)
+            step_ev[s][1].record(stream)
+            launches += lib.blr_profile_end()
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+
+    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+    t_ms = sum(step_ms) / K
+    per_launch = [[ev[s][2 * j].elapsed_time(ev[s][2 * j + 1]) for j in range(n_launch)] for s in range(K)]
+    launch_ms = [sum(per_launch[s][j] for s in range(K)) / K for j in range(n_launch)]
+    if ws > 1:
+        t = torch.tensor([t_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_ms = float(t.item())
+
+    tokens_per_step = n * len(chains)
+    value = ws * tokens_per_step / (t_ms * 1e-3)
+
+    # ---- per-layer accounting; launch j: layer j//2, phase j%2 (0 = proj S1[+S2], 1 = expand S3)
+    peaks = roofline.load_peaks(ROOT)
+    per_layer = []
+    for j, L in enumerate(w.layers):
+        c = roofline.layer_counts(L, n)
+        ms = launch_ms[2 * j] + launch_ms[2 * j + 1]
+        t_roof = roofline.roofline_time_s(c["flops"], c["bytes"], peaks) * 1e3
+        per_layer.append({"layer": f"{L.model}.{L.name}.{L.method}", "ms": ms, "proj_ms": launch_ms[2 * j],
+                          "expand_ms": launch_ms[2 * j + 1], "tflops": c["flops"] / ms * 1e-9,
+                          "gbs_alg": c["bytes"] / ms * 1e-6, "roofline_frac": t_roof / ms})
+
+    # ---- dominant kernel roofline (algorithmic bytes/flops per launch)
+    jmax = max(range(n_launch), key=lambda j: launch_ms[j])
+    Ld = w.layers[jmax // 2]
+    phase = "proj" if jmax % 2 == 0 else "expand"
+    alg = phase_counts(Ld, n, phase)
+    dt_s = launch_ms[jmax] * 1e-3
+    bw_t = alg["bytes"] / peaks["hbm_gbs"] / 1e9
+    tc_t = alg["flops"] / (peaks["bf16_tflops"] * 1e12)
+    bound = "hbm" if bw_t >= tc_t else "tensor"
+    if bound == "hbm":
+        achieved, peak, unit = alg["bytes"] / dt_s / 1e9, peaks["hbm_gbs"], "GB/s"
+    else:
+        achieved, peak, unit = alg["flops"] / dt_s / 1e12, peaks["bf16_tflops"], "TFLOP/s"
+    traffic = profiled_traffic(Ld, phase)
+    roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "traffic": traffic, "kernel": f"blr_gemm_kernel<{phase_kind(Ld, phase)}> ({Ld.model}.{Ld.name}.{Ld.method} {phase})",
+            "algorithmic_bytes": alg["bytes"], "algorithmic_flops": alg["flops"], "launch_ms": launch_ms[jmax],
+            "share_of_step": launch_ms[jmax] / t_ms, "peak_source": peaks.get("source", "measured")}
+
+    # ---- cuBLAS dense bf16 comparator on the same shapes (X @ W, W reconstructed once)
+    dense = None
+    if not args.no_dense:
+        dense = dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev)
+
+    # ---- end to end through the public API with host buffers (H2D X, D2H Y inside the region)
+    e2e = e2e_run(w, chains, facs, xs, flush, stream, min(K, 20), dev)
+
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": K, "warmup": W,
+            "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{w.key}: {w.desc}", "n_tokens_per_gpu": n,
+                       "value_def": f"tokens/s; one step = {len(chains)} BLR MLPs/layer chains x {n} tokens",
+                       "layers": [f"{L.model}.{L.name}.{L.method}(r={L.r},b={L.b})" for L in w.layers],
+                       "l2": "flushed between timed steps (write of 2x L2), outside the step events",
+                       "parallelism": f"token-sharded dp{ws}, no data-path collective"},
+            "roofline": roof, "per_layer": per_layer, "gpu_launches": launches,
+            "clocks": sampler.summary(), "e2e": e2e}
+    if dense is not None:
+        line["cublas_dense_bf16"] = dense
+        line["speedup_vs_cublas"] = dense["ms_per_step"] / t_ms
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def phase_kind(L, phase):
+    if phase == "expand":
+        return "KIND_GEMM"
+    return {"lowrank": "KIND_GEMM", "monarch": "KIND_MONARCH_PROJ", "blast": "KIND_BLAST_PROJ"}[L.method]
+
+
+def phase_counts(L, n, phase):
+    """Algorithmic bytes / FLOPs of one phase: proj reads X and the first-stage
+    factors (V, and S for BLAST); expand reads U and writes Y.  The intermediate is excluded."""
+    B = roofline.BF16
+    if phase == "proj":
+        if L.method == "lowrank":
+            fl, pb = 2 * n * L.i * L.r, L.i * L.r
+        elif L.method == "monarch":
+            fl, pb = 2 * n * L.i * L.r, L.i * L.r
+        else:
+            fl, pb = 2 * n * L.i * L.r + 2 * n * L.r * L.b1 * L.b2, L.i * L.r + L.b1 * L.b2 * L.r
+        return {"bytes": B * (n * L.i + pb), "flops": fl}
+    fl = 2 * n * L.r * L.o
+    return {"bytes": B * (L.r * L.o + n * L.o), "flops": fl}
+
+
+def profiled_traffic(L, phase):
+    """dram bytes per launch from the committed ncu --set full summary, if one exists."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(path))
+        return d.get(f"{L.model}.{L.name}.{L.method}.{phase}")
+    except (OSError, ValueError):
+        return None
+
+
+def dense_weight(L, f):
+    """Dense W (i x o, bf16) for the cuBLAS comparator, reconstructed once in fp32 with torch."""
+    if L.method == "lowrank":
+        V, U = f
+        return (V.float() @ U.float()).to(torch.bfloat16)
+    if L.method == "monarch":
+        V, U = f
+        b1, b2, rp = L.b1, L.b2, L.r_blk
+        p, q = L.p, L.q
+        Vb = V.float().reshape(b1, rp, b2, p)           # m = rho*b2 + k
+        Ub = U.float().reshape(b2, q, b1, rp)           # U[k, c, l*r' + rho]
+        W = torch.einsum("lrka,kclr->lakc", Vb, Ub)     # (b1, p, b2, q)
+        return W.reshape(b1 * p, b2 * q).to(torch.bfloat16)
+    V, S, U = f
+    W = torch.einsum("lar,lkr,krc->lakc", V.float(), S.float(), U.float())
+    return W.reshape(L.i, L.o).to(torch.bfloat16)
+
+
+def dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev):
+    Ws = {j: dense_weight(L, facs[j]) for j, L in enumerate(w.layers)}
+    outs = {j: torch.empty((w.n, L.o), dtype=torch.bfloat16, device=dev) for j, L in enumerate(w.layers)}
+
+    def step():
+        for ci, chain in enumerate(chains):
+            h = xs[ci]
+            for j, L in chain:
+                h = torch.matmul(h, Ws[j], out=outs[j])
+
+    for _ in range(W):
+        flush.zero_()
+        step()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    torch.cuda.synchronize()
+    for s in range(K):
+        flush.zero_()
+        evs[s][0].record(stream)
+        step()
+        evs[s][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / K
+    return {"ms_per_step": ms, "tokens_per_s": w.n * len(chains) / (ms * 1e-3), "impl": "torch.matmul (cuBLAS/cuBLASLt) bf16"}
+
+
+def e2e_run(w, chains, facs, xs, flush, stream, K, dev):
+    """Same step through the public API with pinned HOST buffers: H2D of each chain's X and
+    D2H of each chain's final Y are inside the timed region every step."""
+    xh = {ci: xs[ci].cpu().pin_memory() for ci in xs}
+    last = {ci: chain[-1][1] for ci, chain in enumerate(chains)}
+    yh = {ci: torch.empty((w.n, last[ci].o), dtype=torch.bfloat16).pin_memory() for ci in xs}
+    xd = {ci: torch.empty_like(xs[ci]) for ci in xs}
+    h2d = sum(t.numel() * 2 for t in xh.values())
+    d2h = sum(t.numel() * 2 for t in yh.values())
+
+    def one():
+        for ci in xd:
+            xd[ci].copy_(xh[ci], non_blocking=True)
+        for ci, chain in enumerate(chains):
+            h = xd[ci]
+            for j, L in chain:
+                h = step_call(L, j, h)
+            yh[ci].copy_(h, non_blocking=True)
+
+    import paper_2512_20861_b200 as blr
+
+    def step_call(L, j, h):
+        f = facs[j]
+        if L.method == "lowrank":
+            return blr.lowrank_matmul(h, *f)
+        if L.method == "monarch":
+            return blr.monarch_matmul(h, *f, L.b1, L.b2)
+        return blr.blast_matmul(h, *f)
+
+    one()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for s in range(K):
+        flush.zero_()
+        evs[s][0].record(stream)
+        one()
+        evs[s][1].record(stream)
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in evs) / K
+    return {"value": w.n * len(chains) / (ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,142 @@
+/*
+ * blr.h -- C ABI of the B200-native block-low-rank (BLR) prefill library (arXiv 2512.20861).
+ *
+ * The library computes the multi-token forward product of one linear layer whose weight is
+ * block-low-rank, Y = X W with W in R^{i x o} (§2.1), for three formats:
+ *   - low-rank  W = V U
+ *   - Monarch   W_{l,k} = V_{l,k} U_{l,k}
+ *   - BLAST     W_{l,k} = V_l S_{l,k} U_k, S_{l,k} diag.
+ * with X [n_tok, d_in] and Y [n_tok, d_out], blocks l in [b1] along the input, k in [b2] along
+ * the output, p = d_in / b1, q = d_out / b2.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Every tensor argument is a CUDA DEVICE pointer to a dense, row-major, contiguous array of
+ *    bf16 values (the 16-bit pattern of __nv_bfloat16), base address 16-byte aligned.
+ *    Arithmetic: bf16 operands, fp32 accumulation; the rank-r intermediate is rounded once to
+ *    bf16 (round-to-nearest-even) and Y is rounded RNE to bf16 (reading R11).
+ *  - Y must not alias X, a factor or the workspace.
+ *  - Calls are asynchronous on `stream` (0 = legacy default stream).  The library never
+ *    synchronizes, never allocates or frees caller memory and keeps no pointer after return.
+ *    The caller owns all memory; `workspace` must stay valid until the work on `stream` ends.
+ *  - `workspace` holds the bf16 intermediate between the two tcgen05 phases; query its size
+ *    with the matching *_workspace_size() function.  ws_bytes smaller than that returns
+ *    BLR_ERR_WORKSPACE.
+ *  - Validation happens on the host before any launch; on error nothing is enqueued.
+ *      BLR_ERR_NULL        a required pointer is NULL (with n_tok > 0)
+ *      BLR_ERR_SHAPE       a non-positive dimension, n_tok < 0, b1 !| d_in, b2 !| d_out,
+ *                          or (Monarch) r_blk inconsistent with the factor shapes
+ *      BLR_ERR_ALIGN       a row pitch that is not a multiple of 16 bytes, i.e. d_in, d_out,
+ *                          r, r', p or q not a multiple of 8, or a pointer not 16-B aligned
+ *      BLR_ERR_UNSUPPORTED a shape outside the kernel envelope (b1 or b2 > 16, r' > 256,
+ *                          Monarch transposed output order) -- there is NO CPU fallback
+ *      BLR_ERR_WORKSPACE   ws_bytes too small
+ *      BLR_ERR_ARCH        the current device is not a compute-capability 10.0 (sm_100a) GPU
+ *      BLR_ERR_CUDA        a CUDA runtime/driver error while encoding tensor maps or launching
+ *  - n_tok == 0 is a successful no-op.
+ *  - The library holds one process-wide, thread-safe cache (device properties and the
+ *    tensor-map encoder); blr_clear_cache() drops it.
+ */
+#ifndef BLR_H_
+#define BLR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    BLR_OK = 0,
+    BLR_ERR_NULL = 1,
+    BLR_ERR_SHAPE = 2,
+    BLR_ERR_ALIGN = 3,
+    BLR_ERR_UNSUPPORTED = 4,
+    BLR_ERR_WORKSPACE = 5,
+    BLR_ERR_ARCH = 6,
+    BLR_ERR_CUDA = 7
+} blr_status;
+
+/* Order of the composite (r' b2) middle dimension of the Monarch V tensor. */
+typedef enum {
+    BLR_MON_V_B2_FASTEST = 0,     /* original layout, "contiguous along b2 then r'":  m = rho*b2 + k */
+    BLR_MON_V_RPRIME_FASTEST = 1  /* after re-layout (1), r' first:                  m = k*r' + rho */
+} blr_monarch_vlayout;
+
+/* Order of Monarch output columns (PAPER.md L45 footnote, L219-220). */
+typedef enum {
+    BLR_OUT_CANONICAL = 0,  /* Y[t, k*q + c]  (PAPER.md L53 Y_k blocks side by side)          */
+    BLR_OUT_TRANSPOSED = 1  /* Y[t, c*b2 + k] ("transposed" permutation) -- not yet supported */
+} blr_out_order;
+
+typedef void* blr_stream_t; /* a cudaStream_t */
+
+/*
+ * Low-rank layer, Y = (X V) U.
+ *   X [n_tok, d_in], V [d_in, r], U [r, d_out], Y [n_tok, d_out].
+ *   Workspace: the bf16 intermediate Z [n_tok, r].
+ */
+blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t r,
+                              const void* V, const void* U, void* Y, void* workspace,
+                              size_t ws_bytes, blr_stream_t stream);
+size_t blr_lowrank_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, int64_t r);
+
+/*
+ * Monarch layer, Y_k = sum_l X_l V_{l,k} U_{l,k}, factors in the paper's
+ * storage:
+ *   V [b1, r_blk*b2, p]   middle dimension ordered by v_layout (see blr_monarch_vlayout),
+ *                         V_{l,k}[a, rho] = V[l, m(rho,k), a]
+ *   U [b2, q, b1*r_blk]   inner dimension "contiguous along r' then b1",
+ *                         U_{l,k}[rho, c] = U[k, c, l*r_blk + rho]
+ *   Y [n_tok, d_out]      out_order must be BLR_OUT_CANONICAL.
+ *   The r'<->b2 and b2<->b1 permutations are folded into the kernel's TMA
+ *   addressing; V is read in place in either layout (no re-layout pass).
+ *   Workspace: the bf16 intermediate Z' [b2][n_tok][b1*r_blk].
+ */
+blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1,
+                              int64_t b2, int64_t r_blk, const void* V, const void* U,
+                              int v_layout, int out_order, void* Y, void* workspace,
+                              size_t ws_bytes, blr_stream_t stream);
+size_t blr_monarch_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
+                                  int64_t r_blk);
+
+/*
+ * BLAST layer, Y_k = ( sum_l (X_l V_l) S_{l,k} ) U_k, factors in the paper's
+ * storage:
+ *   V [b1, p, r], S [b1, b2, r] (the diagonals of S_{l,k}), U [b2, r, q], Y [n_tok, d_out].
+ *   (north_star's s_ij is S[j, i, :]: index order (input block, output block); R5.)
+ *   Workspace: the bf16 intermediate Z'' [b2][n_tok][r]  (the S-weighted block sums).
+ */
+blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1,
+                            int64_t b2, int64_t r, const void* V, const void* S, const void* U,
+                            void* Y, void* workspace, size_t ws_bytes, blr_stream_t stream);
+size_t blr_blast_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
+                                int64_t r);
+
+/* Human-readable name of a status code (static storage, never NULL). */
+const char* blr_status_string(blr_status s);
+
+/* Library version "major.minor.patch" (static storage). */
+const char* blr_version(void);
+
+/* Number of CUDA kernel launches the most recent successful call on this thread enqueued. */
+int blr_last_launch_count(void);
+
+/*
+ * Per-launch timing hook (measurement only).  While armed on the calling thread, every kernel
+ * launch the library enqueues records events[2j] (cudaEvent_t) on the launch stream right before
+ * launch j and events[2j+1] right after it, for j < capacity/2; no other effect.  Arm with a
+ * caller-owned array of `capacity` created events; blr_profile_end() disarms and returns the
+ * number of launches recorded.
+ */
+void blr_profile_begin(void** events, int capacity);
+int blr_profile_end(void);
+
+/* Drop the process-wide caches (device properties, tensor-map encoder entry point). */
+void blr_clear_cache(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLR_H_ */

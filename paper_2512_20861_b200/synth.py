@@ -38,12 +38,18 @@ def randn_bf16(shape, std: float, seed: int, device="cpu") -> torch.Tensor:
 def make_x(n: int, i: int, seed: int = 0, layer_id: int = 0, device="cpu",
            outliers: int = 0, outlier_scale: float = 20.0) -> torch.Tensor:
     """Activations X [n, i] ~ N(0,1) in bf16.  ``outliers`` > 0 multiplies that many evenly
-    spaced input channels by ``outlier_scale`` (parity-only stress variant)."""
-    x = randn_bf16((n, i), 1.0, _seed(seed, "X", layer_id), device)
-    if outliers:
-        idx = torch.linspace(0, i - 1, outliers, device=x.device).round().long()
-        x[:, idx] = (x[:, idx].float() * outlier_scale).to(torch.bfloat16)
-    return x
+    spaced input channels by ``outlier_scale`` and then rescales every channel so the expected
+    squared row norm stays i (outlier channels stay ``outlier_scale`` x the others; the layer's
+    output keeps the recipe's unit variance).  Parity-only stress variant."""
+    if not outliers:
+        return randn_bf16((n, i), 1.0, _seed(seed, "X", layer_id), device)
+    g = torch.Generator(device=device)
+    g.manual_seed(_seed(seed, "X", layer_id))
+    x = torch.randn(n, i, generator=g, device=device, dtype=torch.float32)
+    idx = torch.linspace(0, i - 1, outliers, device=x.device).round().long()
+    x[:, idx] *= outlier_scale
+    x *= (i / (i - outliers + outliers * outlier_scale ** 2)) ** 0.5
+    return x.to(torch.bfloat16)
 
 
 def lowrank_factors(i: int, o: int, r: int, seed: int = 0, layer_id: int = 0, device="cpu"):

@@ -1,0 +1,100 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol include/blr.h declares,
+and host-side validation returns the documented status codes before touching CUDA."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_2512_20861_b200 as blr
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "blr.h")
+
+
+def declared_symbols():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(blr_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_entry_points():
+    syms = declared_symbols()
+    for s in ("blr_lowrank_matmul", "blr_monarch_matmul", "blr_blast_matmul", "blr_status_string",
+              "blr_lowrank_workspace_size", "blr_monarch_workspace_size", "blr_blast_workspace_size"):
+        assert s in syms
+
+
+def test_library_exports_every_declared_symbol():
+    blr.build()
+    lib = ctypes.CDLL(blr.lib_path())
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+
+
+def test_status_strings_and_version():
+    lib = blr.load()
+    names = [lib.blr_status_string(c).decode() for c in range(8)]
+    assert names == ["BLR_OK", "BLR_ERR_NULL", "BLR_ERR_SHAPE", "BLR_ERR_ALIGN", "BLR_ERR_UNSUPPORTED",
+                     "BLR_ERR_WORKSPACE", "BLR_ERR_ARCH", "BLR_ERR_CUDA"]
+    assert re.match(r"\d+\.\d+\.\d+", lib.blr_version().decode())
+
+
+def test_workspace_sizes():
+    lib = blr.load()
+    # S3 contraction >= 128: one bf16 intermediate
+    assert lib.blr_lowrank_workspace_size(100, 64, 64, 128) == 100 * 128 * 2
+    assert lib.blr_monarch_workspace_size(100, 64, 64, 4, 2, 32) == 2 * 100 * 4 * 32 * 2
+    assert lib.blr_blast_workspace_size(100, 64, 64, 4, 2, 192) == 2 * 100 * 192 * 2
+    # shorter contractions keep a compensated hi|lo pair: twice the bytes
+    assert lib.blr_lowrank_workspace_size(100, 64, 64, 16) == 2 * 100 * 16 * 2
+    assert lib.blr_monarch_workspace_size(100, 64, 64, 4, 2, 8) == 2 * 2 * 100 * 4 * 8 * 2
+    assert lib.blr_blast_workspace_size(100, 64, 64, 4, 2, 16) == 2 * 2 * 100 * 16 * 2
+    assert lib.blr_blast_workspace_size(0, 64, 64, 4, 2, 16) == 0
+
+
+FAKE = 0x10000  # 16-B aligned, never dereferenced: validation fails before any CUDA call
+
+
+@pytest.mark.parametrize("args,code", [
+    # (n, i, o, b1, b2, r) -> expected status
+    ((-1, 64, 64, 2, 2, 16), 2),   # n < 0
+    ((8, 64, 64, 3, 2, 16), 2),    # b1 does not divide d_in
+    ((8, 64, 64, 2, 3, 16), 2),    # b2 does not divide d_out
+    ((8, 64, 64, 2, 2, 12), 3),    # r not a multiple of 8
+    ((8, 48, 64, 4, 2, 16), 3),    # p = 12 not a multiple of 8
+    ((8, 544, 64, 17, 2, 16), 4),  # b1 > 16 unsupported
+])
+def test_blast_validation(args, code):
+    lib = blr.load()
+    n, i, o, b1, b2, r = args
+    st = lib.blr_blast_matmul(FAKE, n, i, o, b1, b2, r, FAKE, FAKE, FAKE, FAKE, FAKE, 1 << 40, None)
+    assert st == code, (args, lib.blr_status_string(st))
+
+
+def test_null_and_workspace_errors():
+    lib = blr.load()
+    assert lib.blr_blast_matmul(None, 8, 64, 64, 2, 2, 16, FAKE, FAKE, FAKE, FAKE, FAKE, 1 << 40, None) == 1
+    assert lib.blr_blast_matmul(FAKE, 8, 64, 64, 2, 2, 16, FAKE, FAKE, FAKE, FAKE, FAKE, 10, None) == 5
+    assert lib.blr_lowrank_matmul(FAKE, 8, 64, 64, 16, FAKE, FAKE, FAKE, FAKE, 10, None) == 5
+    assert lib.blr_lowrank_matmul(FAKE + 8, 8, 64, 64, 16, FAKE, FAKE, FAKE, FAKE, 1 << 40, None) == 3
+    # n_tok == 0 is a successful no-op even with NULL pointers
+    assert lib.blr_lowrank_matmul(None, 0, 64, 64, 16, None, None, None, None, 0, None) == 0
+
+
+def test_monarch_validation():
+    lib = blr.load()
+    # transposed output order is not yet supported -> UNSUPPORTED, never a fallback
+    assert lib.blr_monarch_matmul(FAKE, 8, 64, 64, 2, 2, 8, FAKE, FAKE, 0, 1, FAKE, FAKE, 1 << 40, None) == 4
+    # invalid V layout flag
+    assert lib.blr_monarch_matmul(FAKE, 8, 64, 64, 2, 2, 8, FAKE, FAKE, 7, 0, FAKE, FAKE, 1 << 40, None) == 2
+    # r' not a multiple of 8
+    assert lib.blr_monarch_matmul(FAKE, 8, 64, 64, 2, 2, 4, FAKE, FAKE, 0, 0, FAKE, FAKE, 1 << 40, None) == 3
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="CPU-only check")
+def test_no_gpu_fails_loudly():
+    """Without a device the valid call returns an error code (no silent CPU fallback)."""
+    lib = blr.load()
+    st = lib.blr_lowrank_matmul(FAKE, 8, 64, 64, 16, FAKE, FAKE, FAKE, FAKE, 1 << 40, None)
+    assert st in (6, 7)
