@@ -210,6 +210,7 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="launch every step from the host (no CUDA graph)")
     args = ap.parse_args()
     w = configs.WORKLOADS[args.config]
     if args.impl == "reference":
@@ -261,24 +262,60 @@ def main():
                 h = call(L, j, h)
         return h
 
+    # ---- launch map: which layer / phase each kernel launch of a step belongs to
+    phases = []  # (layer index, phase name) per launch, in launch order
+    for ci, chain in enumerate(chains):
+        h = xs[ci]
+        for j, L in chain:
+            h = call(L, j, h)
+            nl = lib.blr_last_launch_count()
+            names = ["proj", "expand"] if nl == 2 else ["s1", "s2", "expand"] if nl == 3 else [f"k{i}" for i in range(nl)]
+            phases += [(j, nm) for nm in names]
+    torch.cuda.synchronize()
+    n_launch = len(phases)
+
     # ---- per-launch events (C-ABI profiling hook) and L2 flush buffer
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
-    n_launch = 2 * len(w.layers)
     K, W = args.steps, args.warmup
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2 * n_launch)] for _ in range(K)]
-    for row in ev:
-        for e in row:
-            e.record(stream)  # forces creation of the underlying cudaEvent_t
+    gev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_launch)]
+    for e in gev:
+        e.record(stream)  # forces creation of the underlying cudaEvent_t
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+
+    import ctypes
+    # ---- the step as a CUDA graph (host launch overhead removed, as under the paper's
+    #      torch.compile + CUDA-graph protocol); the per-launch events of the
+    #      C-ABI profiling hook are captured as event-record nodes inside the graph.
+    graph = None
+    if not args.eager:
+        for _ in range(2):
+            step(xs)
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in gev])
+        with torch.cuda.graph(graph):
+            lib.blr_profile_begin(arr, 2 * n_launch)
+            step(xs)
+            per_replay = lib.blr_profile_end()
+        torch.cuda.synchronize()
+
+    def run_step():
+        if graph is not None:
+            graph.replay()
+            return per_replay
+        arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in gev])
+        lib.blr_profile_begin(arr, 2 * n_launch)
+        step(xs)
+        return lib.blr_profile_end()
 
     for _ in range(W):
         flush.zero_()
-        step(xs)
+        run_step()
     torch.cuda.synchronize()
 
-    import ctypes
     launches = 0
+    launch_tot = [0.0] * n_launch
     sampler = Sampler(dev.index)
     if ws > 1:
         torch.distributed.barrier()
@@ -286,20 +323,18 @@ def main():
     with sampler:
         for s in range(K):
             flush.zero_()  # L2 flush between timed steps (outside the step events)
-            arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in ev[s]])
-            lib.blr_profile_begin(arr, 2 * n_launch)
             step_ev[s][0].record(stream)
-            step(xs)
+            launches += run_step()
             step_ev[s][1].record(stream)
-            launches += lib.blr_profile_end()
-        torch.cuda.synchronize()
+            torch.cuda.synchronize()  # between steps, outside the events: read this step's launches
+            for j in range(n_launch):
+                launch_tot[j] += gev[2 * j].elapsed_time(gev[2 * j + 1])
     if ws > 1:
         torch.distributed.barrier()
 
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
     t_ms = sum(step_ms) / K
-    per_launch = [[ev[s][2 * j].elapsed_time(ev[s][2 * j + 1]) for j in range(n_launch)] for s in range(K)]
-    launch_ms = [sum(per_launch[s][j] for s in range(K)) / K for j in range(n_launch)]
+    launch_ms = [v / K for v in launch_tot]
     if ws > 1:
         t = torch.tensor([t_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -308,21 +343,22 @@ def main():
     tokens_per_step = n * len(chains)
     value = ws * tokens_per_step / (t_ms * 1e-3)
 
-    # ---- per-layer accounting; launch j: layer j//2, phase j%2 (0 = proj S1[+S2], 1 = expand S3)
+    # ---- per-layer accounting (sum of that layer's launches; phases named per launch)
     peaks = roofline.load_peaks(ROOT)
     per_layer = []
     for j, L in enumerate(w.layers):
         c = roofline.layer_counts(L, n)
-        ms = launch_ms[2 * j] + launch_ms[2 * j + 1]
+        mine = [(nm, launch_ms[x]) for x, (jj, nm) in enumerate(phases) if jj == j]
+        ms = sum(v for _, v in mine)
         t_roof = roofline.roofline_time_s(c["flops"], c["bytes"], peaks) * 1e3
-        per_layer.append({"layer": f"{L.model}.{L.name}.{L.method}", "ms": ms, "proj_ms": launch_ms[2 * j],
-                          "expand_ms": launch_ms[2 * j + 1], "tflops": c["flops"] / ms * 1e-9,
+        per_layer.append({"layer": f"{L.model}.{L.name}.{L.method}", "ms": ms,
+                          "launch_ms": {nm: v for nm, v in mine}, "tflops": c["flops"] / ms * 1e-9,
                           "gbs_alg": c["bytes"] / ms * 1e-6, "roofline_frac": t_roof / ms})
 
     # ---- dominant kernel roofline (algorithmic bytes/flops per launch)
-    jmax = max(range(n_launch), key=lambda j: launch_ms[j])
-    Ld = w.layers[jmax // 2]
-    phase = "proj" if jmax % 2 == 0 else "expand"
+    jmax = max(range(n_launch), key=lambda x: launch_ms[x])
+    Ld = w.layers[phases[jmax][0]]
+    phase = phases[jmax][1]
     alg = phase_counts(Ld, n, phase)
     dt_s = launch_ms[jmax] * 1e-3
     bw_t = alg["bytes"] / peaks["hbm_gbs"] / 1e9
@@ -334,14 +370,14 @@ def main():
         achieved, peak, unit = alg["flops"] / dt_s / 1e12, peaks["bf16_tflops"], "TFLOP/s"
     traffic = profiled_traffic(Ld, phase)
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-            "traffic": traffic, "kernel": f"blr_gemm_kernel<{phase_kind(Ld, phase)}> ({Ld.model}.{Ld.name}.{Ld.method} {phase})",
+            "traffic": traffic, "kernel": f"{phase_kind(Ld, phase)} ({Ld.model}.{Ld.name}.{Ld.method} {phase})",
             "algorithmic_bytes": alg["bytes"], "algorithmic_flops": alg["flops"], "launch_ms": launch_ms[jmax],
             "share_of_step": launch_ms[jmax] / t_ms, "peak_source": peaks.get("source", "measured")}
 
     # ---- cuBLAS dense bf16 comparator on the same shapes (X @ W, W reconstructed once)
     dense = None
     if not args.no_dense:
-        dense = dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev)
+        dense = dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev, not args.eager)
 
     # ---- end to end through the public API with host buffers (H2D X, D2H Y inside the region)
     e2e = e2e_run(w, chains, facs, xs, flush, stream, min(K, 20), dev)
@@ -353,6 +389,7 @@ def main():
                        "value_def": f"tokens/s; one step = {len(chains)} BLR MLPs/layer chains x {n} tokens",
                        "layers": [f"{L.model}.{L.name}.{L.method}(r={L.r},b={L.b})" for L in w.layers],
                        "l2": "flushed between timed steps (write of 2x L2), outside the step events",
+                       "launch": "eager" if args.eager else "CUDA graph replay of the step (both arms)",
                        "parallelism": f"token-sharded dp{ws}, no data-path collective"},
             "roofline": roof, "per_layer": per_layer, "gpu_launches": launches,
             "clocks": sampler.summary(), "e2e": e2e}
@@ -369,15 +406,22 @@ def main():
 
 
 def phase_kind(L, phase):
-    if phase == "expand":
-        return "KIND_GEMM"
-    return {"lowrank": "KIND_GEMM", "monarch": "KIND_MONARCH_PROJ", "blast": "KIND_BLAST_PROJ"}[L.method]
+    if phase in ("expand", "s1"):
+        return "blr_gemm_kernel<KIND_GEMM>"
+    if phase == "s2":
+        return "blast_s2_kernel"
+    return "blr_gemm_kernel<%s>" % {"lowrank": "KIND_GEMM", "monarch": "KIND_MONARCH_PROJ",
+                                    "blast": "KIND_BLAST_PROJ"}[L.method]
 
 
 def phase_counts(L, n, phase):
     """Algorithmic bytes / FLOPs of one phase: proj reads X and the first-stage
     factors (V, and S for BLAST); expand reads U and writes Y.  The intermediate is excluded."""
     B = roofline.BF16
+    if phase == "s1":   # BLAST split path: Z_l = X_l V_l
+        return {"bytes": B * (n * L.i + L.i * L.r), "flops": 2 * n * L.i * L.r}
+    if phase == "s2":   # BLAST split path: S-weighted block sum (reads S only, algorithmically)
+        return {"bytes": B * L.b1 * L.b2 * L.r, "flops": 2 * n * L.r * L.b1 * L.b2}
     if phase == "proj":
         if L.method == "lowrank":
             fl, pb = 2 * n * L.i * L.r, L.i * L.r
@@ -418,7 +462,7 @@ def dense_weight(L, f):
     return W.reshape(L.i, L.o).to(torch.bfloat16)
 
 
-def dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev):
+def dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev, use_graph=True):
     Ws = {j: dense_weight(L, facs[j]) for j, L in enumerate(w.layers)}
     outs = {j: torch.empty((w.n, L.o), dtype=torch.bfloat16, device=dev) for j, L in enumerate(w.layers)}
 
@@ -428,19 +472,27 @@ def dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev):
             for j, L in chain:
                 h = torch.matmul(h, Ws[j], out=outs[j])
 
-    for _ in range(W):
+    for _ in range(max(W, 2)):
         flush.zero_()
         step()
+    torch.cuda.synchronize()
+    run = step
+    if use_graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            step()
+        run = g.replay
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     torch.cuda.synchronize()
     for s in range(K):
         flush.zero_()
         evs[s][0].record(stream)
-        step()
+        run()
         evs[s][1].record(stream)
     torch.cuda.synchronize()
     ms = sum(a.elapsed_time(b) for a, b in evs) / K
-    return {"ms_per_step": ms, "tokens_per_s": w.n * len(chains) / (ms * 1e-3), "impl": "torch.matmul (cuBLAS/cuBLASLt) bf16"}
+    return {"ms_per_step": ms, "tokens_per_s": w.n * len(chains) / (ms * 1e-3),
+            "impl": "torch.matmul (cuBLAS/cuBLASLt) bf16" + (", CUDA graph" if use_graph else ", eager")}
 
 
 def e2e_run(w, chains, facs, xs, flush, stream, K, dev):

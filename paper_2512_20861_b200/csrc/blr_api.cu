@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -17,6 +18,7 @@ namespace {
 using blr::KParams;
 
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA on sm_100
+constexpr int SMEM_SLACK = 1024;    // runtime 1024-B realignment of the dynamic smem base
 
 struct DevInfo {
     int ok = 0;
@@ -27,7 +29,7 @@ struct DevInfo {
 std::mutex g_mu;
 DevInfo g_dev[64];
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-bool g_attr_set[3][64] = {};
+bool g_attr_set[4][64] = {};
 thread_local int t_last_launches = 0;
 thread_local void** t_prof_events = nullptr;
 thread_local int t_prof_cap = 0;
@@ -60,9 +62,9 @@ blr_status device_info(DevInfo& out, int& dev) {
 
 // bf16 tensor map of rank R: dims[0] innermost, strides in bytes for dims 1..R-1.
 bool encode(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
-            const uint32_t* box, CUtensorMapSwizzle sw) {
+            const uint32_t* box, CUtensorMapSwizzle sw, bool f32 = false) {
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr),
+    CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr),
                           reinterpret_cast<const cuuint64_t*>(dims), reinterpret_cast<const cuuint64_t*>(strides),
                           reinterpret_cast<const cuuint32_t*>(box), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -80,10 +82,32 @@ inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) 
 constexpr int64_t COMP_K_THRESHOLD = 128;
 inline int comp_factor(int64_t k_s3) { return k_s3 < COMP_K_THRESHOLD ? 2 : 1; }
 
-// N tile for a plain GEMM phase: <= 256 columns, multiple of 16, balanced across tiles.
-int choose_bn(int64_t N) {
-    int64_t tiles = cdiv(N, 256);
-    return static_cast<int>(rup(cdiv(N, tiles), 16));
+// BLAST runs S1 and S2 fused (b1 TMEM accumulators per token tile) when all b1 * r columns fit
+// TMEM, so X is read once; otherwise S1 (grouped GEMM), S2 (streaming) and S3 run separately.
+inline bool blast_fused(int64_t b1, int64_t r) {
+    const char* e = getenv("BLR_BLAST_PATH");
+    if (e && !strcmp(e, "fused")) return true;
+    if (e && !strcmp(e, "split")) return false;
+    return b1 * rup(r, 16) <= blr::TMEM_COLS;
+}
+
+// Swizzle for a staged-store box whose rows are `bytes` long (must match the kernel's XOR mask).
+struct Swz {
+    CUtensorMapSwizzle mode;
+    uint32_t mask;
+};
+Swz pick_swz(int64_t bytes) {
+    if (bytes == 128) return {CU_TENSOR_MAP_SWIZZLE_128B, 7u};
+    if (bytes == 64) return {CU_TENSOR_MAP_SWIZZLE_64B, 3u};
+    if (bytes == 32) return {CU_TENSOR_MAP_SWIZZLE_32B, 1u};
+    return {CU_TENSOR_MAP_SWIZZLE_NONE, 0u};
+}
+
+// Largest multiple of 8 <= 64 that divides n (n a multiple of 8).
+int chunk_width(int n) {
+    int cw = std::min(64, n);
+    while (n % cw || cw % 8) --cw;
+    return cw;
 }
 
 // Fill B-operand staging parameters.
@@ -112,28 +136,60 @@ void set_b_staging(KParams& p, bool mn_major) {
     }
 }
 
-// Stages that fit next to the (optional) S tile.
-bool finish_plan(KParams& p) {
-    p.stages = blr::MAX_STAGES;
-    while (p.stages > 1) {
-        blr::SmemLayout L = blr::smem_layout(p);
-        if (L.total + 1024 <= static_cast<uint32_t>(SMEM_LIMIT)) break;
-        --p.stages;
-    }
-    blr::SmemLayout L = blr::smem_layout(p);
-    if (L.total + 1024 > static_cast<uint32_t>(SMEM_LIMIT) || p.stages < 2) return false;
+// Programmatic dependent launch between the library's kernels (BLR_NO_PDL=1 disables).
+bool pdl_enabled() {
+    const char* e = getenv("BLR_NO_PDL");
+    return !(e && e[0] == '1');
+}
+
+bool fits(const KParams& p) {
+    return blr::smem_layout(p).total + SMEM_SLACK <= static_cast<uint32_t>(SMEM_LIMIT);
+}
+
+// Decide weight-stationary vs streaming, staging buffers and ring depth.  `allow_resident`:
+// the kind supports a resident B slice; `stage_buf_bytes` > 0: bytes of one staging buffer.
+bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes) {
     const int cols = p.n_sub * p.BN;
     if (cols > blr::TMEM_COLS) return false;
     p.acc_bufs = (2 * cols <= blr::TMEM_COLS) ? 2 : 1;
-    return true;
+    const char* e = getenv("BLR_NO_RESIDENT");
+    const bool reuse = p.tiles_m >= 2 && p.n_sub == 1 && p.kb_half <= blr::MAX_BRES - 1 && !(e && e[0] == '1');
+    const char* kb_env = getenv("BLR_KBOX");
+    const int kbox_max = (kb_env && kb_env[0] == '1') ? 1 : (p.k_blocks >= 2 ? 2 : 1);
+    for (int resident = (allow_resident && reuse) ? 1 : 0; resident >= 0; --resident) {
+        for (p.kbox = kbox_max; p.kbox >= 1; --p.kbox) {
+            for (int bufs = 2; bufs >= 1; --bufs) {
+                p.b_resident = resident;
+                p.stage_bufs = bufs;
+                if (stage_buf_bytes > 0) p.stage_warp_bytes = static_cast<uint32_t>(bufs * stage_buf_bytes);
+                for (p.stages = blr::MAX_STAGES; p.stages >= (resident ? 3 : 2); --p.stages)
+                    if (fits(p)) return true;
+            }
+        }
+    }
+    return false;
 }
 
+thread_local unsigned long long* t_trace = nullptr;
+
+// Profiling-hook event record: inside stream capture the event must be an *external* record node
+// to carry a timestamp when the graph replays; outside capture a plain record.
+cudaError_t prof_record(void* ev, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return cudaErrorUnknown;
+    return cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), st,
+                                    cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault);
+}  // debug trace buffer (blr_debug_trace)
+
 template <int KIND>
-blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const KParams& p, const DevInfo& d, int dev,
-                  cudaStream_t stream) {
+blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const KParams& p_in,
+                  const DevInfo& d, int dev, cudaStream_t stream) {
+    KParams p = p_in;
+    p.trace = t_trace;
+    if (t_trace) t_trace += 8 * 256;  // next launch traces into the next slot
     auto kfn = blr::blr_gemm_kernel<KIND>;
     const blr::SmemLayout L = blr::smem_layout(p);
-    const int smem = static_cast<int>(L.total + 1024);
+    const int smem = static_cast<int>(L.total + SMEM_SLACK);
     {
         std::lock_guard<std::mutex> lk(g_mu);
         if (!g_attr_set[KIND][dev]) {
@@ -148,13 +204,17 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const KParams& p, 
     cfg.blockDim = dim3(blr::NUM_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cfg.numAttrs = 0;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
-    if (prof && cudaEventRecord(static_cast<cudaEvent_t>(t_prof_events[2 * t_prof_n]), stream) != cudaSuccess)
+    if (prof && prof_record(t_prof_events[2 * t_prof_n], stream) != cudaSuccess)
         return BLR_ERR_CUDA;
-    if (cudaLaunchKernelEx(&cfg, kfn, a, b, p) != cudaSuccess) return BLR_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, kfn, a, b, c, p) != cudaSuccess) return BLR_ERR_CUDA;
     if (prof) {
-        if (cudaEventRecord(static_cast<cudaEvent_t>(t_prof_events[2 * t_prof_n + 1]), stream) != cudaSuccess)
+        if (prof_record(t_prof_events[2 * t_prof_n + 1], stream) != cudaSuccess)
             return BLR_ERR_CUDA;
         ++t_prof_n;
     }
@@ -162,16 +222,43 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const KParams& p, 
     return BLR_OK;
 }
 
-// One plain GEMM phase: out[t, g*N + c] = sum_k A[g][t][k] B[g](k, c), K-major A.
-// comp == 2: A rows hold [hi | lo] (length 2K) and both halves multiply the same B rows.
-// out_comp == 2: out rows hold [hi | lo] (length 2N), i.e. this phase produces an intermediate.
-blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A, int64_t n_tok, int64_t K,
-                      int64_t groups, int64_t N, const void* B, bool b_mn_major, void* out, int64_t out_ld,
-                      int comp = 1, int out_comp = 1) {
+// N tile: <= 256 columns, multiple of 16, balanced.  While the grid would leave SMs idle, split
+// N further (down to 64) -- but only toward a width whose B slice (K x BN) can stay resident,
+// since in streaming mode every extra N tile re-reads the whole A tile.
+int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int sms) {
+    int64_t tiles = cdiv(N, 256);
+    int bn = static_cast<int>(rup(cdiv(N, tiles), 16));
+    // split while the grid leaves SMs idle, but never past one wave (a partial second wave
+    // doubles the makespan of a latency-bound kernel)
+    while (bn > 64 && other_tiles * cdiv(N, bn) < sms) {
+        ++tiles;
+        const int nb = static_cast<int>(rup(cdiv(N, tiles), 16));
+        if (nb < 64 || other_tiles * cdiv(N, nb) > sms) break;
+        bn = nb;
+    }
+    if (K * bn * 2 > 112 * 1024) bn = static_cast<int>(rup(cdiv(N, cdiv(N, 256)), 16));
+    return bn;
+}
+
+struct OutMap {  // 4-D view (N, comp, groups, rows) of a GEMM phase's output
+    void* ptr;
+    int f32;               // 1: fp32 output (unrounded), else bf16
+    int64_t comp;          // 1, or 2 for a compensated [hi | lo] intermediate
+    int64_t comp_stride;   // elements between hi and lo
+    int64_t group_stride;  // elements between groups
+    int64_t row_stride;    // elements between rows
+};
+
+// One plain GEMM phase: out[g](t, c) = sum_k A[g](t, k) B[g](k, c), K-major A.
+//   A map: a_gmid ? (K*comp, groups, rows) : (K*comp, rows, groups) with the given strides.
+//   comp == 2: A rows hold [hi | lo] (lo at column offset K) multiplying the same B rows.
+blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A, int a_gmid, int64_t a_row_stride,
+                      int64_t a_group_stride, int64_t n_tok, int64_t K, int64_t groups, int64_t N, const void* B,
+                      bool b_mn_major, const OutMap& out, int comp) {
     KParams p = {};
     p.n_tok = static_cast<int>(n_tok);
     p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM));
-    p.BN = choose_bn(N);
+    p.BN = choose_bn(N, K, p.tiles_m * groups, d.sm_count);
     p.N = static_cast<int>(N);
     p.tiles_n = static_cast<int>(cdiv(N, p.BN));
     p.groups = static_cast<int>(groups);
@@ -179,19 +266,36 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     p.kb_half = static_cast<int>(cdiv(K, blr::BK));
     p.k_blocks = p.kb_half * comp;
     p.a_lo_off = comp == 2 ? static_cast<int>(K) : 0;
+    p.a_gmid = a_gmid;
     p.n_sub = 1;
     set_b_staging(p, b_mn_major);
-    p.out = static_cast<__nv_bfloat16*>(out);
-    p.out_ld = out_ld * out_comp;
-    p.out_lo_off = out_comp == 2 ? out_ld : 0;
-    if (!finish_plan(p)) return BLR_ERR_UNSUPPORTED;
+    p.out_lo_off = out.comp == 2 ? out.comp_stride : 0;
+    p.out_f32 = out.f32;
+    const int esz = out.f32 ? 4 : 2;
+    p.c_box_w = chunk_width(p.BN);
+    while (p.c_box_w * esz > 128) p.c_box_w /= 2;  // staged rows <= 128 B
+    const Swz cs = pick_swz(p.c_box_w * esz);
+    p.c_swz = cs.mask;
+    if (!finish_plan(p, true, 32 * p.c_box_w * esz)) return BLR_ERR_UNSUPPORTED;
 
-    CUtensorMap ta, tb;
+    CUtensorMap ta, tb, tc;
     {
-        const int64_t Ka = K * comp;  // A row length
-        const uint64_t dims[3] = {static_cast<uint64_t>(Ka), static_cast<uint64_t>(n_tok), static_cast<uint64_t>(groups)};
-        const uint64_t str[2] = {static_cast<uint64_t>(Ka) * 2, static_cast<uint64_t>(Ka * n_tok) * 2};
-        const uint32_t box[3] = {blr::BK, blr::BM, 1};
+        const int64_t Ka = K * comp;  // A row length actually stored
+        uint64_t dims[3], str[2];
+        dims[0] = static_cast<uint64_t>(Ka);
+        if (a_gmid) {
+            dims[1] = static_cast<uint64_t>(groups);
+            dims[2] = static_cast<uint64_t>(n_tok);
+            str[0] = static_cast<uint64_t>(a_group_stride) * 2;
+            str[1] = static_cast<uint64_t>(a_row_stride) * 2;
+        } else {
+            dims[1] = static_cast<uint64_t>(n_tok);
+            dims[2] = static_cast<uint64_t>(groups);
+            str[0] = static_cast<uint64_t>(a_row_stride) * 2;
+            str[1] = static_cast<uint64_t>(a_group_stride > 0 ? a_group_stride : a_row_stride * n_tok) * 2;
+        }
+        const uint32_t box[3] = {static_cast<uint32_t>(blr::BK), a_gmid ? 1u : static_cast<uint32_t>(blr::BM),
+                                 a_gmid ? static_cast<uint32_t>(blr::BM) : 1u};
         if (!encode(&ta, A, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
     }
     if (b_mn_major) {
@@ -205,7 +309,17 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
         const uint32_t box[3] = {blr::BK, static_cast<uint32_t>(p.BN), 1};
         if (!encode(&tb, B, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
     }
-    return launch<blr::KIND_GEMM>(ta, tb, p, d, dev, st);
+    {
+        const uint64_t dims[4] = {static_cast<uint64_t>(N), static_cast<uint64_t>(out.comp),
+                                  static_cast<uint64_t>(groups), static_cast<uint64_t>(n_tok)};
+        const uint64_t str[3] = {static_cast<uint64_t>(out.comp_stride) * 2, static_cast<uint64_t>(out.group_stride) * 2,
+                                 static_cast<uint64_t>(out.row_stride) * 2};
+        const uint64_t es = static_cast<uint64_t>(esz);
+        const uint64_t strb[3] = {str[0] / 2 * es, str[1] / 2 * es, str[2] / 2 * es};
+        const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32};
+        if (!encode(&tc, out.ptr, 4, dims, strb, box, cs.mode, out.f32 != 0)) return BLR_ERR_CUDA;
+    }
+    return launch<blr::KIND_GEMM>(ta, tb, tc, p, d, dev, st);
 }
 
 // X viewed as [n_tok][b1][p] (A operand of the block-diagonal first stage).
@@ -214,6 +328,12 @@ bool encode_x_blocked(CUtensorMap* m, const void* X, int64_t n_tok, int64_t b1, 
     const uint64_t str[2] = {static_cast<uint64_t>(pdim) * 2, static_cast<uint64_t>(pdim * b1) * 2};
     const uint32_t box[3] = {blr::BK, 1, blr::BM};
     return encode(m, X, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+size_t blast_ws_bytes(int64_t n_tok, int64_t b1, int64_t b2, int64_t r) {
+    const size_t zpp = static_cast<size_t>(b2) * n_tok * r * 2 * comp_factor(r);
+    if (blast_fused(b1, r)) return zpp;
+    return zpp + static_cast<size_t>(b1) * n_tok * r * 4;  // + fp32 Z_l of the separate S1
 }
 
 }  // namespace
@@ -234,7 +354,7 @@ const char* blr_status_string(blr_status s) {
     return "BLR_ERR_UNKNOWN";
 }
 
-const char* blr_version(void) { return "0.1.0"; }
+const char* blr_version(void) { return "0.2.0"; }
 
 int blr_last_launch_count(void) { return t_last_launches; }
 
@@ -252,6 +372,9 @@ int blr_profile_end(void) {
     return n;
 }
 
+// Debug (not in blr.h's stable surface): per-CTA timestamps of the next GEMM-kernel launches.
+void blr_debug_trace(unsigned long long* device_buf) { t_trace = device_buf; }
+
 void blr_clear_cache(void) {
     std::lock_guard<std::mutex> lk(g_mu);
     for (auto& d : g_dev) d = DevInfo();
@@ -266,8 +389,8 @@ size_t blr_monarch_workspace_size(int64_t n_tok, int64_t, int64_t, int64_t b1, i
                ? static_cast<size_t>(b2) * n_tok * b1 * r_blk * 2 * comp_factor(b1 * r_blk)
                : 0;
 }
-size_t blr_blast_workspace_size(int64_t n_tok, int64_t, int64_t, int64_t, int64_t b2, int64_t r) {
-    return (n_tok > 0 && b2 > 0 && r > 0) ? static_cast<size_t>(b2) * n_tok * r * 2 * comp_factor(r) : 0;
+size_t blr_blast_workspace_size(int64_t n_tok, int64_t, int64_t, int64_t b1, int64_t b2, int64_t r) {
+    return (n_tok > 0 && b1 > 0 && b2 > 0 && r > 0) ? blast_ws_bytes(n_tok, b1, b2, r) : 0;
 }
 
 blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t r,
@@ -287,11 +410,13 @@ blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int comp = comp_factor(r);
-    // S1: Z = X V (V is [d_in][r]: MN-major B)
-    s = gemm_phase(d, dev, st, X, n_tok, d_in, 1, r, V, true, workspace, r, 1, comp);
+    // S1: Z = X V  (V is [d_in][r]: MN-major B); Z rows [hi | lo] when compensated
+    s = gemm_phase(d, dev, st, X, 0, d_in, 0, n_tok, d_in, 1, r, V, true,
+                   OutMap{workspace, 0, comp, r, r, r * comp}, 1);
     if (s != BLR_OK) return s;
-    // S3: Y = Z U (U is [r][d_out]: MN-major B)
-    return gemm_phase(d, dev, st, workspace, n_tok, r, 1, d_out, U, true, Y, d_out, comp, 1);
+    // S3: Y = Z U  (U is [r][d_out]: MN-major B)
+    return gemm_phase(d, dev, st, workspace, 0, r * comp, 0, n_tok, r, 1, d_out, U, true,
+                      OutMap{Y, 0, 1, d_out, d_out, d_out}, comp);
 }
 
 blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
@@ -319,28 +444,34 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     // ---- phase 1: Z'[k][t][l r' + rho] = (X_l V_{l,k})[t, rho]  (block-diagonal S1 + permutations)
     {
         KParams p = {};
+        p.n_tok = static_cast<int>(n_tok);
+        p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM));
+        // k blocks per N tile: BN = kb r' <= 256 and a multiple of 16; fewer while SMs would idle
         int kb = std::max<int>(1, std::min<int>(static_cast<int>(b2), 256 / static_cast<int>(r_blk)));
         while (kb > 1 && (kb * r_blk) % 16) --kb;
         if ((kb * r_blk) % 16) kb = 2;  // r' odd multiple of 8: pair two k blocks
+        while (kb > 2 && p.tiles_m * b1 * cdiv(b2, kb) < d.sm_count) {
+            int nk = kb - 1;
+            while (nk > 1 && (nk * r_blk) % 16) --nk;
+            if ((nk * r_blk) % 16 || nk * r_blk < 64) break;
+            kb = nk;
+        }
         p.kb_per_tile = kb;
         p.BN = static_cast<int>(kb * r_blk);
         p.N = static_cast<int>(r_blk * b2);
-        p.n_tok = static_cast<int>(n_tok);
-        p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM));
         p.tiles_n = static_cast<int>(cdiv(b2, kb));
         p.groups = static_cast<int>(b1);
         p.total_tiles = p.tiles_m * p.groups * p.tiles_n;
         p.k_blocks = p.kb_half = static_cast<int>(cdiv(pdim, blr::BK));
         p.n_sub = 1;
         set_b_staging(p, false);
-        p.out = static_cast<__nv_bfloat16*>(workspace);
         p.r_blk = static_cast<int>(r_blk);
-        p.b1 = static_cast<int>(b1);
-        p.b2 = static_cast<int>(b2);
-        p.out_ld = K2 * comp;
         p.out_lo_off = comp == 2 ? K2 : 0;
-        if (p.BN > 256 || !finish_plan(p)) return BLR_ERR_UNSUPPORTED;
-        CUtensorMap ta, tb;
+        p.c_box_w = chunk_width(static_cast<int>(r_blk));
+        const Swz cs = pick_swz(p.c_box_w * 2);
+        p.c_swz = cs.mask;
+        if (p.BN > 256 || !finish_plan(p, true, 32 * p.c_box_w * 2)) return BLR_ERR_UNSUPPORTED;
+        CUtensorMap ta, tb, tc;
         if (!encode_x_blocked(&ta, X, n_tok, b1, pdim)) return BLR_ERR_CUDA;
         // V viewed 4-D (a, rho', k, l) so the box (64, r', kb, 1) lands k-major in smem:
         // this is where the r' <-> b2 permutation of PAPER.md L194 happens (no extra pass).
@@ -357,11 +488,19 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         str[2] = static_cast<uint64_t>(r_blk * b2 * pdim) * 2;
         const uint32_t box[4] = {blr::BK, static_cast<uint32_t>(r_blk), static_cast<uint32_t>(kb), 1};
         if (!encode(&tb, V, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
-        s = launch<blr::KIND_MONARCH_PROJ>(ta, tb, p, d, dev, st);
+        // Z' viewed (rho', l, comp, t, k): element at ((k*n + t)*comp + part)*K2 + l*r' + rho'
+        const uint64_t cd[5] = {static_cast<uint64_t>(r_blk), static_cast<uint64_t>(b1), static_cast<uint64_t>(comp),
+                                static_cast<uint64_t>(n_tok), static_cast<uint64_t>(b2)};
+        const uint64_t cstr[4] = {static_cast<uint64_t>(r_blk) * 2, static_cast<uint64_t>(K2) * 2,
+                                  static_cast<uint64_t>(K2 * comp) * 2, static_cast<uint64_t>(K2 * comp * n_tok) * 2};
+        const uint32_t cbox[5] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32, 1};
+        if (!encode(&tc, workspace, 5, cd, cstr, cbox, cs.mode)) return BLR_ERR_CUDA;
+        s = launch<blr::KIND_MONARCH_PROJ>(ta, tb, tc, p, d, dev, st);
         if (s != BLR_OK) return s;
     }
     // ---- phase 2: Y[t, k q + c] = sum_kk Z'[k][t][kk] U[k][c][kk]  (U is [N][K]: K-major B)
-    return gemm_phase(d, dev, st, workspace, n_tok, K2, b2, qdim, U, false, Y, d_out, comp, 1);
+    return gemm_phase(d, dev, st, workspace, 0, K2 * comp, n_tok * K2 * comp, n_tok, K2, b2, qdim, U, false,
+                      OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
 }
 
 blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
@@ -383,13 +522,16 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int comp = comp_factor(r);
+    void* zpp = workspace;  // Z'' [b2][n][r*comp]
 
-    // ---- phase 1: Z''[k][t][rho] = sum_l S[l,k,rho] (X_l V_l)[t, rho]  (S1 on tcgen05, S2 fused)
-    {
+    if (blast_fused(b1, r)) {
+        // ---- phase 1: Z''[k][t][rho] = sum_l S[l,k,rho] (X_l V_l)[t, rho]  (S1 on tcgen05, S2 fused)
         KParams p = {};
-        int R = 256;
-        while (R > 16 && b1 * R > blr::TMEM_COLS) R >>= 1;
-        R = static_cast<int>(std::min<int64_t>(R, rup(r, 16)));
+        // rho-chunk R: b1 TMEM accumulators of R columns, and b2 staged outputs of R/2 columns per
+        // warp (<= 16 KB): b1*R <= 512, b2*R <= 512, R <= 128.
+        int R = 128;
+        while (R > 16 && (b1 * R > blr::TMEM_COLS || b2 * R > 512)) R >>= 1;
+        while (R > 16 && R / 2 >= rup(r, 16)) R >>= 1;
         p.BN = R;
         p.N = static_cast<int>(r);
         p.n_tok = static_cast<int>(n_tok);
@@ -400,25 +542,91 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         p.k_blocks = p.kb_half = static_cast<int>(cdiv(pdim, blr::BK));
         p.n_sub = static_cast<int>(b1);
         set_b_staging(p, true);
-        p.out = static_cast<__nv_bfloat16*>(workspace);
-        p.out_ld = r * comp;
-        p.out_lo_off = comp == 2 ? r : 0;
         p.b1 = static_cast<int>(b1);
         p.b2 = static_cast<int>(b2);
         p.r = static_cast<int>(r);
         p.S = static_cast<const __nv_bfloat16*>(S);
-        if (!finish_plan(p)) return BLR_ERR_UNSUPPORTED;
-        CUtensorMap ta, tb;
+        p.out_lo_off = comp == 2 ? r : 0;
+        p.c_box_w = R / 2;
+        p.c_swz = pick_swz(R).mask;
+        p.stage_warp_bytes = static_cast<uint32_t>(b2) * 32u * (R / 2) * 2u;
+        if (!finish_plan(p, false, 0)) return BLR_ERR_UNSUPPORTED;
+        CUtensorMap ta, tb, tc;
         if (!encode_x_blocked(&ta, X, n_tok, b1, pdim)) return BLR_ERR_CUDA;
         const uint64_t dims[3] = {static_cast<uint64_t>(r), static_cast<uint64_t>(pdim), static_cast<uint64_t>(b1)};
         const uint64_t str[2] = {static_cast<uint64_t>(r) * 2, static_cast<uint64_t>(r * pdim) * 2};
         const uint32_t box[3] = {64, blr::BK, 1};
         if (!encode(&tb, V, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
-        s = launch<blr::KIND_BLAST_PROJ>(ta, tb, p, d, dev, st);
+        // Z'' viewed (rho, comp, t, k): element at ((k*n + t)*comp + part)*r + rho
+        const uint64_t cd[4] = {static_cast<uint64_t>(r), static_cast<uint64_t>(comp), static_cast<uint64_t>(n_tok),
+                                static_cast<uint64_t>(b2)};
+        const uint64_t cstr[3] = {static_cast<uint64_t>(r) * 2, static_cast<uint64_t>(r * comp) * 2,
+                                  static_cast<uint64_t>(r * comp * n_tok) * 2};
+        const uint32_t cbox[4] = {static_cast<uint32_t>(R / 2), 1, 32, 1};
+        if (!encode(&tc, zpp, 4, cd, cstr, cbox, pick_swz(R).mode)) return BLR_ERR_CUDA;
+        s = launch<blr::KIND_BLAST_PROJ>(ta, tb, tc, p, d, dev, st);
         if (s != BLR_OK) return s;
+    } else {
+        // ---- S1: Z[l][t][rho] = (X_l V_l)[t, rho]  -- grouped GEMM over l (A = X viewed (p, b1, n))
+        void* zl = static_cast<char*>(workspace) + static_cast<size_t>(b2) * n_tok * r * 2 * comp;
+        s = gemm_phase(d, dev, st, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true,
+                       OutMap{zl, 1, 1, r, n_tok * r, r}, 1);
+        if (s != BLR_OK) return s;
+        // ---- S2: Z''[k][t][rho] = sum_l S[l,k,rho] Z[l][t][rho]
+        const auto* zb = static_cast<const float*>(zl);
+        const auto* sb = static_cast<const __nv_bfloat16*>(S);
+        auto* ob = static_cast<__nv_bfloat16*>(zpp);
+        const int in = static_cast<int>(n_tok), ib1 = static_cast<int>(b1), ib2 = static_cast<int>(b2),
+                  ir = static_cast<int>(r);
+        cudaLaunchConfig_t cfg = {};
+        // rows per block: ~2 resident blocks per SM over the whole grid, multiple of 16
+        const int64_t chunks = cdiv(r, 64);
+        const int64_t target_blocks = 2LL * d.sm_count;
+        const int rpb = static_cast<int>(std::max<int64_t>(blr::S2_ROWS,
+                                          rup(cdiv(n_tok * chunks, target_blocks), blr::S2_ROWS)));
+        cfg.gridDim = dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(cdiv(n_tok, rpb)));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = static_cast<size_t>(b1 * b2 * 64 * 4 + 2 * b1 * 256 * 16);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+        if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess)
+            return BLR_ERR_CUDA;
+        {
+            std::lock_guard<std::mutex> lk(g_mu);
+            if (!g_attr_set[3][dev]) {
+                const int mx = 16 * 16 * 64 * 4 + 2 * 16 * 256 * 16;
+                if (cudaFuncSetAttribute(blr::blast_s2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess)
+                    return BLR_ERR_CUDA;
+                g_attr_set[3][dev] = true;
+            }
+        }
+        cudaError_t le;
+        const int64_t bmax = std::max(b1, b2);
+        if (bmax <= 4)
+            le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<4>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb);
+        else if (bmax <= 8)
+            le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<8>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb);
+        else
+            le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<16>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb);
+        if (le != cudaSuccess) return BLR_ERR_CUDA;
+        if (cudaGetLastError() != cudaSuccess) return BLR_ERR_CUDA;
+        if (prof) {
+            if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess)
+                return BLR_ERR_CUDA;
+            ++t_prof_n;
+        }
+        ++t_last_launches;
     }
-    // ---- phase 2: Y_k = Z''_k U_k  (U is [b2][r][q]: MN-major B)
-    return gemm_phase(d, dev, st, workspace, n_tok, r, b2, qdim, U, true, Y, d_out, comp, 1);
+    // ---- S3: Y_k = Z''_k U_k  (U is [b2][r][q]: MN-major B)
+    return gemm_phase(d, dev, st, zpp, 0, r * comp, n_tok * r * comp, n_tok, r, b2, qdim, U, true,
+                      OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
 }
 
 }  // extern "C"

@@ -1,22 +1,27 @@
 // blr_kernels.cuh -- the sm_100a kernels of the BLR prefill forward (arXiv 2512.20861).
 //
-// One warp-specialized, persistent tcgen05 GEMM kernel template, instantiated for the two
-// phases of every format:
+// One warp-specialized, persistent tcgen05 GEMM kernel template, instantiated for the phases of
+// every format:
 //
-//   PROJ  (stage S1, and S2 for BLAST):  per token tile T of 128 rows
-//     lowrank : Z[t, rho]            = X[t,:] V[:, rho]
-//     monarch : Z'[k][t][l r' + rho] = (X_l V_{l,k})[t, rho]
-//               -- the r'<->b2 and b2<->b1 permutations are folded into a 4-D TMA box over V
-//                  (rows delivered k-major) and into the epilogue's store address.
-//     blast   : Z''[k][t][rho]       = sum_l S[l,k,rho] (X_l V_l)[t, rho]
-//               -- b1 accumulators (one per l) live side by side in TMEM; the epilogue warps
-//                  apply the S-weighted block sum on fp32 CUDA cores and round once to bf16.
-//   EXPAND (stage S3):                    Y[t, k q + c] = sum_kk Z_k[t, kk] U_k[kk, c]
+//   KIND_GEMM          out[g](t, c) = sum_kk A[g](t, kk) B[g](kk, c)        grouped GEMM
+//       lowrank S1: Z = X V, S3: Y = Z U
+//       Monarch S3: Y_k = Z'_k U_k^T
+//       BLAST   S1: Z_l = X_l V_l (grouped over l), S3: Y_k = Z''_k U_k
+//   KIND_MONARCH_PROJ  Z'[k][t][l r' + rho] = (X_l V_{l,k})[t, rho]
+//       the r'<->b2 and b2<->b1 permutations of PAPER.md L194 are folded into a 4-D TMA box
+//       over V (N rows delivered k-major whatever V's layout) and into the store coordinates.
+//   KIND_BLAST_PROJ    Z''[k][t][rho] = sum_l S[l,k,rho] (X_l V_l)[t, rho]
+//       b1 accumulators side by side in TMEM; the epilogue applies the S-weighted block sum with
+//       packed fp32x2 FMAs (used when b1 * r fits TMEM; else BLAST runs S1/S2/S3 separately).
 //
 // Roles: warp 0 = TMA producer (1 thread), warp 1 = TMEM allocator + MMA issuer (1 thread),
-// warps 2..9 = epilogue (two warps per TMEM lane quarter).  Operands stream through a
-// STAGES-deep smem ring guarded by full/empty mbarriers; accumulators are double-buffered in
-// TMEM when two fit in 512 columns, so the epilogue of tile j overlaps the MMAs of tile j+1.
+// warps 2..9 = epilogue (two warps per TMEM lane quarter, each half of the tile's columns).
+// A streams through a STAGES-deep smem ring (full/empty mbarriers).  B either streams through
+// the same ring, or -- "weight-stationary" mode -- is loaded once per (group, N-block) slice into
+// a resident smem region while the CTA walks a contiguous run of token tiles, so per-SM ingress
+// is only the activations (the per-SM TMA ingress is ~63 B/clk, benchmarks/micro).  TMEM
+// accumulators are double-buffered when two fit in 512 columns.  Epilogue: tcgen05.ld ->
+// bf16 (RNE) -> 128B-swizzled smem staging -> TMA bulk tensor store (full lines, OOB clipped).
 #pragma once
 #include "ptx.cuh"
 
@@ -29,6 +34,7 @@ constexpr int NUM_EPI_WARPS = 8;
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;
 constexpr int TMEM_COLS = 512;
 constexpr int MAX_STAGES = 8;
+constexpr int MAX_BRES = 48;       // max resident B k-blocks (one mbarrier each)
 
 enum Kind : int { KIND_GEMM = 0, KIND_MONARCH_PROJ = 1, KIND_BLAST_PROJ = 2 };
 
@@ -44,66 +50,104 @@ struct KParams {
     int k_blocks;     // K blocks per sub-GEMM (2x when the A operand is compensated hi|lo)
     int kb_half;      // K blocks per part: blocks >= kb_half read the lo half of A
     int a_lo_off;     // column offset of the lo half inside A's rows (0: not compensated)
+    int a_gmid;       // A map coordinate order: 0 = (k, t, g), 1 = (k, g, t)
+    int kbox;         // 64-wide K blocks per pipeline stage (1 or 2; 2 halves the handshakes)
     int n_sub;        // sub-GEMMs accumulated into separate TMEM slots (BLAST proj: b1)
     int stages;       // smem ring depth
     int acc_bufs;     // TMEM accumulator buffers (1 or 2)
+    int b_resident;   // 1: B slice resident in smem per (group, N-block) (weight-stationary)
     // ---- B operand staging
     int b_mn_major;      // 1: B stored [K][N] (N contiguous), 0: B stored [N][K]
-    int b_boxes;         // TMA boxes per stage for B (MN-major with BN > 64)
+    int b_boxes;         // TMA boxes per k-block for B (MN-major)
     int b_box_n;         // N elements per box (MN-major)
-    uint32_t b_stage_bytes;
+    uint32_t b_stage_bytes;  // bytes of one B k-block in smem
     uint32_t b_lbo, b_sbo, b_layout, b_kstep;  // UMMA descriptor parameters for B
     // ---- epilogue
-    __nv_bfloat16* out;  // Y (GEMM), Z' (Monarch proj), Z'' (BLAST proj)
-    long long out_ld;    // row pitch of out in elements
-    long long out_lo_off;  // >0: also store lo = bf16(z - bf16(z)) at +out_lo_off (compensated)
-    int r_blk;           // Monarch: r'
-    int kb_per_tile;     // Monarch: output blocks k per N tile
-    int b1, b2;          // Monarch / BLAST block counts
-    int r;               // BLAST: rank
+    long long out_lo_off;  // >0: also store lo = bf16(z - bf16(z)) (compensated intermediate)
+    int c_box_w;           // staged store chunk width (elements)
+    uint32_t c_swz;        // staging swizzle mask (7: 128 B, 3: 64 B, 1: 32 B, 0: none) = TMA map's
+    uint32_t stage_warp_bytes;  // staging bytes per epilogue warp
+    int stage_bufs;        // staging buffers per warp (GEMM / Monarch kinds)
+    int out_f32;           // GEMM kind: store fp32 (no rounding; BLAST split-path S1 output)
+    int r_blk;             // Monarch: r'
+    int kb_per_tile;       // Monarch: output blocks k per N tile
+    int b1, b2;            // BLAST block counts
+    int r;                 // BLAST: rank
     const __nv_bfloat16* S;  // BLAST: S [b1][b2][r]
+    unsigned long long* trace;  // debug: per-CTA %globaltimer stamps [grid][8] (nullptr = off)
 };
 
 struct SmemLayout {
-    uint32_t a_off, b_off, s_off, bar_off, total;
+    uint32_t a_off, b_off, c_off, s_off, bar_off, total;
 };
+
+__host__ __device__ inline int kb_resident(const KParams& p) {  // resident B blocks (padded to kbox)
+    return (p.kb_half + p.kbox - 1) / p.kbox * p.kbox;
+}
+__host__ __device__ inline uint32_t b_region_bytes(const KParams& p) {
+    return p.b_resident ? p.b_stage_bytes * kb_resident(p) : p.b_stage_bytes * p.kbox * p.stages;
+}
 
 __host__ __device__ inline SmemLayout smem_layout(const KParams& p) {
     SmemLayout L;
-    const uint32_t a_stage = BM * BK * 2;
+    const uint32_t a_stage = BM * BK * 2 * p.kbox;
     L.a_off = 0;
     L.b_off = L.a_off + a_stage * p.stages;
-    L.s_off = L.b_off + p.b_stage_bytes * p.stages;
+    L.c_off = L.b_off + b_region_bytes(p);  // all multiples of 1024
+    L.s_off = L.c_off + p.stage_warp_bytes * NUM_EPI_WARPS;
     uint32_t s_bytes = 0;
-    if (p.b1 > 0 && p.b2 > 0 && p.S != nullptr) s_bytes = p.b1 * p.b2 * p.BN * 4;
+    if (p.S != nullptr) s_bytes = p.b1 * p.b2 * p.BN * 4;
     L.bar_off = (L.s_off + s_bytes + 15) & ~15u;
-    L.total = L.bar_off + 8 * (2 * MAX_STAGES + 4) + 16;
+    L.total = L.bar_off + 8 * (2 * MAX_STAGES + 6 + MAX_BRES) + 16;
     return L;
 }
 
-// Tile index -> (m block, group, n block); n block fastest so consecutive tiles share A.
+// ---------------------------------------------------------------------------- tile schedule ----
+// Streaming mode: round-robin tiles, n block fastest (consecutive tiles share the A tile in L2).
+// Weight-stationary mode: tiles ordered slice-major (slice = (g, n block)), token tile fastest,
+// and each CTA takes one contiguous run, so it reloads B only when its run crosses a slice.
 struct TileCoord {
-    int m_blk, g, n_blk;
+    int m_blk, g, n_blk, slice;
 };
 __device__ __forceinline__ TileCoord tile_coord(const KParams& p, int tile) {
     TileCoord c;
-    c.n_blk = tile % p.tiles_n;
-    const int rest = tile / p.tiles_n;
-    c.g = rest % p.groups;
-    c.m_blk = rest / p.groups;
+    if (p.b_resident) {
+        c.m_blk = tile % p.tiles_m;
+        c.slice = tile / p.tiles_m;
+        c.g = c.slice / p.tiles_n;
+        c.n_blk = c.slice % p.tiles_n;
+    } else {
+        c.n_blk = tile % p.tiles_n;
+        const int rest = tile / p.tiles_n;
+        c.g = rest % p.groups;
+        c.m_blk = rest / p.groups;
+        c.slice = -1;
+    }
     return c;
 }
+__device__ __forceinline__ void tile_range(const KParams& p, int& first, int& last, int& step) {
+    if (p.b_resident) {
+        first = static_cast<int>((static_cast<long long>(blockIdx.x) * p.total_tiles) / gridDim.x);
+        last = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * p.total_tiles) / gridDim.x);
+        step = 1;
+    } else {
+        first = blockIdx.x;
+        last = p.total_tiles;
+        step = gridDim.x;
+    }
+}
 
-// Store 8 fp32 values as bf16 (RNE); with lo_off > 0 also store the residual bf16(v - bf16(v))
-// at dst + lo_off (compensated intermediate for short S3 contractions).
-__device__ __forceinline__ void store8(__nv_bfloat16* dst, const float (&f)[8], long long lo_off) {
+// Stage 8 fp32 values (one 16-B chunk `chunk` of row `row`) as bf16 RNE into a row-major staging
+// tile whose rows are `row_bytes` long, applying the TMA swizzle (16-B chunk index XOR address
+// bits [7, 7+log2(mask+1)) ).  part 1 stages the compensation term lo = bf16(v - bf16(v)).
+__device__ __forceinline__ void stage_row8(uint32_t buf, int row, int chunk, uint32_t row_bytes, uint32_t swz,
+                                           const float (&f)[8], int part) {
     uint4 w;
     w.x = ptx::pack_bf16x2(f[0], f[1]);
     w.y = ptx::pack_bf16x2(f[2], f[3]);
     w.z = ptx::pack_bf16x2(f[4], f[5]);
     w.w = ptx::pack_bf16x2(f[6], f[7]);
-    *reinterpret_cast<uint4*>(dst) = w;
-    if (lo_off > 0) {
+    if (part) {
         const uint32_t hw[4] = {w.x, w.y, w.z, w.w};
         float r[8];
 #pragma unroll
@@ -111,19 +155,36 @@ __device__ __forceinline__ void store8(__nv_bfloat16* dst, const float (&f)[8], 
             r[2 * e] = f[2 * e] - __uint_as_float(hw[e] << 16);
             r[2 * e + 1] = f[2 * e + 1] - __uint_as_float(hw[e] & 0xFFFF0000u);
         }
-        uint4 l;
-        l.x = ptx::pack_bf16x2(r[0], r[1]);
-        l.y = ptx::pack_bf16x2(r[2], r[3]);
-        l.z = ptx::pack_bf16x2(r[4], r[5]);
-        l.w = ptx::pack_bf16x2(r[6], r[7]);
-        *reinterpret_cast<uint4*>(dst + lo_off) = l;
+        w.x = ptx::pack_bf16x2(r[0], r[1]);
+        w.y = ptx::pack_bf16x2(r[2], r[3]);
+        w.z = ptx::pack_bf16x2(r[4], r[5]);
+        w.w = ptx::pack_bf16x2(r[6], r[7]);
+    }
+    uint32_t off = row * row_bytes + chunk * 16;
+    off ^= ((off >> 7) & swz) << 4;
+    ptx::st_shared_v4(buf + off, w);
+}
+
+// Stage 8 fp32 values unrounded (two 16-B chunks 2*chunk8, 2*chunk8+1 of row `row`).
+__device__ __forceinline__ void stage_row8_f32(uint32_t buf, int row, int chunk8, uint32_t row_bytes, uint32_t swz,
+                                               const float (&f)[8]) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint4 w;
+        w.x = __float_as_uint(f[4 * h + 0]);
+        w.y = __float_as_uint(f[4 * h + 1]);
+        w.z = __float_as_uint(f[4 * h + 2]);
+        w.w = __float_as_uint(f[4 * h + 3]);
+        uint32_t off = row * row_bytes + (2 * chunk8 + h) * 16;
+        off ^= ((off >> 7) & swz) << 4;
+        ptx::st_shared_v4(buf + off, w);
     }
 }
 
 template <int KIND>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     blr_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const KParams p) {
+                    const __grid_constant__ CUtensorMap tmC, const KParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the 128-B swizzle atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -137,10 +198,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t empty_bar = full_bar + 8 * MAX_STAGES;
     const uint32_t tfull_bar = empty_bar + 8 * MAX_STAGES;
     const uint32_t tempty_bar = tfull_bar + 16;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.bar_off + 8 * (2 * MAX_STAGES + 4));
+    const uint32_t bfree_bar = tempty_bar + 16;   // MMAs done reading the resident B
+    const uint32_t bfull_bar = bfree_bar + 16;    // [MAX_BRES]: resident B k-block kb landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + L.bar_off + 8 * (2 * MAX_STAGES + 6 + MAX_BRES));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 8 : nullptr;
+    if (trace && threadIdx.x == 0) trace[0] = ptx::globaltimer();
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
@@ -151,9 +216,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::mbar_init(tfull_bar + 8 * b, 1);
             ptx::mbar_init(tempty_bar + 8 * b, NUM_EPI_WARPS);
         }
+        for (int kb = 0; kb < MAX_BRES; ++kb) ptx::mbar_init(bfull_bar + 8 * kb, 1);
+        ptx::mbar_init(bfree_bar, 1);
         ptx::fence_barrier_init();
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
+        ptx::prefetch_tmap(&tmC);
     }
     if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(ptx::smem_u32(tmem_slot));
     ptx::tc_fence_before();
@@ -161,50 +229,98 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t acc_stride = static_cast<uint32_t>(p.n_sub * p.BN);  // columns per buffer
+    if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
+    // Programmatic dependent launch: everything above overlapped the previous kernel's tail.
+    // Roles that read the previous kernel's output (producer: A) or write outputs it may still
+    // read (epilogue) call griddep_wait() first; the producer prefetches the resident weight
+    // slice -- never written by a previous kernel -- before waiting.
+    ptx::griddep_launch_dependents();
+    int first, last, step;
+    tile_range(p, first, last, step);
 
     if (warp == 0) {
         // ===================================================== TMA producer =================
         if (lane == 0) {
-            const uint32_t a_bytes = BM * BK * 2;
-            const uint32_t tx = a_bytes + (p.b_mn_major ? p.b_boxes * p.b_box_n * BK * 2
-                                                        : static_cast<uint32_t>(p.BN) * BK * 2);
+            const uint32_t a_blk = BM * BK * 2;  // one 64-wide K block of A (16 KB)
+            const uint32_t b_bytes = p.b_mn_major ? p.b_boxes * p.b_box_n * BK * 2
+                                                  : static_cast<uint32_t>(p.BN) * BK * 2;
+            const uint32_t tx = p.kbox * (a_blk + (p.b_resident ? 0u : b_bytes));
+            const int n_steps = (p.k_blocks + p.kbox - 1) / p.kbox;
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+            int cur_slice = -1;
+            uint32_t nslices = 0;
+            bool waited = false;
+            for (int tile = first; tile < last; tile += step) {
                 const TileCoord tc = tile_coord(p, tile);
                 const int m0 = tc.m_blk * BM;
                 const int n0 = tc.n_blk * p.BN;
+                if (p.b_resident && tc.slice != cur_slice) {
+                    // (re)load the weight slice once for the contiguous run of token tiles
+                    if (nslices > 0) ptx::mbar_wait(bfree_bar, (nslices - 1) & 1);
+                    const int kbr = kb_resident(p);
+                    for (int kb = 0; kb < kbr; ++kb) {
+                        const uint32_t b_dst = b_base + kb * p.b_stage_bytes;
+                        const uint32_t bb = bfull_bar + 8 * kb;  // per-block barrier: MMA starts early
+                        ptx::mbar_arrive_expect_tx(bb, b_bytes);
+                        const int k0 = kb * BK;
+                        if constexpr (KIND == KIND_MONARCH_PROJ) {
+                            ptx::tma_load_4d(b_dst, &tmB, bb, k0, 0, tc.n_blk * p.kb_per_tile, tc.g);
+                        } else if (p.b_mn_major) {
+                            for (int j = 0; j < p.b_boxes; ++j)
+                                ptx::tma_load_3d(b_dst + j * (p.b_box_n * BK * 2), &tmB, bb,
+                                                 n0 + j * p.b_box_n, k0, tc.g);
+                        } else {
+                            ptx::tma_load_3d(b_dst, &tmB, bb, k0, n0, tc.g);
+                        }
+                    }
+                    cur_slice = tc.slice;
+                    ++nslices;
+                }
+                if (!waited) {
+                    ptx::griddep_wait();  // A (activations / intermediate) comes from the previous kernel
+                    waited = true;
+                    if (trace) trace[2] = ptx::globaltimer();
+                }
                 for (int sub = 0; sub < p.n_sub; ++sub) {
-                    for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    for (int si = 0; si < n_steps; ++si) {
                         ptx::mbar_wait(empty_bar + 8 * stage, phase ^ 1);
                         const uint32_t fb = full_bar + 8 * stage;
                         ptx::mbar_arrive_expect_tx(fb, tx);
-                        const uint32_t a_dst = a_base + stage * (BM * BK * 2);
-                        const uint32_t b_dst = b_base + stage * p.b_stage_bytes;
-                        const int k0 = kb * BK;
-                        if constexpr (KIND == KIND_GEMM) {
-                            // A = [groups][n_tok][K(|K)] ; B = [groups][K][N] (MN) or [groups][N][K]
-                            // Compensated A: blocks >= kb_half read the lo half against the same B rows.
-                            const int part = kb >= p.kb_half ? 1 : 0;
-                            const int kk0 = (kb - part * p.kb_half) * BK;
-                            ptx::tma_load_3d(a_dst, &tmA, fb, part * p.a_lo_off + kk0, m0, tc.g);
-                            if (p.b_mn_major) {
-                                for (int j = 0; j < p.b_boxes; ++j)
-                                    ptx::tma_load_3d(b_dst + j * (p.b_box_n * BK * 2), &tmB, fb,
-                                                     n0 + j * p.b_box_n, kk0, tc.g);
-                            } else {
-                                ptx::tma_load_3d(b_dst, &tmB, fb, kk0, n0, tc.g);
+                        const uint32_t a_st = a_base + stage * (a_blk * p.kbox);
+                        const uint32_t b_st = b_base + stage * (p.b_stage_bytes * p.kbox);
+                        for (int j = 0; j < p.kbox; ++j) {
+                            const int kb = si * p.kbox + j;
+                            const uint32_t a_dst = a_st + j * a_blk;
+                            const uint32_t b_dst = b_st + j * p.b_stage_bytes;
+                            // compensated A: blocks >= kb_half read the lo half against the same B rows
+                            const int part = (p.a_lo_off > 0 && kb >= p.kb_half) ? 1 : 0;
+                            const int k0 = (kb - part * p.kb_half) * BK;  // padded block: k0 >= K, zero-filled
+                            if constexpr (KIND == KIND_GEMM) {
+                                if (p.a_gmid)
+                                    ptx::tma_load_3d(a_dst, &tmA, fb, part * p.a_lo_off + k0, tc.g, m0);
+                                else
+                                    ptx::tma_load_3d(a_dst, &tmA, fb, part * p.a_lo_off + k0, m0, tc.g);
+                                if (!p.b_resident) {
+                                    if (p.b_mn_major) {
+                                        for (int q = 0; q < p.b_boxes; ++q)
+                                            ptx::tma_load_3d(b_dst + q * (p.b_box_n * BK * 2), &tmB, fb,
+                                                             n0 + q * p.b_box_n, k0, tc.g);
+                                    } else {
+                                        ptx::tma_load_3d(b_dst, &tmB, fb, k0, n0, tc.g);
+                                    }
+                                }
+                            } else if constexpr (KIND == KIND_MONARCH_PROJ) {
+                                // A = X viewed [n_tok][b1][p]; B = V viewed 4-D (a, rho', k, l)
+                                ptx::tma_load_3d(a_dst, &tmA, fb, k0, tc.g, m0);
+                                if (!p.b_resident)
+                                    ptx::tma_load_4d(b_dst, &tmB, fb, k0, 0, tc.n_blk * p.kb_per_tile, tc.g);
+                            } else {  // KIND_BLAST_PROJ: sub = l
+                                ptx::tma_load_3d(a_dst, &tmA, fb, k0, sub, m0);
+                                for (int q = 0; q < p.b_boxes; ++q)
+                                    ptx::tma_load_3d(b_dst + q * (p.b_box_n * BK * 2), &tmB, fb,
+                                                     n0 + q * p.b_box_n, k0, sub);
                             }
-                        } else if constexpr (KIND == KIND_MONARCH_PROJ) {
-                            // A = X viewed [n_tok][b1][p]; B = V viewed 4-D (a, rho', k, l):
-                            // rows of the N tile arrive k-major whatever V's composite order.
-                            ptx::tma_load_3d(a_dst, &tmA, fb, k0, tc.g, m0);
-                            ptx::tma_load_4d(b_dst, &tmB, fb, k0, 0, tc.n_blk * p.kb_per_tile, tc.g);
-                        } else {  // KIND_BLAST_PROJ: sub = l
-                            ptx::tma_load_3d(a_dst, &tmA, fb, k0, sub, m0);
-                            for (int j = 0; j < p.b_boxes; ++j)
-                                ptx::tma_load_3d(b_dst + j * (p.b_box_n * BK * 2), &tmB, fb,
-                                                 n0 + j * p.b_box_n, k0, sub);
                         }
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
@@ -215,47 +331,79 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ===================================================== MMA issuer ===================
         if (lane == 0) {
             const uint32_t idesc = ptx::idesc_bf16(BM, p.BN, p.b_mn_major);
+            // descriptors are built once; per-MMA only the 14-bit start-address field advances
+            const uint64_t a_desc0 = ptx::smem_desc(a_base, 16, 1024, ptx::LAYOUT_SW128);
+            const uint64_t b_desc0 = ptx::smem_desc(b_base, p.b_lbo, p.b_sbo, p.b_layout);
+            const uint32_t a_blk = BM * BK * 2;
+            const int n_steps = (p.k_blocks + p.kbox - 1) / p.kbox;
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+            int cur_slice = -1;
+            uint32_t nslices = 0;
+            for (int tile = first; tile < last; tile += step) {
+                const TileCoord tc = tile_coord(p, tile);
+                bool fresh = false;  // first tile of a new resident slice: wait per B block
+                if (p.b_resident && tc.slice != cur_slice) {
+                    cur_slice = tc.slice;
+                    ++nslices;
+                    fresh = true;
+                }
                 ptx::mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
                 ptx::tc_fence_after();
                 for (int sub = 0; sub < p.n_sub; ++sub) {
                     const uint32_t d_tmem = tmem_base + acc * acc_stride + sub * p.BN;
-                    for (int kb = 0; kb < p.k_blocks; ++kb) {
+                    for (int si = 0; si < n_steps; ++si) {
                         ptx::mbar_wait(full_bar + 8 * stage, phase);
                         ptx::tc_fence_after();
-                        const uint32_t a_s = a_base + stage * (BM * BK * 2);
-                        const uint32_t b_s = b_base + stage * p.b_stage_bytes;
+                        if (trace && trace[3] == 0) trace[3] = ptx::globaltimer();
+                        for (int j = 0; j < p.kbox; ++j) {
+                            const int kb = si * p.kbox + j;
+                            const int bkb = (p.a_lo_off > 0 && kb >= p.kb_half) ? kb - p.kb_half : kb;
+                            if (fresh && kb < kb_resident(p)) ptx::mbar_wait(bfull_bar + 8 * bkb, (nslices - 1) & 1);
+                            const uint32_t a_off = stage * (a_blk * p.kbox) + j * a_blk;
+                            const uint32_t b_off = p.b_resident ? bkb * p.b_stage_bytes
+                                                                : stage * (p.b_stage_bytes * p.kbox) + j * p.b_stage_bytes;
 #pragma unroll
-                        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-                            // A: K-major, 128-B swizzle, 8-row groups 1024 B apart; +32 B per K=16.
-                            const uint64_t ad = ptx::smem_desc(a_s + kk * 32, 16, 1024, ptx::LAYOUT_SW128);
-                            const uint64_t bd = ptx::smem_desc(b_s + kk * p.b_kstep, p.b_lbo, p.b_sbo, p.b_layout);
-                            ptx::mma_bf16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                            for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                                // A: K-major, 128-B swizzle, 8-row groups 1024 B apart; +32 B per K=16.
+                                const uint64_t ad = a_desc0 + ((a_off + kk * 32) >> 4);
+                                const uint64_t bd = b_desc0 + ((b_off + kk * p.b_kstep) >> 4);
+                                ptx::mma_bf16(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
+                            }
                         }
                         ptx::mma_commit(empty_bar + 8 * stage);  // frees the smem slot
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
                 }
                 ptx::mma_commit(tfull_bar + 8 * acc);  // accumulator ready for the epilogue
+                if (trace) trace[4] = ptx::globaltimer();
                 if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
+                if (p.b_resident) {
+                    const int nt = tile + step;
+                    if (nt >= last || tile_coord(p, nt).slice != cur_slice) ptx::mma_commit(bfree_bar);
+                }
             }
         }
     } else {
         // ===================================================== epilogue =====================
+        // Each warp owns TMEM lane quarter (warp % 4) = 32 token rows; the two warps of a quarter
+        // split the tile's columns.  Results are rounded to bf16, staged in swizzled smem and
+        // written with TMA bulk tensor stores (full 128-B lines, rows >= n_tok clipped by TMA).
         const int ew = warp - 2;              // 0..7
         const int quarter = warp & 3;         // TMEM lane quarter this warp may access
         const int half = ew >> 2;             // which half of the columns
-        const int row_in_tile = quarter * 32 + lane;
         const uint32_t lane_addr = static_cast<uint32_t>(quarter * 32) << 16;
+        const uint32_t stg = sbase + L.c_off + ew * p.stage_warp_bytes;  // this warp's staging
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+        uint32_t nstore = 0;  // staged chunks written by this warp (buffer rotation)
+        ptx::griddep_wait();  // our stores must not overtake the previous kernel's reads
+        for (int tile = first; tile < last; tile += step) {
             const TileCoord tc = tile_coord(p, tile);
-            const int t = tc.m_blk * BM + row_in_tile;
+            const int m0 = tc.m_blk * BM;
+            const int row0 = m0 + quarter * 32;
             const int n0 = tc.n_blk * p.BN;
             if constexpr (KIND == KIND_BLAST_PROJ) {
                 // stage S[l][k][n0 : n0+BN] (fp32) for the S-weighted block sum
@@ -275,74 +423,106 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
             if constexpr (KIND == KIND_BLAST_PROJ) {
                 // Z''_k[t, rho] = sum_l S[l,k,rho] * Z_l[t, rho]   (Fig. 6 "s * z'")
-                const int nsc = p.BN / 8;
-                for (int sc = half; sc < nsc; sc += 2) {
-                    float acc8[16][8];
+                // This warp: rows of its quarter, rho in [n0 + half*BN/2, n0 + (half+1)*BN/2).
+                const int W = p.BN / 2;               // staged row width (elements)
+                const uint32_t row_bytes = W * 2;
+                const uint32_t kstride = 32 * row_bytes;  // staging bytes per output block k
+                const int parts = p.out_lo_off > 0 ? 2 : 1;
+                for (int part = 0; part < parts; ++part) {
+                    if (lane == 0) ptx::bulk_wait_read<0>();
+                    __syncwarp();
+                    for (int sc = 0; sc < W / 8; ++sc) {
+                        const int col = half * W + sc * 8;  // column within the tile
+                        unsigned long long acc2[16][4];
 #pragma unroll
-                    for (int k = 0; k < 16; ++k)
+                        for (int k = 0; k < 16; ++k)
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) acc8[k][e] = 0.f;
-                    for (int l = 0; l < p.b1; ++l) {
-                        float z[8];
-                        ptx::tmem_ld_x8(tbase + l * p.BN + sc * 8, z);
-                        ptx::tmem_wait_ld();
-                        const float* srow = s_tile + (l * p.b2) * p.BN + sc * 8;
+                            for (int e = 0; e < 4; ++e) acc2[k][e] = 0ull;
+                        for (int l = 0; l < p.b1; ++l) {
+                            float z[8];
+                            ptx::tmem_ld_x8(tbase + l * p.BN + col, z);
+                            ptx::tmem_wait_ld();
+                            unsigned long long z2[4];
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) z2[e] = ptx::pack_f32x2(z[2 * e], z[2 * e + 1]);
+                            const float* srow = s_tile + (l * p.b2) * p.BN + col;
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                if (k < p.b2) {
+                                    const ulonglong2 sa = *reinterpret_cast<const ulonglong2*>(srow + k * p.BN);
+                                    const ulonglong2 sb = *reinterpret_cast<const ulonglong2*>(srow + k * p.BN + 4);
+                                    ptx::ffma2(acc2[k][0], sa.x, z2[0]);
+                                    ptx::ffma2(acc2[k][1], sa.y, z2[1]);
+                                    ptx::ffma2(acc2[k][2], sb.x, z2[2]);
+                                    ptx::ffma2(acc2[k][3], sb.y, z2[3]);
+                                }
+                            }
+                        }
 #pragma unroll
                         for (int k = 0; k < 16; ++k) {
                             if (k < p.b2) {
-                                const float4 s0 = *reinterpret_cast<const float4*>(srow + k * p.BN);
-                                const float4 s1 = *reinterpret_cast<const float4*>(srow + k * p.BN + 4);
-                                acc8[k][0] = fmaf(s0.x, z[0], acc8[k][0]);
-                                acc8[k][1] = fmaf(s0.y, z[1], acc8[k][1]);
-                                acc8[k][2] = fmaf(s0.z, z[2], acc8[k][2]);
-                                acc8[k][3] = fmaf(s0.w, z[3], acc8[k][3]);
-                                acc8[k][4] = fmaf(s1.x, z[4], acc8[k][4]);
-                                acc8[k][5] = fmaf(s1.y, z[5], acc8[k][5]);
-                                acc8[k][6] = fmaf(s1.z, z[6], acc8[k][6]);
-                                acc8[k][7] = fmaf(s1.w, z[7], acc8[k][7]);
+                                float f[8];
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) ptx::unpack_f32x2(acc2[k][e], f[2 * e], f[2 * e + 1]);
+                                stage_row8(stg + k * kstride, lane, sc, row_bytes, p.c_swz, f, part);
                             }
                         }
                     }
-                    const int rho0 = n0 + sc * 8;
-                    if (t < p.n_tok && rho0 < p.r) {
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) {
-                            if (k < p.b2) {
-                                __nv_bfloat16* dst = p.out + (static_cast<long long>(k) * p.n_tok + t) * p.out_ld + rho0;
-                                store8(dst, acc8[k], p.out_lo_off);
-                            }
-                        }
+                    ptx::fence_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        for (int k = 0; k < p.b2; ++k)
+                            ptx::tma_store_4d(&tmC, stg + k * kstride, n0 + half * W, part, row0, k);
+                        ptx::bulk_commit();
                     }
                 }
             } else {
                 const int nvalid = min(p.BN, p.N - n0);
-                for (int c0 = half * 32; c0 < nvalid; c0 += 64) {
-                    uint32_t v[32];
-                    ptx::tmem_ld_x32(tbase + c0, v);
+                const int parts = p.out_lo_off > 0 ? 2 : 1;
+                // column chunks of CW elements; chunk j of this warp starts at col = (half + 2 j) * CW
+                const int CW = p.c_box_w;
+                const uint32_t row_bytes = CW * (p.out_f32 ? 4 : 2);
+                const uint32_t buf_bytes = 32 * row_bytes;
+                for (int c0 = half * CW; c0 < nvalid; c0 += 2 * CW) {
+                    // TMEM -> registers: CW fp32 columns of this warp's 32 rows (CW <= 64, mult. of 8)
+                    float fv[64];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (j * 8 < CW) ptx::tmem_ld_x8(tbase + c0 + j * 8, *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
                     ptx::tmem_wait_ld();
-                    if (t < p.n_tok) {
+                    for (int part = 0; part < parts; ++part) {
+                        const uint32_t buf = stg + (nstore % p.stage_bufs) * buf_bytes;
+                        ++nstore;
+                        // the bulk store that last read `buf` must have finished reading it
+                        if (lane == 0) {
+                            if (p.stage_bufs == 2) ptx::bulk_wait_read<1>();
+                            else ptx::bulk_wait_read<0>();
+                        }
+                        __syncwarp();
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int c = c0 + j * 8;
-                            if (c < nvalid) {
-                                float f[8];
-#pragma unroll
-                                for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[j * 8 + e]);
-                                __nv_bfloat16* dst;
-                                if constexpr (KIND == KIND_GEMM) {
-                                    // Y[t, g*N + n0 + c]  (canonical k-major output)
-                                    dst = p.out + static_cast<long long>(t) * p.out_ld +
-                                          static_cast<long long>(tc.g) * p.N + n0 + c;
-                                } else {
-                                    // Monarch: column c of the tile is (k, rho') = (k0 + c / r', c % r');
-                                    // Z'[k][t][l r' + rho']  (the b2 <-> b1 permutation)
-                                    const int k = tc.n_blk * p.kb_per_tile + c / p.r_blk;
-                                    const int rho = c % p.r_blk;
-                                    dst = p.out + (static_cast<long long>(k) * p.n_tok + t) * p.out_ld +
-                                          tc.g * p.r_blk + rho;
-                                }
-                                store8(dst, f, p.out_lo_off);
+                        for (int j = 0; j < 8; ++j) {
+                            if (j * 8 < CW) {
+                                if (p.out_f32)
+                                    stage_row8_f32(buf, lane, j, row_bytes, p.c_swz,
+                                                   *reinterpret_cast<const float(*)[8]>(&fv[j * 8]));
+                                else
+                                    stage_row8(buf, lane, j, row_bytes, p.c_swz,
+                                               *reinterpret_cast<const float(*)[8]>(&fv[j * 8]), part);
                             }
+                        }
+                        ptx::fence_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if constexpr (KIND == KIND_GEMM) {
+                                // out (N, comp, groups, rows): element (c, part, g, t)
+                                ptx::tma_store_4d(&tmC, buf, n0 + c0, part, tc.g, row0);
+                            } else {
+                                // Monarch: chunk lies inside one output block k (CW divides r');
+                                // Z'[k][t][l r' + rho]  (the b2 <-> b1 permutation)
+                                const int k = tc.n_blk * p.kb_per_tile + c0 / p.r_blk;
+                                ptx::tma_store_5d(&tmC, buf, c0 % p.r_blk, tc.g, part, row0, k);
+                            }
+                            ptx::bulk_commit();
                         }
                     }
                 }
@@ -352,14 +532,127 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (lane == 0) ptx::mbar_arrive(tempty_bar + 8 * acc);
             if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
         }
+        if (trace && ew == 0 && lane == 0) trace[5] = ptx::globaltimer();
+        if (lane == 0) ptx::bulk_wait<0>();
+        __syncwarp();
+        if (trace && ew == 0 && lane == 0) trace[6] = ptx::globaltimer();
     }
 
     ptx::tc_fence_before();
     __syncthreads();
+    if (trace && threadIdx.x == 0) trace[7] = ptx::globaltimer();
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
     }
+}
+
+// ------------------------------------------------------------------------- BLAST S2 kernel -----
+// Z''[k][t][rho] = sum_l S[l,k,rho] * Z[l][t][rho]   (the S-weighted block sum)
+// Used when b1 * r does not fit TMEM, between the S1 grouped GEMM and the S3 expand.
+// Bandwidth-bound streaming kernel.  Block = 256 threads = 16 token rows x a 64-wide rho chunk;
+// it stages the chunk's S slice once in smem (fp32) and walks `rows_per_block` rows in passes of
+// 16.  Thread (row, 4 rho) prefetches its next row's b1 fp32 chunks with cp.async into a
+// double-buffered smem ring (no register cost), then accumulates the current row from smem.
+// Z is the unrounded fp32 S1 output; fp32 accumulation in a fixed l order and one RNE rounding
+// (plus the compensation term when comp == 2) -- the same single rounding as the fused path.
+constexpr int S2_ROWS = 16;  // rows per pass (256 threads / 16 threads per 64-rho row segment)
+template <int MAXB>
+__global__ void __launch_bounds__(256)
+    blast_s2_kernel(const float* __restrict__ Z, const __nv_bfloat16* __restrict__ S,
+                    __nv_bfloat16* __restrict__ Zpp, int n_tok, int b1, int b2, int r, int comp,
+                    int rows_per_block) {
+    extern __shared__ __align__(16) float s2_smem[];
+    float* s_sm = s2_smem;                          // [b1][b2][64] fp32
+    float4* zbuf = reinterpret_cast<float4*>(s2_smem + b1 * b2 * 64);  // [2][b1][256] float4
+    const int rho_base = blockIdx.x * 64;
+    for (int v = threadIdx.x; v < b1 * b2 * 8; v += blockDim.x) {
+        const int lk = v >> 3, c8 = (v & 7) * 8;
+        float* dst = s_sm + lk * 64 + c8;
+        if (rho_base + c8 < r) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(S + static_cast<long long>(lk) * r + rho_base + c8));
+            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                dst[2 * e] = __uint_as_float(ww[e] << 16);
+                dst[2 * e + 1] = __uint_as_float(ww[e] & 0xFFFF0000u);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dst[e] = 0.f;
+        }
+    }
+    const int c4 = threadIdx.x & 15;
+    const int rho0 = rho_base + c4 * 4;
+    const bool col_ok = rho0 < r;
+    const int row_lo = blockIdx.y * rows_per_block;
+    const int row_hi = min(n_tok, row_lo + rows_per_block);
+    const int npass = (row_hi - row_lo + S2_ROWS - 1) / S2_ROWS;
+    ptx::griddep_wait();  // Z is the previous kernel's output
+    auto prefetch = [&](int pass, int buf) {
+        const int t = row_lo + pass * S2_ROWS + (threadIdx.x >> 4);
+        if (col_ok && t < row_hi) {
+            for (int l = 0; l < b1; ++l)
+                ptx::cp_async16(ptx::smem_u32(zbuf + (buf * b1 + l) * 256 + threadIdx.x),
+                                Z + (static_cast<long long>(l) * n_tok + t) * r + rho0);
+        }
+        ptx::cp_async_commit();
+    };
+    prefetch(0, 0);
+    __syncthreads();  // S staged
+    for (int pass = 0; pass < npass; ++pass) {
+        const int buf = pass & 1;
+        if (pass + 1 < npass) prefetch(pass + 1, buf ^ 1);
+        else ptx::cp_async_commit();
+        ptx::cp_async_wait<1>();  // this thread's chunks of `pass` have landed (own data only)
+        const int t = row_lo + pass * S2_ROWS + (threadIdx.x >> 4);
+        if (!col_ok || t >= row_hi) continue;
+        unsigned long long acc2[MAXB][2];
+#pragma unroll
+        for (int k = 0; k < MAXB; ++k) acc2[k][0] = acc2[k][1] = 0ull;
+#pragma unroll
+        for (int l = 0; l < MAXB; ++l) {
+            if (l < b1) {
+                const float4 z = zbuf[(buf * b1 + l) * 256 + threadIdx.x];
+                const unsigned long long za = ptx::pack_f32x2(z.x, z.y);
+                const unsigned long long zb = ptx::pack_f32x2(z.z, z.w);
+                const float* srow = s_sm + (l * b2) * 64 + c4 * 4;
+#pragma unroll
+                for (int k = 0; k < MAXB; ++k) {
+                    if (k < b2) {
+                        const ulonglong2 sv = *reinterpret_cast<const ulonglong2*>(srow + k * 64);
+                        ptx::ffma2(acc2[k][0], sv.x, za);
+                        ptx::ffma2(acc2[k][1], sv.y, zb);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < MAXB; ++k) {
+            if (k < b2) {
+                float f[4];
+                ptx::unpack_f32x2(acc2[k][0], f[0], f[1]);
+                ptx::unpack_f32x2(acc2[k][1], f[2], f[3]);
+                uint2 w;
+                w.x = ptx::pack_bf16x2(f[0], f[1]);
+                w.y = ptx::pack_bf16x2(f[2], f[3]);
+                __nv_bfloat16* dst = Zpp + ((static_cast<long long>(k) * n_tok + t) * comp) * r + rho0;
+                *reinterpret_cast<uint2*>(dst) = w;
+                if (comp == 2) {
+                    float q[4];
+                    q[0] = f[0] - __uint_as_float(w.x << 16);
+                    q[1] = f[1] - __uint_as_float(w.x & 0xFFFF0000u);
+                    q[2] = f[2] - __uint_as_float(w.y << 16);
+                    q[3] = f[3] - __uint_as_float(w.y & 0xFFFF0000u);
+                    uint2 lo;
+                    lo.x = ptx::pack_bf16x2(q[0], q[1]);
+                    lo.y = ptx::pack_bf16x2(q[2], q[3]);
+                    *reinterpret_cast<uint2*>(dst + r) = lo;
+                }
+            }
+        }
+    }
+    ptx::cp_async_wait<0>();
 }
 
 }  // namespace blr

@@ -1,0 +1,37 @@
+"""Intra-kernel timeline: per-CTA %globaltimer stamps for each GEMM-kernel launch of one layer call.
+stamps: 0 entry, 1 setup done, 2 after griddepcontrol.wait, 3 MMA got first stage, 4 last MMA commit,
+5 epilogue done (warp 2), 6 bulk stores drained, 7 exit."""
+import ctypes, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2512_20861_b200 as blr
+from paper_2512_20861_b200 import configs, synth
+method, model, layer = (sys.argv[1:4] + ["lowrank", "GPT2-S", "c_fc"][len(sys.argv[1:4]):])[:3]
+n = int(sys.argv[4]) if len(sys.argv) > 4 else 8192
+L = configs.table3(model, layer, method)
+lib = blr.load()
+lib.blr_debug_trace.argtypes = [ctypes.c_void_p]
+dev = torch.device("cuda")
+if L.method == "lowrank":
+    fac = [t.to(dev) for t in synth.lowrank_factors(L.i, L.o, L.r)]; run = lambda X: blr.lowrank_matmul(X, *fac)
+elif L.method == "monarch":
+    fac = [t.to(dev) for t in synth.monarch_factors(L.i, L.o, L.b1, L.b2, L.r_blk)]; run = lambda X: blr.monarch_matmul(X, *fac, L.b1, L.b2)
+else:
+    fac = [t.to(dev) for t in synth.blast_factors(L.i, L.o, L.b1, L.b2, L.r)]; run = lambda X: blr.blast_matmul(X, *fac)
+X = synth.make_x(n, L.i, device=dev)
+run(X); run(X); torch.cuda.synchronize()
+buf = torch.zeros(4 * 256 * 8, dtype=torch.int64, device=dev)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev); flush.zero_()
+lib.blr_debug_trace(buf.data_ptr()); run(X); lib.blr_debug_trace(None); torch.cuda.synchronize()
+t = buf.view(4, 256, 8).cpu()
+print(f"{L.model}.{L.name}.{L.method} n={n}")
+for k in range(4):
+    tk = t[k]; ctas = tk[:, 0] > 0
+    if not ctas.any(): break
+    tk = tk[ctas].double(); t0 = tk[:, 0].min()
+    rel = (tk - t0) / 1000.0  # us
+    names = ["entry", "setup", "gdwait", "1stfull", "lastmma", "epidone", "drained", "exit"]
+    print(f" launch {k}: {int(ctas.sum())} CTAs; us since first CTA entry (min/med/max):")
+    for c, nm in enumerate(names):
+        col = rel[:, c][tk[:, c] > 0]
+        if len(col): print(f"   {nm:8s} {col.min():7.2f} {col.median():7.2f} {col.max():7.2f}")
