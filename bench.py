@@ -273,6 +273,9 @@ def main():
             phases += [(j, nm) for nm in names]
     torch.cuda.synchronize()
     n_launch = len(phases)
+    if os.environ.get("BLR_DUMP_PHASES"):
+        json.dump([f"{w.layers[j].model}.{w.layers[j].name}.{w.layers[j].method}.{nm}" for j, nm in phases],
+                  open(os.environ["BLR_DUMP_PHASES"], "w"))
 
     # ---- per-launch events (C-ABI profiling hook) and L2 flush buffer
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -336,9 +339,8 @@ def main():
     t_ms = sum(step_ms) / K
     launch_ms = [v / K for v in launch_tot]
     if ws > 1:
-        t = torch.tensor([t_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        t_ms = float(t.item())
+        from paper_2512_20861_b200 import dist as bdist
+        t_ms = bdist.max_over_ranks(t_ms, device=dev)
 
     tokens_per_step = n * len(chains)
     value = ws * tokens_per_step / (t_ms * 1e-3)
@@ -368,7 +370,7 @@ def main():
         achieved, peak, unit = alg["bytes"] / dt_s / 1e9, peaks["hbm_gbs"], "GB/s"
     else:
         achieved, peak, unit = alg["flops"] / dt_s / 1e12, peaks["bf16_tflops"], "TFLOP/s"
-    traffic = profiled_traffic(Ld, phase)
+    traffic = profiled_traffic(Ld, phase, w.key)
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
             "traffic": traffic, "kernel": f"{phase_kind(Ld, phase)} ({Ld.model}.{Ld.name}.{Ld.method} {phase})",
             "algorithmic_bytes": alg["bytes"], "algorithmic_flops": alg["flops"], "launch_ms": launch_ms[jmax],
@@ -434,9 +436,10 @@ def phase_counts(L, n, phase):
     return {"bytes": B * (L.r * L.o + n * L.o), "flops": fl}
 
 
-def profiled_traffic(L, phase):
-    """dram bytes per launch from the committed ncu --set full summary, if one exists."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def profiled_traffic(L, phase, cfg_key):
+    """dram__bytes_read.sum + dram__bytes_write.sum of that launch from the committed
+    `ncu --set full` capture (profiles/ncu_traffic_<config>.json, scripts/profile_round.sh)."""
+    path = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg_key}.json")
     try:
         d = json.load(open(path))
         return d.get(f"{L.model}.{L.name}.{L.method}.{phase}")

@@ -148,7 +148,7 @@ bool fits(const KParams& p) {
 
 // Decide weight-stationary vs streaming, staging buffers and ring depth.  `allow_resident`:
 // the kind supports a resident B slice; `stage_buf_bytes` > 0: bytes of one staging buffer.
-bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes) {
+bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) {
     const int cols = p.n_sub * p.BN;
     if (cols > blr::TMEM_COLS) return false;
     p.acc_bufs = (2 * cols <= blr::TMEM_COLS) ? 2 : 1;
@@ -163,7 +163,13 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes) {
                 p.stage_bufs = bufs;
                 if (stage_buf_bytes > 0) p.stage_warp_bytes = static_cast<uint32_t>(bufs * stage_buf_bytes);
                 for (p.stages = blr::MAX_STAGES; p.stages >= (resident ? 3 : 2); --p.stages)
-                    if (fits(p)) return true;
+                    if (fits(p)) {
+                        // slice ownership with lockstep token walks when every slice gets >= 1 CTA
+                        const int slices = p.groups * p.tiles_n;
+                        p.cps = 0;
+                        if (resident && slices <= sms) p.cps = std::max(1, std::min(sms / slices, p.tiles_m));
+                        return true;
+                    }
             }
         }
     }
@@ -198,7 +204,8 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
             g_attr_set[KIND][dev] = true;
         }
     }
-    const int grid = static_cast<int>(std::min<int64_t>(p.total_tiles, d.sm_count));
+    int grid = static_cast<int>(std::min<int64_t>(p.total_tiles, d.sm_count));
+    if (p.b_resident && p.cps > 0) grid = p.groups * p.tiles_n * p.cps;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(blr::NUM_THREADS);
@@ -276,7 +283,7 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     while (p.c_box_w * esz > 128) p.c_box_w /= 2;  // staged rows <= 128 B
     const Swz cs = pick_swz(p.c_box_w * esz);
     p.c_swz = cs.mask;
-    if (!finish_plan(p, true, 32 * p.c_box_w * esz)) return BLR_ERR_UNSUPPORTED;
+    if (!finish_plan(p, true, 32 * p.c_box_w * esz, d.sm_count)) return BLR_ERR_UNSUPPORTED;
 
     CUtensorMap ta, tb, tc;
     {
@@ -470,7 +477,7 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         p.c_box_w = chunk_width(static_cast<int>(r_blk));
         const Swz cs = pick_swz(p.c_box_w * 2);
         p.c_swz = cs.mask;
-        if (p.BN > 256 || !finish_plan(p, true, 32 * p.c_box_w * 2)) return BLR_ERR_UNSUPPORTED;
+        if (p.BN > 256 || !finish_plan(p, true, 32 * p.c_box_w * 2, d.sm_count)) return BLR_ERR_UNSUPPORTED;
         CUtensorMap ta, tb, tc;
         if (!encode_x_blocked(&ta, X, n_tok, b1, pdim)) return BLR_ERR_CUDA;
         // V viewed 4-D (a, rho', k, l) so the box (64, r', kb, 1) lands k-major in smem:
@@ -550,7 +557,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         p.c_box_w = R / 2;
         p.c_swz = pick_swz(R).mask;
         p.stage_warp_bytes = static_cast<uint32_t>(b2) * 32u * (R / 2) * 2u;
-        if (!finish_plan(p, false, 0)) return BLR_ERR_UNSUPPORTED;
+        if (!finish_plan(p, false, 0, d.sm_count)) return BLR_ERR_UNSUPPORTED;
         CUtensorMap ta, tb, tc;
         if (!encode_x_blocked(&ta, X, n_tok, b1, pdim)) return BLR_ERR_CUDA;
         const uint64_t dims[3] = {static_cast<uint64_t>(r), static_cast<uint64_t>(pdim), static_cast<uint64_t>(b1)};

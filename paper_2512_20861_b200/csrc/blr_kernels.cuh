@@ -56,6 +56,8 @@ struct KParams {
     int stages;       // smem ring depth
     int acc_bufs;     // TMEM accumulator buffers (1 or 2)
     int b_resident;   // 1: B slice resident in smem per (group, N-block) (weight-stationary)
+    int cps;          // >0 (resident only): each CTA owns slice blockIdx % slices and 1/cps of the
+                      // token tiles; all CTAs walk their token range in lockstep (L2 reuse of A)
     // ---- B operand staging
     int b_mn_major;      // 1: B stored [K][N] (N contiguous), 0: B stored [N][K]
     int b_boxes;         // TMA boxes per k-block for B (MN-major)
@@ -126,7 +128,13 @@ __device__ __forceinline__ TileCoord tile_coord(const KParams& p, int tile) {
     return c;
 }
 __device__ __forceinline__ void tile_range(const KParams& p, int& first, int& last, int& step) {
-    if (p.b_resident) {
+    if (p.b_resident && p.cps > 0) {
+        const int slices = p.groups * p.tiles_n;
+        const int sl = blockIdx.x % slices, part = blockIdx.x / slices;
+        first = sl * p.tiles_m + (part * p.tiles_m) / p.cps;
+        last = sl * p.tiles_m + ((part + 1) * p.tiles_m) / p.cps;
+        step = 1;
+    } else if (p.b_resident) {
         first = static_cast<int>((static_cast<long long>(blockIdx.x) * p.total_tiles) / gridDim.x);
         last = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * p.total_tiles) / gridDim.x);
         step = 1;
