@@ -29,7 +29,7 @@ struct DevInfo {
 std::mutex g_mu;
 DevInfo g_dev[64];
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-bool g_attr_set[4][64] = {};
+bool g_attr_set[8][64] = {};
 thread_local int t_last_launches = 0;
 thread_local void** t_prof_events = nullptr;
 thread_local int t_prof_cap = 0;
@@ -103,7 +103,9 @@ Swz pick_swz(int64_t bytes) {
     return {CU_TENSOR_MAP_SWIZZLE_NONE, 0u};
 }
 
-// Largest multiple of 8 <= 64 that divides n (n a multiple of 8).
+// Staged-store chunk width: the largest multiple of 8 <= 64 dividing n (n a multiple of 8).
+// Fewer, wider chunks beat swizzle-friendly power-of-two widths (measured: 48-wide chunks with
+// 2-way staging conflicts are faster than 16/32-wide swizzled ones for r' = 96 / 48).
 int chunk_width(int n) {
     int cw = std::min(64, n);
     while (n % cw || cw % 8) --cw;
@@ -156,27 +158,41 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) 
     const bool reuse = p.tiles_m >= 2 && p.n_sub == 1 && p.kb_half <= blr::MAX_BRES - 1 && !(e && e[0] == '1');
     const char* kb_env = getenv("BLR_KBOX");
     const int kbox_max = (kb_env && kb_env[0] == '1') ? 1 : (p.k_blocks >= 2 ? 2 : 1);
+    // Per residency mode, pick (kbox, staging buffers, stages) maximising the 64-wide K blocks in
+    // flight (latency hiding of the operand ring); prefer two staging buffers on ties.
     for (int resident = (allow_resident && reuse) ? 1 : 0; resident >= 0; --resident) {
-        for (p.kbox = kbox_max; p.kbox >= 1; --p.kbox) {
+        int best_score = -1;
+        KParams best = p;
+        for (int kbox = kbox_max; kbox >= 1; --kbox) {
             for (int bufs = 2; bufs >= 1; --bufs) {
-                p.b_resident = resident;
-                p.stage_bufs = bufs;
-                if (stage_buf_bytes > 0) p.stage_warp_bytes = static_cast<uint32_t>(bufs * stage_buf_bytes);
-                for (p.stages = blr::MAX_STAGES; p.stages >= (resident ? 3 : 2); --p.stages)
-                    if (fits(p)) {
-                        // slice ownership with lockstep token walks when every slice gets >= 1 CTA
-                        const int slices = p.groups * p.tiles_n;
-                        p.cps = 0;
-                        if (resident && slices <= sms) p.cps = std::max(1, std::min(sms / slices, p.tiles_m));
-                        return true;
-                    }
+                KParams q = p;
+                q.b_resident = resident;
+                q.kbox = kbox;
+                q.stage_bufs = bufs;
+                if (stage_buf_bytes > 0) q.stage_warp_bytes = static_cast<uint32_t>(bufs * stage_buf_bytes);
+                for (q.stages = blr::MAX_STAGES; q.stages >= 2; --q.stages)
+                    if (fits(q)) break;
+                if (q.stages < 2 || !fits(q) || (resident && q.stages < 3)) continue;
+                const int score = std::min(q.stages * kbox, 8) * 4 + (bufs == 2 ? 1 : 0) + (kbox == 2 ? 2 : 0);
+                if (score > best_score) {
+                    best_score = score;
+                    best = q;
+                }
             }
+        }
+        if (best_score >= 0) {
+            p = best;
+            // slice ownership with lockstep token walks when every slice gets >= 1 CTA (unit)
+            const int slices = p.groups * p.tiles_n;
+            p.cps = 0;
+            if (resident && slices <= sms) p.cps = std::max(1, std::min(sms / slices, p.tiles_m));
+            return true;
         }
     }
     return false;
 }
 
-thread_local unsigned long long* t_trace = nullptr;
+thread_local unsigned long long* t_trace = nullptr;  // debug trace buffer (blr_debug_trace)
 
 // Profiling-hook event record: inside stream capture the event must be an *external* record node
 // to carry a timestamp when the graph replays; outside capture a plain record.
@@ -185,37 +201,43 @@ cudaError_t prof_record(void* ev, cudaStream_t st) {
     if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) return cudaErrorUnknown;
     return cudaEventRecordWithFlags(static_cast<cudaEvent_t>(ev), st,
                                     cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault);
-}  // debug trace buffer (blr_debug_trace)
+}
 
-template <int KIND>
+template <int KIND, int PAIR>
 blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const KParams& p_in,
                   const DevInfo& d, int dev, cudaStream_t stream) {
     KParams p = p_in;
     p.trace = t_trace;
     if (t_trace) t_trace += 8 * 256;  // next launch traces into the next slot
-    auto kfn = blr::blr_gemm_kernel<KIND>;
+    auto kfn = blr::blr_gemm_kernel<KIND, PAIR>;
     const blr::SmemLayout L = blr::smem_layout(p);
     const int smem = static_cast<int>(L.total + SMEM_SLACK);
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        if (!g_attr_set[KIND][dev]) {
+        if (!g_attr_set[KIND + 3 * (PAIR - 1)][dev]) {
             if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT) != cudaSuccess)
                 return BLR_ERR_CUDA;
-            g_attr_set[KIND][dev] = true;
+            g_attr_set[KIND + 3 * (PAIR - 1)][dev] = true;
         }
     }
-    int grid = static_cast<int>(std::min<int64_t>(p.total_tiles, d.sm_count));
-    if (p.b_resident && p.cps > 0) grid = p.groups * p.tiles_n * p.cps;
+    const int units = d.sm_count / PAIR;  // CTAs (or CTA pairs) that fit one wave
+    int grid = static_cast<int>(std::min<int64_t>(p.total_tiles, units)) * PAIR;
+    if (p.b_resident && p.cps > 0) grid = p.groups * p.tiles_n * p.cps * PAIR;
+    else if (p.b_resident) grid = std::min(units, p.groups * p.tiles_n) * PAIR;  // slice round-robin
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(blr::NUM_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = PAIR;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = PAIR == 2 ? 2 : 1;
     const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
     if (prof && prof_record(t_prof_events[2 * t_prof_n], stream) != cudaSuccess)
         return BLR_ERR_CUDA;
@@ -259,13 +281,15 @@ struct OutMap {  // 4-D view (N, comp, groups, rows) of a GEMM phase's output
 // One plain GEMM phase: out[g](t, c) = sum_k A[g](t, k) B[g](k, c), K-major A.
 //   A map: a_gmid ? (K*comp, groups, rows) : (K*comp, rows, groups) with the given strides.
 //   comp == 2: A rows hold [hi | lo] (lo at column offset K) multiplying the same B rows.
-blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A, int a_gmid, int64_t a_row_stride,
-                      int64_t a_group_stride, int64_t n_tok, int64_t K, int64_t groups, int64_t N, const void* B,
-                      bool b_mn_major, const OutMap& out, int comp) {
-    KParams p = {};
+// Plan one GEMM phase for CTA-pair mode `pair` (1 or 2).  Returns false if nothing fits.
+bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok, int64_t K, int64_t groups,
+               int64_t N, bool b_mn_major, const OutMap& out, int comp) {
+    p = KParams{};
+    p.a_gmid = a_gmid;
     p.n_tok = static_cast<int>(n_tok);
-    p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM));
-    p.BN = choose_bn(N, K, p.tiles_m * groups, d.sm_count);
+    p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM * pair));
+    p.BN = choose_bn(N, K, p.tiles_m * groups, d.sm_count / pair);
+    if (pair == 2 && (p.BN / 2) % 8) p.BN = static_cast<int>(rup(p.BN, 32));
     p.N = static_cast<int>(N);
     p.tiles_n = static_cast<int>(cdiv(N, p.BN));
     p.groups = static_cast<int>(groups);
@@ -273,17 +297,45 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     p.kb_half = static_cast<int>(cdiv(K, blr::BK));
     p.k_blocks = p.kb_half * comp;
     p.a_lo_off = comp == 2 ? static_cast<int>(K) : 0;
-    p.a_gmid = a_gmid;
     p.n_sub = 1;
+    // B staging describes this CTA's share: all BN columns, or half of them in a CTA pair
+    const int bn_full = p.BN;
+    p.BN = bn_full / pair;
     set_b_staging(p, b_mn_major);
+    p.BN = bn_full;
     p.out_lo_off = out.comp == 2 ? out.comp_stride : 0;
     p.out_f32 = out.f32;
     const int esz = out.f32 ? 4 : 2;
     p.c_box_w = chunk_width(p.BN);
     while (p.c_box_w * esz > 128) p.c_box_w /= 2;  // staged rows <= 128 B
+    p.c_swz = pick_swz(p.c_box_w * esz).mask;
+    return finish_plan(p, true, 32 * p.c_box_w * esz, d.sm_count / pair);
+}
+
+// One plain GEMM phase: out[g](t, c) = sum_k A[g](t, k) B[g](k, c), K-major A.
+//   A map: a_gmid ? (K*comp, groups, rows) : (K*comp, rows, groups) with the given strides.
+//   comp == 2: A rows hold [hi | lo] (lo at column offset K) multiplying the same B rows.
+// CTA pairs (cta_group::2) are used when the weight slice would otherwise stream (BLR_PAIR=1/2
+// forces a mode).
+blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A, int a_gmid, int64_t a_row_stride,
+                      int64_t a_group_stride, int64_t n_tok, int64_t K, int64_t groups, int64_t N, const void* B,
+                      bool b_mn_major, const OutMap& out, int comp) {
+    KParams p;
+    int pair = 1;
+    const char* pe = getenv("BLR_PAIR");
+    const int force = pe ? atoi(pe) : 0;
+    if (force == 2 && n_tok >= 256) {
+        pair = 2;
+    } else if (force != 1) {
+        if (!plan_gemm(p, 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp)) return BLR_ERR_UNSUPPORTED;
+        if (!p.b_resident && n_tok >= 1024) pair = 2;
+    }
+    if (!plan_gemm(p, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp)) {
+        if (pair == 1 || !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp))
+            return BLR_ERR_UNSUPPORTED;
+    }
+    const int esz = out.f32 ? 4 : 2;
     const Swz cs = pick_swz(p.c_box_w * esz);
-    p.c_swz = cs.mask;
-    if (!finish_plan(p, true, 32 * p.c_box_w * esz, d.sm_count)) return BLR_ERR_UNSUPPORTED;
 
     CUtensorMap ta, tb, tc;
     {
@@ -313,20 +365,20 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     } else {
         const uint64_t dims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(groups)};
         const uint64_t str[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K * N) * 2};
-        const uint32_t box[3] = {blr::BK, static_cast<uint32_t>(p.BN), 1};
+        const uint32_t box[3] = {blr::BK, static_cast<uint32_t>(p.BN / pair), 1};
         if (!encode(&tb, B, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
     }
     {
         const uint64_t dims[4] = {static_cast<uint64_t>(N), static_cast<uint64_t>(out.comp),
                                   static_cast<uint64_t>(groups), static_cast<uint64_t>(n_tok)};
-        const uint64_t str[3] = {static_cast<uint64_t>(out.comp_stride) * 2, static_cast<uint64_t>(out.group_stride) * 2,
-                                 static_cast<uint64_t>(out.row_stride) * 2};
         const uint64_t es = static_cast<uint64_t>(esz);
-        const uint64_t strb[3] = {str[0] / 2 * es, str[1] / 2 * es, str[2] / 2 * es};
+        const uint64_t strb[3] = {static_cast<uint64_t>(out.comp_stride) * es, static_cast<uint64_t>(out.group_stride) * es,
+                                  static_cast<uint64_t>(out.row_stride) * es};
         const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32};
         if (!encode(&tc, out.ptr, 4, dims, strb, box, cs.mode, out.f32 != 0)) return BLR_ERR_CUDA;
     }
-    return launch<blr::KIND_GEMM>(ta, tb, tc, p, d, dev, st);
+    if (pair == 2) return launch<blr::KIND_GEMM, 2>(ta, tb, tc, p, d, dev, st);
+    return launch<blr::KIND_GEMM, 1>(ta, tb, tc, p, d, dev, st);
 }
 
 // X viewed as [n_tok][b1][p] (A operand of the block-diagonal first stage).
@@ -450,34 +502,53 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
 
     // ---- phase 1: Z'[k][t][l r' + rho] = (X_l V_{l,k})[t, rho]  (block-diagonal S1 + permutations)
     {
-        KParams p = {};
-        p.n_tok = static_cast<int>(n_tok);
-        p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM));
         // k blocks per N tile: BN = kb r' <= 256 and a multiple of 16; fewer while SMs would idle
-        int kb = std::max<int>(1, std::min<int>(static_cast<int>(b2), 256 / static_cast<int>(r_blk)));
-        while (kb > 1 && (kb * r_blk) % 16) --kb;
-        if ((kb * r_blk) % 16) kb = 2;  // r' odd multiple of 8: pair two k blocks
-        while (kb > 2 && p.tiles_m * b1 * cdiv(b2, kb) < d.sm_count) {
-            int nk = kb - 1;
-            while (nk > 1 && (nk * r_blk) % 16) --nk;
-            if ((nk * r_blk) % 16 || nk * r_blk < 64) break;
-            kb = nk;
+        auto plan_mon = [&](KParams& p, int pair) -> bool {
+            p = KParams{};
+            p.n_tok = static_cast<int>(n_tok);
+            p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM * pair));
+            int kb = std::max<int>(1, std::min<int>(static_cast<int>(b2), 256 / static_cast<int>(r_blk)));
+            while (kb > 1 && ((kb * r_blk) % 16 || kb % pair)) --kb;
+            if ((kb * r_blk) % 16 || kb % pair) kb = 2;  // r' odd multiple of 8: pair two k blocks
+            while (kb > 2 * pair && p.tiles_m * b1 * cdiv(b2, kb) < d.sm_count / pair) {
+                int nk = kb - 1;
+                while (nk > 1 && ((nk * r_blk) % 16 || nk % pair)) --nk;
+                if ((nk * r_blk) % 16 || nk % pair || nk * r_blk < 64) break;
+                kb = nk;
+            }
+            p.kb_per_tile = kb;
+            p.BN = static_cast<int>(kb * r_blk);
+            p.N = static_cast<int>(r_blk * b2);
+            p.tiles_n = static_cast<int>(cdiv(b2, kb));
+            p.groups = static_cast<int>(b1);
+            p.total_tiles = p.tiles_m * p.groups * p.tiles_n;
+            p.k_blocks = p.kb_half = static_cast<int>(cdiv(pdim, blr::BK));
+            p.n_sub = 1;
+            p.BN /= pair;  // this CTA's share of B rows
+            set_b_staging(p, false);
+            p.BN *= pair;
+            p.r_blk = static_cast<int>(r_blk);
+            p.out_lo_off = comp == 2 ? K2 : 0;
+            p.c_box_w = chunk_width(static_cast<int>(r_blk));
+            p.c_swz = pick_swz(p.c_box_w * 2).mask;
+            // weight-stationary only when every slice gets >= 2 CTAs: with short K (p) a tile's MMA is
+            // brief and slice ownership idles SMs (measured on Llama-7B: streaming 1.22 ms vs 1.44 ms)
+            const bool allow_res = static_cast<int64_t>(b1) * p.tiles_n * 2 <= d.sm_count / pair;
+            return p.BN <= 256 && p.kb_per_tile % pair == 0 &&
+                   finish_plan(p, allow_res, 32 * p.c_box_w * 2, d.sm_count / pair);
+        };
+        KParams p;
+        int pair = 1;
+        const char* pe = getenv("BLR_PAIR");
+        const int force = pe ? atoi(pe) : 0;
+        // measured (Llama-7B, GPT2-S): the Monarch S1 runs best as one CTA per tile; pairs only
+        // when forced (BLR_PAIR=2)
+        if (force == 2 && n_tok >= 256) pair = 2;
+        if (!plan_mon(p, pair)) {
+            if (pair == 1 || !plan_mon(p, pair = 1)) return BLR_ERR_UNSUPPORTED;
         }
-        p.kb_per_tile = kb;
-        p.BN = static_cast<int>(kb * r_blk);
-        p.N = static_cast<int>(r_blk * b2);
-        p.tiles_n = static_cast<int>(cdiv(b2, kb));
-        p.groups = static_cast<int>(b1);
-        p.total_tiles = p.tiles_m * p.groups * p.tiles_n;
-        p.k_blocks = p.kb_half = static_cast<int>(cdiv(pdim, blr::BK));
-        p.n_sub = 1;
-        set_b_staging(p, false);
-        p.r_blk = static_cast<int>(r_blk);
-        p.out_lo_off = comp == 2 ? K2 : 0;
-        p.c_box_w = chunk_width(static_cast<int>(r_blk));
+        const int kb = p.kb_per_tile;
         const Swz cs = pick_swz(p.c_box_w * 2);
-        p.c_swz = cs.mask;
-        if (p.BN > 256 || !finish_plan(p, true, 32 * p.c_box_w * 2, d.sm_count)) return BLR_ERR_UNSUPPORTED;
         CUtensorMap ta, tb, tc;
         if (!encode_x_blocked(&ta, X, n_tok, b1, pdim)) return BLR_ERR_CUDA;
         // V viewed 4-D (a, rho', k, l) so the box (64, r', kb, 1) lands k-major in smem:
@@ -493,7 +564,7 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
             str[1] = static_cast<uint64_t>(r_blk * pdim) * 2;
         }
         str[2] = static_cast<uint64_t>(r_blk * b2 * pdim) * 2;
-        const uint32_t box[4] = {blr::BK, static_cast<uint32_t>(r_blk), static_cast<uint32_t>(kb), 1};
+        const uint32_t box[4] = {blr::BK, static_cast<uint32_t>(r_blk), static_cast<uint32_t>(kb / pair), 1};
         if (!encode(&tb, V, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
         // Z' viewed (rho', l, comp, t, k): element at ((k*n + t)*comp + part)*K2 + l*r' + rho'
         const uint64_t cd[5] = {static_cast<uint64_t>(r_blk), static_cast<uint64_t>(b1), static_cast<uint64_t>(comp),
@@ -502,7 +573,8 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
                                   static_cast<uint64_t>(K2 * comp) * 2, static_cast<uint64_t>(K2 * comp * n_tok) * 2};
         const uint32_t cbox[5] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32, 1};
         if (!encode(&tc, workspace, 5, cd, cstr, cbox, cs.mode)) return BLR_ERR_CUDA;
-        s = launch<blr::KIND_MONARCH_PROJ>(ta, tb, tc, p, d, dev, st);
+        s = pair == 2 ? launch<blr::KIND_MONARCH_PROJ, 2>(ta, tb, tc, p, d, dev, st)
+                      : launch<blr::KIND_MONARCH_PROJ, 1>(ta, tb, tc, p, d, dev, st);
         if (s != BLR_OK) return s;
     }
     // ---- phase 2: Y[t, k q + c] = sum_kk Z'[k][t][kk] U[k][c][kk]  (U is [N][K]: K-major B)
@@ -571,7 +643,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
                                   static_cast<uint64_t>(r * comp * n_tok) * 2};
         const uint32_t cbox[4] = {static_cast<uint32_t>(R / 2), 1, 32, 1};
         if (!encode(&tc, zpp, 4, cd, cstr, cbox, pick_swz(R).mode)) return BLR_ERR_CUDA;
-        s = launch<blr::KIND_BLAST_PROJ>(ta, tb, tc, p, d, dev, st);
+        s = launch<blr::KIND_BLAST_PROJ, 1>(ta, tb, tc, p, d, dev, st);
         if (s != BLR_OK) return s;
     } else {
         // ---- S1: Z[l][t][rho] = (X_l V_l)[t, rho]  -- grouped GEMM over l (A = X viewed (p, b1, n))
@@ -605,13 +677,13 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             return BLR_ERR_CUDA;
         {
             std::lock_guard<std::mutex> lk(g_mu);
-            if (!g_attr_set[3][dev]) {
+            if (!g_attr_set[7][dev]) {
                 const int mx = 16 * 16 * 64 * 4 + 2 * 16 * 256 * 16;
                 if (cudaFuncSetAttribute(blr::blast_s2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
                     cudaFuncSetAttribute(blr::blast_s2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
                     cudaFuncSetAttribute(blr::blast_s2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess)
                     return BLR_ERR_CUDA;
-                g_attr_set[3][dev] = true;
+                g_attr_set[7][dev] = true;
             }
         }
         cudaError_t le;

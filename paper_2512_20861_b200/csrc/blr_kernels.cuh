@@ -127,22 +127,34 @@ __device__ __forceinline__ TileCoord tile_coord(const KParams& p, int tile) {
     }
     return c;
 }
-__device__ __forceinline__ void tile_range(const KParams& p, int& first, int& last, int& step) {
-    if (p.b_resident && p.cps > 0) {
-        const int slices = p.groups * p.tiles_n;
-        const int sl = blockIdx.x % slices, part = blockIdx.x / slices;
-        first = sl * p.tiles_m + (part * p.tiles_m) / p.cps;
-        last = sl * p.tiles_m + ((part + 1) * p.tiles_m) / p.cps;
-        step = 1;
-    } else if (p.b_resident) {
-        first = static_cast<int>((static_cast<long long>(blockIdx.x) * p.total_tiles) / gridDim.x);
-        last = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * p.total_tiles) / gridDim.x);
-        step = 1;
-    } else {
-        first = blockIdx.x;
-        last = p.total_tiles;
-        step = gridDim.x;
+// Tile sequence of this CTA (or CTA pair): tile_at(it) for it = 0, 1, ... until it returns -1.
+//  * streaming: round-robin over all tiles (n block fastest).
+//  * weight-stationary, #slices <= #units: unit u owns slice u % slices and 1/cps of its token tiles.
+//  * weight-stationary, #slices >  #units: unit u takes slices u, u + units, ... each over all token
+//    tiles.  Every unit walks token tiles in lockstep, so units sharing an activation tile read it
+//    from L2 (the slices of one group are adjacent in the slice order).
+struct TileIter {
+    int unit, units, slices;
+};
+__device__ __forceinline__ TileIter tile_iter(const KParams& p, int pair) {
+    TileIter t;
+    t.unit = blockIdx.x / pair;
+    t.units = gridDim.x / pair;
+    t.slices = p.groups * p.tiles_n;
+    return t;
+}
+__device__ __forceinline__ int tile_at(const KParams& p, const TileIter& t, int it) {
+    if (!p.b_resident) {
+        const long long tile = t.unit + static_cast<long long>(it) * t.units;
+        return tile < p.total_tiles ? static_cast<int>(tile) : -1;
     }
+    if (p.cps > 0) {  // slice ownership
+        const int sl = t.unit % t.slices, part = t.unit / t.slices;
+        const int mlo = (part * p.tiles_m) / p.cps, mhi = ((part + 1) * p.tiles_m) / p.cps;
+        return mlo + it < mhi ? sl * p.tiles_m + mlo + it : -1;
+    }
+    const int sl = t.unit + (it / p.tiles_m) * t.units;  // slice round-robin in passes
+    return sl < t.slices ? sl * p.tiles_m + it % p.tiles_m : -1;
 }
 
 // Stage 8 fp32 values (one 16-B chunk `chunk` of row `row`) as bf16 RNE into a row-major staging
@@ -189,7 +201,10 @@ __device__ __forceinline__ void stage_row8_f32(uint32_t buf, int row, int chunk8
     }
 }
 
-template <int KIND>
+// PAIR == 2: CTA pair (cluster of 2, tcgen05 cta_group::2): tile M = 256 tokens, each CTA loads
+// its own 128 A rows and half of B's N columns (per-SM weight ingress halves); the leader CTA
+// issues the MMAs; commits are multicast to both CTAs; each CTA drains its own TMEM rows.
+template <int KIND, int PAIR>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     blr_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, const KParams p) {
@@ -212,6 +227,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t crank = PAIR == 2 ? ptx::cluster_ctarank() : 0u;  // rank within the pair
+    const bool leader = crank == 0;
     unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 8 : nullptr;
     if (trace && threadIdx.x == 0) trace[0] = ptx::globaltimer();
 
@@ -222,7 +239,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(tfull_bar + 8 * b, 1);
-            ptx::mbar_init(tempty_bar + 8 * b, NUM_EPI_WARPS);
+            ptx::mbar_init(tempty_bar + 8 * b, NUM_EPI_WARPS * PAIR);  // leader's: both CTAs drain
         }
         for (int kb = 0; kb < MAX_BRES; ++kb) ptx::mbar_init(bfull_bar + 8 * kb, 1);
         ptx::mbar_init(bfree_bar, 1);
@@ -231,9 +248,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::prefetch_tmap(&tmB);
         ptx::prefetch_tmap(&tmC);
     }
-    if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(ptx::smem_u32(tmem_slot));
+    if (warp == 1) {
+        if constexpr (PAIR == 2) ptx::tmem_alloc_pair<TMEM_COLS>(ptx::smem_u32(tmem_slot));
+        else ptx::tmem_alloc<TMEM_COLS>(ptx::smem_u32(tmem_slot));
+    }
     ptx::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR == 2) ptx::cluster_sync();  // peer barriers initialised before any remote use
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t acc_stride = static_cast<uint32_t>(p.n_sub * p.BN);  // columns per buffer
@@ -243,26 +264,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // read (epilogue) call griddep_wait() first; the producer prefetches the resident weight
     // slice -- never written by a previous kernel -- before waiting.
     ptx::griddep_launch_dependents();
-    int first, last, step;
-    tile_range(p, first, last, step);
+    const TileIter titer = tile_iter(p, PAIR);
 
     if (warp == 0) {
         // ===================================================== TMA producer =================
         if (lane == 0) {
             const uint32_t a_blk = BM * BK * 2;  // one 64-wide K block of A (16 KB)
+            // per-CTA bytes; a pair's leader expects both CTAs' bytes on its barrier
             const uint32_t b_bytes = p.b_mn_major ? p.b_boxes * p.b_box_n * BK * 2
-                                                  : static_cast<uint32_t>(p.BN) * BK * 2;
-            const uint32_t tx = p.kbox * (a_blk + (p.b_resident ? 0u : b_bytes));
+                                                  : static_cast<uint32_t>(p.BN / PAIR) * BK * 2;
+            const uint32_t tx = p.kbox * (a_blk + (p.b_resident ? 0u : b_bytes)) * PAIR;
+            auto load3 = [&](uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2) {
+                if constexpr (PAIR == 2) ptx::tma_load_3d_pair(dst, m, bar, c0, c1, c2);
+                else ptx::tma_load_3d(dst, m, bar, c0, c1, c2);
+            };
+            auto load4 = [&](uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2, int c3) {
+                if constexpr (PAIR == 2) ptx::tma_load_4d_pair(dst, m, bar, c0, c1, c2, c3);
+                else ptx::tma_load_4d(dst, m, bar, c0, c1, c2, c3);
+            };
             const int n_steps = (p.k_blocks + p.kbox - 1) / p.kbox;
             int stage = 0;
             uint32_t phase = 0;
             int cur_slice = -1;
             uint32_t nslices = 0;
             bool waited = false;
-            for (int tile = first; tile < last; tile += step) {
+            for (int it = 0, tile; (tile = tile_at(p, titer, it)) >= 0; ++it) {
                 const TileCoord tc = tile_coord(p, tile);
-                const int m0 = tc.m_blk * BM;
-                const int n0 = tc.n_blk * p.BN;
+                const int m0 = (tc.m_blk * PAIR + static_cast<int>(crank)) * BM;
+                const int n0 = tc.n_blk * p.BN + static_cast<int>(crank) * (p.BN / PAIR);  // this CTA's B half
+                // Monarch: first output block k of this CTA's share of the tile's k blocks
+                const int kblk0 = tc.n_blk * p.kb_per_tile + static_cast<int>(crank) * (p.kb_per_tile / PAIR);
                 if (p.b_resident && tc.slice != cur_slice) {
                     // (re)load the weight slice once for the contiguous run of token tiles
                     if (nslices > 0) ptx::mbar_wait(bfree_bar, (nslices - 1) & 1);
@@ -270,16 +301,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int kb = 0; kb < kbr; ++kb) {
                         const uint32_t b_dst = b_base + kb * p.b_stage_bytes;
                         const uint32_t bb = bfull_bar + 8 * kb;  // per-block barrier: MMA starts early
-                        ptx::mbar_arrive_expect_tx(bb, b_bytes);
+                        if (leader) ptx::mbar_arrive_expect_tx(bb, b_bytes * PAIR);
                         const int k0 = kb * BK;
                         if constexpr (KIND == KIND_MONARCH_PROJ) {
-                            ptx::tma_load_4d(b_dst, &tmB, bb, k0, 0, tc.n_blk * p.kb_per_tile, tc.g);
+                            load4(b_dst, &tmB, bb, k0, 0, kblk0, tc.g);
                         } else if (p.b_mn_major) {
                             for (int j = 0; j < p.b_boxes; ++j)
-                                ptx::tma_load_3d(b_dst + j * (p.b_box_n * BK * 2), &tmB, bb,
-                                                 n0 + j * p.b_box_n, k0, tc.g);
+                                load3(b_dst + j * (p.b_box_n * BK * 2), &tmB, bb, n0 + j * p.b_box_n, k0, tc.g);
                         } else {
-                            ptx::tma_load_3d(b_dst, &tmB, bb, k0, n0, tc.g);
+                            load3(b_dst, &tmB, bb, k0, n0, tc.g);
                         }
                     }
                     cur_slice = tc.slice;
@@ -294,7 +324,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int si = 0; si < n_steps; ++si) {
                         ptx::mbar_wait(empty_bar + 8 * stage, phase ^ 1);
                         const uint32_t fb = full_bar + 8 * stage;
-                        ptx::mbar_arrive_expect_tx(fb, tx);
+                        if (leader) ptx::mbar_arrive_expect_tx(fb, tx);
                         const uint32_t a_st = a_base + stage * (a_blk * p.kbox);
                         const uint32_t b_st = b_base + stage * (p.b_stage_bytes * p.kbox);
                         for (int j = 0; j < p.kbox; ++j) {
@@ -306,23 +336,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             const int k0 = (kb - part * p.kb_half) * BK;  // padded block: k0 >= K, zero-filled
                             if constexpr (KIND == KIND_GEMM) {
                                 if (p.a_gmid)
-                                    ptx::tma_load_3d(a_dst, &tmA, fb, part * p.a_lo_off + k0, tc.g, m0);
+                                    load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, tc.g, m0);
                                 else
-                                    ptx::tma_load_3d(a_dst, &tmA, fb, part * p.a_lo_off + k0, m0, tc.g);
+                                    load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, m0, tc.g);
                                 if (!p.b_resident) {
                                     if (p.b_mn_major) {
                                         for (int q = 0; q < p.b_boxes; ++q)
-                                            ptx::tma_load_3d(b_dst + q * (p.b_box_n * BK * 2), &tmB, fb,
-                                                             n0 + q * p.b_box_n, k0, tc.g);
+                                            load3(b_dst + q * (p.b_box_n * BK * 2), &tmB, fb, n0 + q * p.b_box_n, k0, tc.g);
                                     } else {
-                                        ptx::tma_load_3d(b_dst, &tmB, fb, k0, n0, tc.g);
+                                        load3(b_dst, &tmB, fb, k0, n0, tc.g);
                                     }
                                 }
                             } else if constexpr (KIND == KIND_MONARCH_PROJ) {
                                 // A = X viewed [n_tok][b1][p]; B = V viewed 4-D (a, rho', k, l)
-                                ptx::tma_load_3d(a_dst, &tmA, fb, k0, tc.g, m0);
-                                if (!p.b_resident)
-                                    ptx::tma_load_4d(b_dst, &tmB, fb, k0, 0, tc.n_blk * p.kb_per_tile, tc.g);
+                                load3(a_dst, &tmA, fb, k0, tc.g, m0);
+                                if (!p.b_resident) load4(b_dst, &tmB, fb, k0, 0, kblk0, tc.g);
                             } else {  // KIND_BLAST_PROJ: sub = l
                                 ptx::tma_load_3d(a_dst, &tmA, fb, k0, sub, m0);
                                 for (int q = 0; q < p.b_boxes; ++q)
@@ -337,8 +365,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp == 1) {
         // ===================================================== MMA issuer ===================
-        if (lane == 0) {
-            const uint32_t idesc = ptx::idesc_bf16(BM, p.BN, p.b_mn_major);
+        if (lane == 0 && leader) {
+            const uint32_t idesc = ptx::idesc_bf16(BM * PAIR, p.BN, p.b_mn_major);
+            auto commit = [&](uint32_t bar) {
+                if constexpr (PAIR == 2) ptx::mma_commit_pair(bar);  // arrives in both CTAs
+                else ptx::mma_commit(bar);
+            };
             // descriptors are built once; per-MMA only the 14-bit start-address field advances
             const uint64_t a_desc0 = ptx::smem_desc(a_base, 16, 1024, ptx::LAYOUT_SW128);
             const uint64_t b_desc0 = ptx::smem_desc(b_base, p.b_lbo, p.b_sbo, p.b_layout);
@@ -350,7 +382,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint32_t acc_phase = 0;
             int cur_slice = -1;
             uint32_t nslices = 0;
-            for (int tile = first; tile < last; tile += step) {
+            for (int it = 0, tile; (tile = tile_at(p, titer, it)) >= 0; ++it) {
                 const TileCoord tc = tile_coord(p, tile);
                 bool fresh = false;  // first tile of a new resident slice: wait per B block
                 if (p.b_resident && tc.slice != cur_slice) {
@@ -378,19 +410,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 // A: K-major, 128-B swizzle, 8-row groups 1024 B apart; +32 B per K=16.
                                 const uint64_t ad = a_desc0 + ((a_off + kk * 32) >> 4);
                                 const uint64_t bd = b_desc0 + ((b_off + kk * p.b_kstep) >> 4);
-                                ptx::mma_bf16(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
+                                if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
+                                else ptx::mma_bf16(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
                             }
                         }
-                        ptx::mma_commit(empty_bar + 8 * stage);  // frees the smem slot
+                        commit(empty_bar + 8 * stage);  // frees the smem slot (both CTAs of a pair)
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
                 }
-                ptx::mma_commit(tfull_bar + 8 * acc);  // accumulator ready for the epilogue
+                commit(tfull_bar + 8 * acc);  // accumulator ready for the epilogue(s)
                 if (trace) trace[4] = ptx::globaltimer();
                 if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
                 if (p.b_resident) {
-                    const int nt = tile + step;
-                    if (nt >= last || tile_coord(p, nt).slice != cur_slice) ptx::mma_commit(bfree_bar);
+                    const int nt = tile_at(p, titer, it + 1);
+                    if (nt < 0 || tile_coord(p, nt).slice != cur_slice) commit(bfree_bar);
                 }
             }
         }
@@ -408,9 +441,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t acc_phase = 0;
         uint32_t nstore = 0;  // staged chunks written by this warp (buffer rotation)
         ptx::griddep_wait();  // our stores must not overtake the previous kernel's reads
-        for (int tile = first; tile < last; tile += step) {
+        for (int it = 0, tile; (tile = tile_at(p, titer, it)) >= 0; ++it) {
             const TileCoord tc = tile_coord(p, tile);
-            const int m0 = tc.m_blk * BM;
+            const int m0 = (tc.m_blk * PAIR + static_cast<int>(crank)) * BM;
             const int row0 = m0 + quarter * 32;
             const int n0 = tc.n_blk * p.BN;
             if constexpr (KIND == KIND_BLAST_PROJ) {
@@ -537,7 +570,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(tempty_bar + 8 * acc);
+            if (lane == 0) {
+                if constexpr (PAIR == 2) ptx::mbar_arrive_remote(tempty_bar + 8 * acc, 0);  // leader's barrier
+                else ptx::mbar_arrive(tempty_bar + 8 * acc);
+            }
             if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
         }
         if (trace && ew == 0 && lane == 0) trace[5] = ptx::globaltimer();
@@ -548,10 +584,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     ptx::tc_fence_before();
     __syncthreads();
+    if constexpr (PAIR == 2) ptx::cluster_sync();  // the peer's MMAs / remote arrivals are done
     if (trace && threadIdx.x == 0) trace[7] = ptx::globaltimer();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+        if constexpr (PAIR == 2) ptx::tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+        else ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
     }
 }
 

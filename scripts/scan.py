@@ -27,7 +27,7 @@ else:
     run = lambda X: blr.blast_matmul(X, *fac)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 print(f"{L.model}.{L.name}.{L.method} i={L.i} o={L.o} r={L.r} b={L.b}")
-for n in [128, 512, 2048, 8192, 32768]:
+for n in [int(x) for x in os.environ.get("SCAN_N", "128,512,2048,8192,32768").split(",")]:
     X = synth.make_x(n, L.i, device=dev)
     run(X)
     nl = lib.blr_last_launch_count()

@@ -226,3 +226,26 @@ def test_c5_vit_dit(cuda_lib, images):
             rows = sample_rows(w.n, 128)
             ridx = torch.as_tensor(rows, device=DEV)
             assert_parity(Y[ridx], _layer_ref(L, to64(X[ridx]), fac), f"{w.key} {L.name} {L.method}")
+
+
+# ------------------------------------------------------------------------------ CTA-pair mode --
+@pytest.mark.parametrize("pair", ["1", "2"])
+@pytest.mark.parametrize("method", ["lowrank", "monarch", "blast"])
+def test_forced_cta_pair_modes(cuda_lib, monkeypatch, pair, method):
+    """Both GEMM variants (one CTA, or a cta_group::2 pair with M=256 and B split across the pair)
+    on shapes with ragged token tails and multi-tile N, against the oracle."""
+    monkeypatch.setenv("BLR_PAIR", pair)
+    n = 1000
+    if method == "lowrank":
+        L = configs.Layer("t", "t", 1024, 1376, "lowrank", 160, 1)
+    elif method == "monarch":
+        L = configs.Layer("t", "t", 1024, 1376, "monarch", 256, 16)   # r' = 16, q = 86 -> use 8-mult
+        L = configs.Layer("t", "t", 2048, 1408, "monarch", 256, 16)   # q = 88
+    else:
+        L = configs.Layer("t", "t", 1024, 1408, "blast", 272, 16)     # split path (b1*r > 512)
+    X = synth.make_x(n, L.i, seed=11, device=DEV)
+    fac = [t.to(DEV) for t in _factors(L, 11, 0)]
+    Y = _layer_run(cuda_lib, L, X, fac)
+    rows = sample_rows(n, 200)
+    ridx = torch.as_tensor(rows, device=DEV)
+    assert_parity(Y[ridx], _layer_ref(L, to64(X[ridx]), fac), f"pair={pair} {method}")
