@@ -140,8 +140,13 @@ int main() {
     CK(cudaFuncSetAttribute(ingress, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     CK(cudaFuncSetAttribute(ingress, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 
-    struct Case { const char* name; int mode; int grid; size_t footprint; int csize; int nst; int bps; int smem_kb; };
+    struct Case { const char* name; int mode; int grid; size_t footprint; int csize; int nst; int bps; int smem_kb; int wide = 1; };
     std::vector<Case> cases = {
+        {"L2 32MiB 8x16KB contiguous rows", 0, sms, size_t(32) << 20, 1, 8, 1, 0, 1},
+        {"L2 32MiB 8x16KB strided x3 (384B rows)", 0, sms, size_t(32) << 20, 1, 8, 1, 0, 3},
+        {"L2 32MiB 8x16KB strided x8 (1KB rows)", 0, sms, size_t(32) << 20, 1, 8, 1, 0, 8},
+        {"L2 32MiB 6x32KB contiguous", 0, sms, size_t(32) << 20, 1, 6, 2, 0, 1},
+        {"L2 32MiB 6x32KB strided x3", 0, sms, size_t(32) << 20, 1, 6, 2, 0, 3},
         {"L2 32MiB 8x16KB smem 128KB", 0, sms, size_t(32) << 20, 1, 8, 1, 128},
         {"L2 32MiB 8x16KB smem 160KB", 0, sms, size_t(32) << 20, 1, 8, 1, 160},
         {"L2 32MiB 8x16KB smem 200KB", 0, sms, size_t(32) << 20, 1, 8, 1, 200},
@@ -159,8 +164,8 @@ int main() {
     for (auto& c : cases) {
         const uint64_t total_rows = c.footprint / 128;
         CUtensorMap tm;
-        const uint64_t dims[2] = {64, total_rows};
-        const uint64_t str[1] = {128};
+        const uint64_t dims[2] = {64ull * c.wide, total_rows / c.wide};
+        const uint64_t str[1] = {128ull * c.wide};
         const uint32_t box[2] = {64, (uint32_t)(c.mode == 2 ? BOX_ROWS / c.csize : BOX_ROWS)};
         const uint32_t es[2] = {1, 1};
         CUresult r = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, str, box, es,
@@ -168,7 +173,7 @@ int main() {
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) { printf("encode failed %d\n", (int)r); return 1; }
         int ctas_sharing = (c.mode == 2) ? c.grid / c.csize : c.grid;
-        int rows_per_cta = (int)(total_rows / (c.mode == 1 ? 1 : ctas_sharing)) / BOX_ROWS * BOX_ROWS;
+        int rows_per_cta = (int)(total_rows / c.wide / (c.mode == 1 ? 1 : ctas_sharing)) / BOX_ROWS * BOX_ROWS;
         if (c.mode == 1) rows_per_cta = (int)total_rows / BOX_ROWS * BOX_ROWS;
         const int iters = 2000;
         cudaLaunchConfig_t cfg = {};

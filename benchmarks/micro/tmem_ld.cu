@@ -1,0 +1,92 @@
+// tmem_ld.cu -- microbenchmark: tcgen05.ld (TMEM -> registers) throughput per SM, for the
+// epilogue cost model.  W warps (multiple of 4) each read their lane quarter of a 128 x 512 fp32
+// TMEM region repeatedly with 32x32b.x{8,32,64} loads.
+// Build: nvcc -std=c++17 -O3 -gencode arch=compute_100a,code=sm_100a -o tmem_ld tmem_ld.cu
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int X>
+__device__ __forceinline__ void ld(uint32_t taddr, uint32_t* r);
+template <>
+__device__ __forceinline__ void ld<8>(uint32_t t, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(t));
+}
+template <>
+__device__ __forceinline__ void ld<32>(uint32_t t, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+        "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(t));
+}
+
+template <int X>
+__global__ void __launch_bounds__(512, 1) k(int iters, unsigned long long* out, uint32_t* sink) {
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t base = slot + ((uint32_t)((warp & 3) * 32) << 16);
+    const int nw = blockDim.x / 32;
+    const int col0 = (warp >> 2) * 32;  // warps of the same quarter read different columns
+    uint32_t acc = 0;
+    __syncthreads();
+    unsigned long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+        uint32_t r[X];
+        for (int c = col0; c + X <= 512; c += (nw / 4) * 32 > X ? (nw / 4) * 32 : X) {
+            ld<X>(base + c, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+            for (int j = 0; j < X; ++j) acc += r[j];
+        }
+    }
+    unsigned long long t1 = clock64();
+    __syncthreads();
+    if (threadIdx.x == 0) out[blockIdx.x] = t1 - t0;
+    sink[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
+}
+
+template <int X>
+void run(int warps) {
+    unsigned long long* d;
+    uint32_t* sink;
+    cudaMalloc(&d, 8 * 148);
+    cudaMalloc(&sink, 4 * 148 * 512);
+    const int iters = 200;
+    k<X><<<148, warps * 32>>>(iters, d, sink);
+    cudaDeviceSynchronize();
+    k<X><<<148, warps * 32>>>(iters, d, sink);
+    cudaDeviceSynchronize();
+    unsigned long long h;
+    cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+    // bytes read per CTA: each warp reads 32 lanes x (columns it visits) x 4 B
+    const int step = (warps / 4) * 32 > X ? (warps / 4) * 32 : X;
+    long long per_warp_cols = 0;
+    for (int c = 0; c + X <= 512; c += step) per_warp_cols += X;
+    const double bytes = double(iters) * warps * 32 * per_warp_cols * 4;
+    printf("x%-3d warps %2d: %.1f B/clk/SM TMEM->RF (%s)\n", X, warps, bytes / h, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+    for (int w : {4, 8, 16}) {
+        run<8>(w);
+        run<32>(w);
+    }
+    return 0;
+}

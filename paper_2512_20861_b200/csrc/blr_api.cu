@@ -208,7 +208,11 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
                   const DevInfo& d, int dev, cudaStream_t stream) {
     KParams p = p_in;
     p.trace = t_trace;
-    if (t_trace) t_trace += 8 * 256;  // next launch traces into the next slot
+    if (t_trace) {
+        const char* e = getenv("BLR_DBG");
+        p.dbg = e ? atoi(e) : 0;
+    }
+    if (t_trace) t_trace += 128 * 256;  // next launch traces into the next slot
     auto kfn = blr::blr_gemm_kernel<KIND, PAIR>;
     const blr::SmemLayout L = blr::smem_layout(p);
     const int smem = static_cast<int>(L.total + SMEM_SLACK);

@@ -76,7 +76,8 @@ struct KParams {
     int b1, b2;            // BLAST block counts
     int r;                 // BLAST: rank
     const __nv_bfloat16* S;  // BLAST: S [b1][b2][r]
-    unsigned long long* trace;  // debug: per-CTA %globaltimer stamps [grid][8] (nullptr = off)
+    unsigned long long* trace;  // debug: per-CTA %globaltimer stamps [grid][64] (nullptr = off)
+    int dbg;                    // debug bits (0 in production): 1 skip epilogue bulk stores, 2 skip staging
 };
 
 struct SmemLayout {
@@ -229,7 +230,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int lane = threadIdx.x & 31;
     const uint32_t crank = PAIR == 2 ? ptx::cluster_ctarank() : 0u;  // rank within the pair
     const bool leader = crank == 0;
-    unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 8 : nullptr;
+    unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 128 : nullptr;
     if (trace && threadIdx.x == 0) trace[0] = ptx::globaltimer();
 
     if (threadIdx.x == 0) {
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int cur_slice = -1;
             uint32_t nslices = 0;
             bool waited = false;
+            int nstep_tr = 0;
             for (int it = 0, tile; (tile = tile_at(p, titer, it)) >= 0; ++it) {
                 const TileCoord tc = tile_coord(p, tile);
                 const int m0 = (tc.m_blk * PAIR + static_cast<int>(crank)) * BM;
@@ -325,6 +327,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         ptx::mbar_wait(empty_bar + 8 * stage, phase ^ 1);
                         const uint32_t fb = full_bar + 8 * stage;
                         if (leader) ptx::mbar_arrive_expect_tx(fb, tx);
+                        if (trace && nstep_tr < 32) trace[64 + nstep_tr] = ptx::globaltimer();
+                        ++nstep_tr;
                         const uint32_t a_st = a_base + stage * (a_blk * p.kbox);
                         const uint32_t b_st = b_base + stage * (p.b_stage_bytes * p.kbox);
                         for (int j = 0; j < p.kbox; ++j) {
@@ -382,6 +386,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint32_t acc_phase = 0;
             int cur_slice = -1;
             uint32_t nslices = 0;
+            int mstep_tr = 0;
             for (int it = 0, tile; (tile = tile_at(p, titer, it)) >= 0; ++it) {
                 const TileCoord tc = tile_coord(p, tile);
                 bool fresh = false;  // first tile of a new resident slice: wait per B block
@@ -397,7 +402,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int si = 0; si < n_steps; ++si) {
                         ptx::mbar_wait(full_bar + 8 * stage, phase);
                         ptx::tc_fence_after();
-                        if (trace && trace[3] == 0) trace[3] = ptx::globaltimer();
+                        if (trace) {
+                            if (trace[3] == 0) trace[3] = ptx::globaltimer();
+                            if (mstep_tr < 32) trace[96 + mstep_tr] = ptx::globaltimer();
+                            ++mstep_tr;
+                        }
                         for (int j = 0; j < p.kbox; ++j) {
                             const int kb = si * p.kbox + j;
                             const int bkb = (p.a_lo_off > 0 && kb >= p.kb_half) ? kb - p.kb_half : kb;
@@ -419,7 +428,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
                 commit(tfull_bar + 8 * acc);  // accumulator ready for the epilogue(s)
-                if (trace) trace[4] = ptx::globaltimer();
+                if (trace) {
+                    trace[4] = ptx::globaltimer();
+                    if (it < 24) trace[16 + it] = trace[4];  // per-tile MMA issue-complete time
+                }
                 if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
                 if (p.b_resident) {
                     const int nt = tile_at(p, titer, it + 1);
@@ -542,7 +554,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         __syncwarp();
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
-                            if (j * 8 < CW) {
+                            if (j * 8 < CW && !(p.dbg & 2)) {
                                 if (p.out_f32)
                                     stage_row8_f32(buf, lane, j, row_bytes, p.c_swz,
                                                    *reinterpret_cast<const float(*)[8]>(&fv[j * 8]));
@@ -553,7 +565,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                         ptx::fence_async_smem();
                         __syncwarp();
-                        if (lane == 0) {
+                        if (lane == 0 && !(p.dbg & 1)) {
                             if constexpr (KIND == KIND_GEMM) {
                                 // out (N, comp, groups, rows): element (c, part, g, t)
                                 ptx::tma_store_4d(&tmC, buf, n0 + c0, part, tc.g, row0);
@@ -568,6 +580,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
             }
+            if (trace && ew == 0 && lane == 0 && it < 24) trace[40 + it] = ptx::globaltimer();  // epilogue done
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {

@@ -20,10 +20,10 @@ else:
     fac = [t.to(dev) for t in synth.blast_factors(L.i, L.o, L.b1, L.b2, L.r)]; run = lambda X: blr.blast_matmul(X, *fac)
 X = synth.make_x(n, L.i, device=dev)
 run(X); run(X); torch.cuda.synchronize()
-buf = torch.zeros(4 * 256 * 8, dtype=torch.int64, device=dev)
+buf = torch.zeros(4 * 256 * 128, dtype=torch.int64, device=dev)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev); flush.zero_()
 lib.blr_debug_trace(buf.data_ptr()); run(X); lib.blr_debug_trace(None); torch.cuda.synchronize()
-t = buf.view(4, 256, 8).cpu()
+t = buf.view(4, 256, 128).cpu()
 print(f"{L.model}.{L.name}.{L.method} n={n}")
 for k in range(4):
     tk = t[k]; ctas = tk[:, 0] > 0
@@ -35,3 +35,12 @@ for k in range(4):
     for c, nm in enumerate(names):
         col = rel[:, c][tk[:, c] > 0]
         if len(col): print(f"   {nm:8s} {col.min():7.2f} {col.median():7.2f} {col.max():7.2f}")
+    c0 = tk[0]
+    mm = [(c0[16 + i] - t0).item() / 1000 for i in range(24) if c0[16 + i] > 0]
+    ep = [(c0[40 + i] - t0).item() / 1000 for i in range(24) if c0[40 + i] > 0]
+    print("   CTA0 per-tile MMA-commit us:", " ".join(f"{v:.2f}" for v in mm))
+    print("   CTA0 per-tile epilogue-done us:", " ".join(f"{v:.2f}" for v in ep))
+    pi = [(c0[64 + i] - t0).item() / 1000 for i in range(32) if c0[64 + i] > 0]
+    mf = [(c0[96 + i] - t0).item() / 1000 for i in range(32) if c0[96 + i] > 0]
+    print("   CTA0 producer issue  us:", " ".join(f"{v:.2f}" for v in pi))
+    print("   CTA0 MMA full-ready  us:", " ".join(f"{v:.2f}" for v in mf))
