@@ -290,27 +290,43 @@ def main():
     # ---- the step as a CUDA graph (host launch overhead removed, as under the paper's
     #      torch.compile + CUDA-graph protocol); the per-launch events of the
     #      C-ABI profiling hook are captured as event-record nodes inside the graph.
-    graph = None
+    # Two graphs of the same step: `graph` (timed; nothing but the kernels, so programmatic
+    # dependent launch overlaps each kernel's prologue with its predecessor) and `graph_prof`
+    # (per-launch event-record nodes between the kernels, replayed separately after the timed
+    # region for the per-phase breakdown -- the events serialise the launches, so its per-launch
+    # sum is an upper bound of the step).
+    graph = graph_prof = None
     if not args.eager:
         for _ in range(2):
             step(xs)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
-        arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in gev])
         with torch.cuda.graph(graph):
+            step(xs)
+        graph_prof = torch.cuda.CUDAGraph()
+        arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in gev])
+        with torch.cuda.graph(graph_prof):
             lib.blr_profile_begin(arr, 2 * n_launch)
             step(xs)
-            per_replay = lib.blr_profile_end()
+            per_replay_prof = lib.blr_profile_end()
+        assert per_replay_prof == n_launch
         torch.cuda.synchronize()
 
     def run_step():
         if graph is not None:
             graph.replay()
-            return per_replay
+            return n_launch
+        step(xs)
+        return n_launch
+
+    def run_step_profiled():
+        if graph_prof is not None:
+            graph_prof.replay()
+            return
         arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in gev])
         lib.blr_profile_begin(arr, 2 * n_launch)
         step(xs)
-        return lib.blr_profile_end()
+        lib.blr_profile_end()
 
     for _ in range(W):
         flush.zero_()
@@ -318,7 +334,6 @@ def main():
     torch.cuda.synchronize()
 
     launches = 0
-    launch_tot = [0.0] * n_launch
     sampler = Sampler(dev.index)
     if ws > 1:
         torch.distributed.barrier()
@@ -329,11 +344,25 @@ def main():
             step_ev[s][0].record(stream)
             launches += run_step()
             step_ev[s][1].record(stream)
-            torch.cuda.synchronize()  # between steps, outside the events: read this step's launches
-            for j in range(n_launch):
-                launch_tot[j] += gev[2 * j].elapsed_time(gev[2 * j + 1])
+        torch.cuda.synchronize()
     if ws > 1:
         torch.distributed.barrier()
+
+    # per-launch breakdown (profiled graph, outside the timed region)
+    launch_tot = [0.0] * n_launch
+    kp = max(3, min(K, 20))
+    prof_step_ms = 0.0
+    pe = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    for s in range(kp):
+        flush.zero_()
+        pe[0].record(stream)
+        run_step_profiled()
+        pe[1].record(stream)
+        torch.cuda.synchronize()
+        prof_step_ms += pe[0].elapsed_time(pe[1]) / kp
+        for j in range(n_launch):
+            launch_tot[j] += gev[2 * j].elapsed_time(gev[2 * j + 1])
+    launch_tot = [v * K / kp for v in launch_tot]
 
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
     t_ms = sum(step_ms) / K
@@ -393,7 +422,7 @@ def main():
                        "l2": "flushed between timed steps (write of 2x L2), outside the step events",
                        "launch": "eager" if args.eager else "CUDA graph replay of the step (both arms)",
                        "parallelism": f"token-sharded dp{ws}, no data-path collective"},
-            "roofline": roof, "per_layer": per_layer, "gpu_launches": launches,
+            "roofline": roof, "per_layer": per_layer, "ms_per_step_with_launch_events": prof_step_ms, "gpu_launches": launches,
             "clocks": sampler.summary(), "e2e": e2e}
     if dense is not None:
         line["cublas_dense_bf16"] = dense

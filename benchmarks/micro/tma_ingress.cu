@@ -142,24 +142,20 @@ int main() {
 
     struct Case { const char* name; int mode; int grid; size_t footprint; int csize; int nst; int bps; int smem_kb; int wide = 1; };
     std::vector<Case> cases = {
-        {"L2 32MiB 8x16KB contiguous rows", 0, sms, size_t(32) << 20, 1, 8, 1, 0, 1},
-        {"L2 32MiB 8x16KB strided x3 (384B rows)", 0, sms, size_t(32) << 20, 1, 8, 1, 0, 3},
-        {"L2 32MiB 8x16KB strided x8 (1KB rows)", 0, sms, size_t(32) << 20, 1, 8, 1, 0, 8},
-        {"L2 32MiB 6x32KB contiguous", 0, sms, size_t(32) << 20, 1, 6, 2, 0, 1},
-        {"L2 32MiB 6x32KB strided x3", 0, sms, size_t(32) << 20, 1, 6, 2, 0, 3},
-        {"L2 32MiB 8x16KB smem 128KB", 0, sms, size_t(32) << 20, 1, 8, 1, 128},
-        {"L2 32MiB 8x16KB smem 160KB", 0, sms, size_t(32) << 20, 1, 8, 1, 160},
-        {"L2 32MiB 8x16KB smem 200KB", 0, sms, size_t(32) << 20, 1, 8, 1, 200},
-        {"L2 32MiB 8x16KB smem 224KB", 0, sms, size_t(32) << 20, 1, 8, 1, 224},
-        {"L2 32MiB 4x16KB in flight", 0, sms, size_t(32) << 20, 1, 4, 1, 0},
-        {"L2 32MiB 6x32KB in flight", 0, sms, size_t(32) << 20, 1, 6, 2, 0},
-        {"L2 32MiB 12x16KB in flight", 0, sms, size_t(32) << 20, 1, 12, 1, 0},
-        {"L2 32MiB 4x48KB in flight", 0, sms, size_t(32) << 20, 1, 4, 3, 0},
-        {"HBM 2GiB 12x16KB in flight", 0, sms, size_t(2) << 30, 1, 12, 1, 0},
-        {"HBM 2GiB 4x48KB in flight", 0, sms, size_t(2) << 30, 1, 4, 3, 0},
-        {"distinct, L2-resident 32 MiB", 0, sms, size_t(32) << 20, 1, 8, 1, 0},
-        {"same slice all CTAs (1 MiB)", 1, sms, size_t(1) << 20, 1, 8, 1, 0},
-        {"distinct, L2 32 MiB, half the SMs 12x16", 0, sms / 2, size_t(32) << 20, 1, 12, 1, 0},
+        {"HBM 148 SMs 1x16KB in flight", 0, sms, size_t(2) << 30, 1, 1, 1, 0},
+        {"HBM 148 SMs 2x16KB in flight", 0, sms, size_t(2) << 30, 1, 2, 1, 0},
+        {"HBM 148 SMs 4x16KB in flight", 0, sms, size_t(2) << 30, 1, 4, 1, 0},
+        {"HBM 148 SMs 8x16KB in flight", 0, sms, size_t(2) << 30, 1, 8, 1, 0},
+        {"HBM 148 SMs 2x32KB in flight", 0, sms, size_t(2) << 30, 1, 2, 2, 0},
+        {"HBM 148 SMs 4x32KB in flight", 0, sms, size_t(2) << 30, 1, 4, 2, 0},
+        {"HBM 148 SMs 6x32KB in flight", 0, sms, size_t(2) << 30, 1, 6, 2, 0},
+        {"HBM 64 SMs 4x32KB in flight", 0, 64, size_t(2) << 30, 1, 4, 2, 0},
+        {"HBM 64 SMs 6x32KB in flight", 0, 64, size_t(2) << 30, 1, 6, 2, 0},
+        {"HBM 64 SMs 4x48KB in flight", 0, 64, size_t(2) << 30, 1, 4, 3, 0},
+        {"HBM 128 SMs 4x48KB in flight", 0, 128, size_t(2) << 30, 1, 4, 3, 0},
+        {"L2 148 SMs 1x16KB in flight", 0, sms, size_t(32) << 20, 1, 1, 1, 0},
+        {"L2 148 SMs 2x16KB in flight", 0, sms, size_t(32) << 20, 1, 2, 1, 0},
+        {"L2 148 SMs 2x32KB in flight", 0, sms, size_t(32) << 20, 1, 2, 2, 0},
     };
     for (auto& c : cases) {
         const uint64_t total_rows = c.footprint / 128;

@@ -208,10 +208,8 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
                   const DevInfo& d, int dev, cudaStream_t stream) {
     KParams p = p_in;
     p.trace = t_trace;
-    if (t_trace) {
-        const char* e = getenv("BLR_DBG");
-        p.dbg = e ? atoi(e) : 0;
-    }
+    if (const char* e = getenv("BLR_DBG")) p.dbg = atoi(e);  // debug experiments only
+    if (const char* e = getenv("BLR_DBG_LAUNCH"); e && atoi(e) != t_last_launches) p.dbg = 0;  // only launch k
     if (t_trace) t_trace += 128 * 256;  // next launch traces into the next slot
     auto kfn = blr::blr_gemm_kernel<KIND, PAIR>;
     const blr::SmemLayout L = blr::smem_layout(p);
@@ -228,6 +226,12 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     int grid = static_cast<int>(std::min<int64_t>(p.total_tiles, units)) * PAIR;
     if (p.b_resident && p.cps > 0) grid = p.groups * p.tiles_n * p.cps * PAIR;
     else if (p.b_resident) grid = std::min(units, p.groups * p.tiles_n) * PAIR;  // slice round-robin
+    if (const char* pe = getenv("BLR_PLAN"); pe && pe[0] == '1')
+        fprintf(stderr,
+                "[blr plan] kind=%d pair=%d grid=%d tiles=%dx%dx%d BN=%d kblk=%d kbox=%d stages=%d res=%d cps=%d "
+                "bufs=%d acc=%d cbox=%d smem=%d\n",
+                KIND, PAIR, grid, p.tiles_m, p.groups, p.tiles_n, p.BN, p.k_blocks, p.kbox, p.stages, p.b_resident,
+                p.cps, p.stage_bufs, p.acc_bufs, p.c_box_w, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(blr::NUM_THREADS);
@@ -474,10 +478,18 @@ blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int comp = comp_factor(r);
     // S1: Z = X V  (V is [d_in][r]: MN-major B); Z rows [hi | lo] when compensated
+    if (const char* e = getenv("BLR_DBG_SKIP_S1"); e && e[0] == '1') {  // debug: S3 only
+        ++t_last_launches;
+    } else
     s = gemm_phase(d, dev, st, X, 0, d_in, 0, n_tok, d_in, 1, r, V, true,
                    OutMap{workspace, 0, comp, r, r, r * comp}, 1);
     if (s != BLR_OK) return s;
     // S3: Y = Z U  (U is [r][d_out]: MN-major B)
+    if (const char* e = getenv("BLR_DBG_DOUBLE"); e && e[0] == '1') {  // debug: run S3 twice
+        s = gemm_phase(d, dev, st, workspace, 0, r * comp, 0, n_tok, r, 1, d_out, U, true,
+                       OutMap{Y, 0, 1, d_out, d_out, d_out}, comp);
+        if (s != BLR_OK) return s;
+    }
     return gemm_phase(d, dev, st, workspace, 0, r * comp, 0, n_tok, r, 1, d_out, U, true,
                       OutMap{Y, 0, 1, d_out, d_out, d_out}, comp);
 }

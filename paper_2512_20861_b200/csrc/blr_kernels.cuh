@@ -77,12 +77,18 @@ struct KParams {
     int r;                 // BLAST: rank
     const __nv_bfloat16* S;  // BLAST: S [b1][b2][r]
     unsigned long long* trace;  // debug: per-CTA %globaltimer stamps [grid][64] (nullptr = off)
-    int dbg;                    // debug bits (0 in production): 1 skip epilogue bulk stores, 2 skip staging
+    int dbg;                    // debug bits (0 in production): 1 skip bulk stores, 2 skip staging,
+                                //   4 skip the whole GEMM epilogue, 8 skip MMAs, 16 plain-arrive slot release (PAIR 1),
+                                //   32 no accumulator hand-off, 64 no resident weight loads
 };
 
 struct SmemLayout {
-    uint32_t a_off, b_off, c_off, s_off, bar_off, total;
+    uint32_t a_off, b_off, c_off, s_off, bar_off, tab_off, total;
 };
+// Per-CTA tile table: the coordinates of the CTA's first TILE_TAB tiles, computed once by all
+// threads in the prologue, so the single-thread producer / MMA loops and the epilogue do no
+// integer division per tile (the per-tile index arithmetic of one thread measured ~0.5 us).
+constexpr int TILE_TAB = 256;
 
 __host__ __device__ inline int kb_resident(const KParams& p) {  // resident B blocks (padded to kbox)
     return (p.kb_half + p.kbox - 1) / p.kbox * p.kbox;
@@ -101,7 +107,8 @@ __host__ __device__ inline SmemLayout smem_layout(const KParams& p) {
     uint32_t s_bytes = 0;
     if (p.S != nullptr) s_bytes = p.b1 * p.b2 * p.BN * 4;
     L.bar_off = (L.s_off + s_bytes + 15) & ~15u;
-    L.total = L.bar_off + 8 * (2 * MAX_STAGES + 6 + MAX_BRES) + 16;
+    L.tab_off = L.bar_off + 8 * (2 * MAX_STAGES + 6 + MAX_BRES) + 16;
+    L.total = L.tab_off + TILE_TAB * 8;
     return L;
 }
 
@@ -156,6 +163,31 @@ __device__ __forceinline__ int tile_at(const KParams& p, const TileIter& t, int 
     }
     const int sl = t.unit + (it / p.tiles_m) * t.units;  // slice round-robin in passes
     return sl < t.slices ? sl * p.tiles_m + it % p.tiles_m : -1;
+}
+// Number of tiles of this CTA's sequence (tile_at(it) >= 0 exactly for it < tile_count).
+__device__ __forceinline__ int tile_count(const KParams& p, const TileIter& t) {
+    if (!p.b_resident) return t.unit < p.total_tiles ? (p.total_tiles - t.unit + t.units - 1) / t.units : 0;
+    if (p.cps > 0) {
+        const int part = t.unit / t.slices;
+        return ((part + 1) * p.tiles_m) / p.cps - (part * p.tiles_m) / p.cps;
+    }
+    return t.unit < t.slices ? (t.slices - t.unit + t.units - 1) / t.units * p.tiles_m : 0;
+}
+__device__ __forceinline__ uint2 tile_pack(const TileCoord& c) {
+    return make_uint2(static_cast<uint32_t>(c.m_blk), (static_cast<uint32_t>(c.g) << 16) | static_cast<uint32_t>(c.n_blk));
+}
+// Coordinates of this CTA's tile `it` (< tile_count): from the table, else computed.
+__device__ __forceinline__ TileCoord tile_get(const KParams& p, const TileIter& t, const uint2* tab, int it) {
+    if (it < TILE_TAB) {
+        const uint2 e = tab[it];
+        TileCoord c;
+        c.m_blk = static_cast<int>(e.x);
+        c.g = static_cast<int>(e.y >> 16);
+        c.n_blk = static_cast<int>(e.y & 0xFFFFu);
+        c.slice = p.b_resident ? c.g * p.tiles_n + c.n_blk : -1;
+        return c;
+    }
+    return tile_coord(p, tile_at(p, t, it));
 }
 
 // Stage 8 fp32 values (one 16-B chunk `chunk` of row `row`) as bf16 RNE into a row-major staging
@@ -231,7 +263,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t crank = PAIR == 2 ? ptx::cluster_ctarank() : 0u;  // rank within the pair
     const bool leader = crank == 0;
     unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 128 : nullptr;
-    if (trace && threadIdx.x == 0) trace[0] = ptx::globaltimer();
+    // trace stamps: [0] %globaltimer at entry, [8] %clock64 at entry; every other stamp is a
+    // %clock64 value (cheap; converted on the host with the SM clock)
+    if (trace && threadIdx.x == 0) {
+        trace[0] = ptx::globaltimer();
+        trace[8] = clock64();
+    }
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
@@ -253,23 +290,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if constexpr (PAIR == 2) ptx::tmem_alloc_pair<TMEM_COLS>(ptx::smem_u32(tmem_slot));
         else ptx::tmem_alloc<TMEM_COLS>(ptx::smem_u32(tmem_slot));
     }
+    const TileIter titer = tile_iter(p, PAIR);
+    const int ntiles = tile_count(p, titer);
+    uint2* tile_tab = reinterpret_cast<uint2*>(smem + L.tab_off);
+    for (int e = threadIdx.x; e < ntiles && e < TILE_TAB; e += NUM_THREADS)
+        tile_tab[e] = tile_pack(tile_coord(p, tile_at(p, titer, e)));
     ptx::tc_fence_before();
     __syncthreads();
     if constexpr (PAIR == 2) ptx::cluster_sync();  // peer barriers initialised before any remote use
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     const uint32_t acc_stride = static_cast<uint32_t>(p.n_sub * p.BN);  // columns per buffer
-    if (trace && threadIdx.x == 0) trace[1] = ptx::globaltimer();
+    if (trace && threadIdx.x == 0) trace[1] = clock64();
     // Programmatic dependent launch: everything above overlapped the previous kernel's tail.
     // Roles that read the previous kernel's output (producer: A) or write outputs it may still
     // read (epilogue) call griddep_wait() first; the producer prefetches the resident weight
     // slice -- never written by a previous kernel -- before waiting.
     ptx::griddep_launch_dependents();
-    const TileIter titer = tile_iter(p, PAIR);
 
     if (warp == 0) {
         // ===================================================== TMA producer =================
-        if (lane == 0) {
+        // The whole warp runs the (warp-uniform) schedule so that the compiler keeps coordinates
+        // and addresses in uniform registers; one elected lane issues each TMA.  (A lone-lane
+        // loop forces per-instruction ELECT/broadcast sequences and measured ~3x slower.)
+        {
             const uint32_t a_blk = BM * BK * 2;  // one 64-wide K block of A (16 KB)
             // per-CTA bytes; a pair's leader expects both CTAs' bytes on its barrier
             const uint32_t b_bytes = p.b_mn_major ? p.b_boxes * p.b_box_n * BK * 2
@@ -284,14 +328,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 else ptx::tma_load_4d(dst, m, bar, c0, c1, c2, c3);
             };
             const int n_steps = (p.k_blocks + p.kbox - 1) / p.kbox;
+            const int kbr = (p.dbg & 64) ? 0 : kb_resident(p);  // dbg 64: no weight loads
             int stage = 0;
             uint32_t phase = 0;
             int cur_slice = -1;
             uint32_t nslices = 0;
             bool waited = false;
             int nstep_tr = 0;
-            for (int it = 0, tile; (tile = tile_at(p, titer, it)) >= 0; ++it) {
-                const TileCoord tc = tile_coord(p, tile);
+            for (int it = 0; it < ntiles; ++it) {
+                const TileCoord tc = tile_get(p, titer, tile_tab, it);
                 const int m0 = (tc.m_blk * PAIR + static_cast<int>(crank)) * BM;
                 const int n0 = tc.n_blk * p.BN + static_cast<int>(crank) * (p.BN / PAIR);  // this CTA's B half
                 // Monarch: first output block k of this CTA's share of the tile's k blocks
@@ -299,69 +344,75 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (p.b_resident && tc.slice != cur_slice) {
                     // (re)load the weight slice once for the contiguous run of token tiles
                     if (nslices > 0) ptx::mbar_wait(bfree_bar, (nslices - 1) & 1);
-                    const int kbr = kb_resident(p);
-                    for (int kb = 0; kb < kbr; ++kb) {
-                        const uint32_t b_dst = b_base + kb * p.b_stage_bytes;
-                        const uint32_t bb = bfull_bar + 8 * kb;  // per-block barrier: MMA starts early
-                        if (leader) ptx::mbar_arrive_expect_tx(bb, b_bytes * PAIR);
-                        const int k0 = kb * BK;
-                        if constexpr (KIND == KIND_MONARCH_PROJ) {
-                            load4(b_dst, &tmB, bb, k0, 0, kblk0, tc.g);
-                        } else if (p.b_mn_major) {
-                            for (int j = 0; j < p.b_boxes; ++j)
-                                load3(b_dst + j * (p.b_box_n * BK * 2), &tmB, bb, n0 + j * p.b_box_n, k0, tc.g);
-                        } else {
-                            load3(b_dst, &tmB, bb, k0, n0, tc.g);
+                    if (ptx::elect_one()) {
+                        for (int kb = 0; kb < kbr; ++kb) {
+                            const uint32_t b_dst = b_base + kb * p.b_stage_bytes;
+                            const uint32_t bb = bfull_bar + 8 * kb;  // per-block barrier: MMA starts early
+                            if (leader) ptx::mbar_arrive_expect_tx(bb, b_bytes * PAIR);
+                            const int k0 = kb * BK;
+                            if constexpr (KIND == KIND_MONARCH_PROJ) {
+                                load4(b_dst, &tmB, bb, k0, 0, kblk0, tc.g);
+                            } else if (p.b_mn_major) {
+                                for (int j = 0; j < p.b_boxes; ++j)
+                                    load3(b_dst + j * (p.b_box_n * BK * 2), &tmB, bb, n0 + j * p.b_box_n, k0, tc.g);
+                            } else {
+                                load3(b_dst, &tmB, bb, k0, n0, tc.g);
+                            }
                         }
                     }
+                    __syncwarp();
                     cur_slice = tc.slice;
                     ++nslices;
                 }
                 if (!waited) {
                     ptx::griddep_wait();  // A (activations / intermediate) comes from the previous kernel
                     waited = true;
-                    if (trace) trace[2] = ptx::globaltimer();
+                    if (trace && lane == 0) trace[2] = clock64();
                 }
                 for (int sub = 0; sub < p.n_sub; ++sub) {
                     for (int si = 0; si < n_steps; ++si) {
                         ptx::mbar_wait(empty_bar + 8 * stage, phase ^ 1);
                         const uint32_t fb = full_bar + 8 * stage;
-                        if (leader) ptx::mbar_arrive_expect_tx(fb, tx);
-                        if (trace && nstep_tr < 32) trace[64 + nstep_tr] = ptx::globaltimer();
-                        ++nstep_tr;
                         const uint32_t a_st = a_base + stage * (a_blk * p.kbox);
                         const uint32_t b_st = b_base + stage * (p.b_stage_bytes * p.kbox);
-                        for (int j = 0; j < p.kbox; ++j) {
-                            const int kb = si * p.kbox + j;
-                            const uint32_t a_dst = a_st + j * a_blk;
-                            const uint32_t b_dst = b_st + j * p.b_stage_bytes;
-                            // compensated A: blocks >= kb_half read the lo half against the same B rows
-                            const int part = (p.a_lo_off > 0 && kb >= p.kb_half) ? 1 : 0;
-                            const int k0 = (kb - part * p.kb_half) * BK;  // padded block: k0 >= K, zero-filled
-                            if constexpr (KIND == KIND_GEMM) {
-                                if (p.a_gmid)
-                                    load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, tc.g, m0);
-                                else
-                                    load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, m0, tc.g);
-                                if (!p.b_resident) {
-                                    if (p.b_mn_major) {
-                                        for (int q = 0; q < p.b_boxes; ++q)
-                                            load3(b_dst + q * (p.b_box_n * BK * 2), &tmB, fb, n0 + q * p.b_box_n, k0, tc.g);
-                                    } else {
-                                        load3(b_dst, &tmB, fb, k0, n0, tc.g);
+                        if (ptx::elect_one()) {
+                            if (leader) ptx::mbar_arrive_expect_tx(fb, tx);
+                            if (trace && nstep_tr < 32) trace[64 + nstep_tr] = clock64();
+                            for (int j = 0; j < p.kbox; ++j) {
+                                const int kb = si * p.kbox + j;
+                                const uint32_t a_dst = a_st + j * a_blk;
+                                const uint32_t b_dst = b_st + j * p.b_stage_bytes;
+                                // compensated A: blocks >= kb_half read the lo half against the same B rows
+                                const int part = (p.a_lo_off > 0 && kb >= p.kb_half) ? 1 : 0;
+                                const int k0 = (kb - part * p.kb_half) * BK;  // padded block: k0 >= K, zero-filled
+                                if constexpr (KIND == KIND_GEMM) {
+                                    if (p.a_gmid)
+                                        load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, tc.g, m0);
+                                    else
+                                        load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, m0, tc.g);
+                                    if (!p.b_resident) {
+                                        if (p.b_mn_major) {
+                                            for (int q = 0; q < p.b_boxes; ++q)
+                                                load3(b_dst + q * (p.b_box_n * BK * 2), &tmB, fb, n0 + q * p.b_box_n, k0,
+                                                      tc.g);
+                                        } else {
+                                            load3(b_dst, &tmB, fb, k0, n0, tc.g);
+                                        }
                                     }
+                                } else if constexpr (KIND == KIND_MONARCH_PROJ) {
+                                    // A = X viewed [n_tok][b1][p]; B = V viewed 4-D (a, rho', k, l)
+                                    load3(a_dst, &tmA, fb, k0, tc.g, m0);
+                                    if (!p.b_resident) load4(b_dst, &tmB, fb, k0, 0, kblk0, tc.g);
+                                } else {  // KIND_BLAST_PROJ: sub = l
+                                    ptx::tma_load_3d(a_dst, &tmA, fb, k0, sub, m0);
+                                    for (int q = 0; q < p.b_boxes; ++q)
+                                        ptx::tma_load_3d(b_dst + q * (p.b_box_n * BK * 2), &tmB, fb,
+                                                         n0 + q * p.b_box_n, k0, sub);
                                 }
-                            } else if constexpr (KIND == KIND_MONARCH_PROJ) {
-                                // A = X viewed [n_tok][b1][p]; B = V viewed 4-D (a, rho', k, l)
-                                load3(a_dst, &tmA, fb, k0, tc.g, m0);
-                                if (!p.b_resident) load4(b_dst, &tmB, fb, k0, 0, kblk0, tc.g);
-                            } else {  // KIND_BLAST_PROJ: sub = l
-                                ptx::tma_load_3d(a_dst, &tmA, fb, k0, sub, m0);
-                                for (int q = 0; q < p.b_boxes; ++q)
-                                    ptx::tma_load_3d(b_dst + q * (p.b_box_n * BK * 2), &tmB, fb,
-                                                     n0 + q * p.b_box_n, k0, sub);
                             }
                         }
+                        __syncwarp();
+                        ++nstep_tr;
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -369,17 +420,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
     } else if (warp == 1) {
         // ===================================================== MMA issuer ===================
-        if (lane == 0 && leader) {
+        // Warp-wide schedule (uniform registers); one elected lane issues the MMAs and commits.
+        if (leader) {
             const uint32_t idesc = ptx::idesc_bf16(BM * PAIR, p.BN, p.b_mn_major);
             auto commit = [&](uint32_t bar) {
                 if constexpr (PAIR == 2) ptx::mma_commit_pair(bar);  // arrives in both CTAs
                 else ptx::mma_commit(bar);
             };
             // descriptors are built once; per-MMA only the 14-bit start-address field advances
+            // (a 32-bit add on the low word: the field never carries out)
             const uint64_t a_desc0 = ptx::smem_desc(a_base, 16, 1024, ptx::LAYOUT_SW128);
             const uint64_t b_desc0 = ptx::smem_desc(b_base, p.b_lbo, p.b_sbo, p.b_layout);
+            const uint32_t a_lo0 = static_cast<uint32_t>(a_desc0), a_hi = static_cast<uint32_t>(a_desc0 >> 32);
+            const uint32_t b_lo0 = static_cast<uint32_t>(b_desc0), b_hi = static_cast<uint32_t>(b_desc0 >> 32);
             const uint32_t a_blk = BM * BK * 2;
             const int n_steps = (p.k_blocks + p.kbox - 1) / p.kbox;
+            const int kbr = kb_resident(p);
+            const bool wait_b = p.b_resident && !(p.dbg & 64);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -387,56 +444,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int cur_slice = -1;
             uint32_t nslices = 0;
             int mstep_tr = 0;
-            for (int it = 0, tile; (tile = tile_at(p, titer, it)) >= 0; ++it) {
-                const TileCoord tc = tile_coord(p, tile);
+            for (int it = 0; it < ntiles; ++it) {
+                const TileCoord tc = tile_get(p, titer, tile_tab, it);
                 bool fresh = false;  // first tile of a new resident slice: wait per B block
                 if (p.b_resident && tc.slice != cur_slice) {
                     cur_slice = tc.slice;
                     ++nslices;
                     fresh = true;
                 }
-                ptx::mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
+                if (!(p.dbg & 32)) ptx::mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
                 ptx::tc_fence_after();
                 for (int sub = 0; sub < p.n_sub; ++sub) {
                     const uint32_t d_tmem = tmem_base + acc * acc_stride + sub * p.BN;
                     for (int si = 0; si < n_steps; ++si) {
                         ptx::mbar_wait(full_bar + 8 * stage, phase);
-                        ptx::tc_fence_after();
-                        if (trace) {
-                            if (trace[3] == 0) trace[3] = ptx::globaltimer();
-                            if (mstep_tr < 32) trace[96 + mstep_tr] = ptx::globaltimer();
-                            ++mstep_tr;
-                        }
-                        for (int j = 0; j < p.kbox; ++j) {
-                            const int kb = si * p.kbox + j;
-                            const int bkb = (p.a_lo_off > 0 && kb >= p.kb_half) ? kb - p.kb_half : kb;
-                            if (fresh && kb < kb_resident(p)) ptx::mbar_wait(bfull_bar + 8 * bkb, (nslices - 1) & 1);
-                            const uint32_t a_off = stage * (a_blk * p.kbox) + j * a_blk;
-                            const uint32_t b_off = p.b_resident ? bkb * p.b_stage_bytes
-                                                                : stage * (p.b_stage_bytes * p.kbox) + j * p.b_stage_bytes;
-#pragma unroll
-                            for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-                                // A: K-major, 128-B swizzle, 8-row groups 1024 B apart; +32 B per K=16.
-                                const uint64_t ad = a_desc0 + ((a_off + kk * 32) >> 4);
-                                const uint64_t bd = b_desc0 + ((b_off + kk * p.b_kstep) >> 4);
-                                if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
-                                else ptx::mma_bf16(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
+                        if (fresh && wait_b) {  // this step's resident B blocks have landed
+                            for (int j = 0; j < p.kbox; ++j) {
+                                const int kb = si * p.kbox + j;
+                                const int bkb = (p.a_lo_off > 0 && kb >= p.kb_half) ? kb - p.kb_half : kb;
+                                if (kb < kbr) ptx::mbar_wait(bfull_bar + 8 * bkb, (nslices - 1) & 1);
                             }
                         }
-                        commit(empty_bar + 8 * stage);  // frees the smem slot (both CTAs of a pair)
+                        ptx::tc_fence_after();
+                        if (ptx::elect_one()) {
+                            if (trace) {
+                                if (mstep_tr == 0) trace[3] = clock64();
+                                if (mstep_tr < 32) trace[96 + mstep_tr] = clock64();
+                            }
+                            for (int j = 0; j < p.kbox; ++j) {
+                                const int kb = si * p.kbox + j;
+                                const int bkb = (p.a_lo_off > 0 && kb >= p.kb_half) ? kb - p.kb_half : kb;
+                                const uint32_t a_off = stage * (a_blk * p.kbox) + j * a_blk;
+                                const uint32_t b_off = p.b_resident ? bkb * p.b_stage_bytes
+                                                                    : stage * (p.b_stage_bytes * p.kbox) + j * p.b_stage_bytes;
+#pragma unroll
+                                for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                                    // A: K-major, 128-B swizzle, 8-row groups 1024 B apart; +32 B per K=16.
+                                    const uint64_t ad = ptx::desc_make(a_lo0 + ((a_off + kk * 32) >> 4), a_hi);
+                                    const uint64_t bd = ptx::desc_make(b_lo0 + ((b_off + kk * p.b_kstep) >> 4), b_hi);
+                                    if (p.dbg & 8) continue;  // debug: skip the MMA itself
+                                    if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
+                                    else ptx::mma_bf16(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
+                                }
+                            }
+                            if (p.dbg & 16) ptx::mbar_arrive(empty_bar + 8 * stage);  // debug: plain release
+                            else commit(empty_bar + 8 * stage);  // frees the smem slot (both CTAs of a pair)
+                        }
+                        __syncwarp();
+                        ++mstep_tr;
                         if (++stage == p.stages) { stage = 0; phase ^= 1; }
                     }
                 }
-                commit(tfull_bar + 8 * acc);  // accumulator ready for the epilogue(s)
-                if (trace) {
-                    trace[4] = ptx::globaltimer();
-                    if (it < 24) trace[16 + it] = trace[4];  // per-tile MMA issue-complete time
+                const bool last_of_slice =
+                    p.b_resident && (it + 1 >= ntiles || tile_get(p, titer, tile_tab, it + 1).slice != cur_slice);
+                if (ptx::elect_one()) {
+                    commit(tfull_bar + 8 * acc);  // accumulator ready for the epilogue(s)
+                    if (last_of_slice) commit(bfree_bar);
+                    if (trace) {
+                        trace[4] = clock64();
+                        if (it < 24) trace[16 + it] = trace[4];  // per-tile MMA issue-complete time
+                    }
                 }
+                __syncwarp();
                 if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
-                if (p.b_resident) {
-                    const int nt = tile_at(p, titer, it + 1);
-                    if (nt < 0 || tile_coord(p, nt).slice != cur_slice) commit(bfree_bar);
-                }
             }
         }
     } else {
@@ -453,8 +523,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t acc_phase = 0;
         uint32_t nstore = 0;  // staged chunks written by this warp (buffer rotation)
         ptx::griddep_wait();  // our stores must not overtake the previous kernel's reads
-        for (int it = 0, tile; (tile = tile_at(p, titer, it)) >= 0; ++it) {
-            const TileCoord tc = tile_coord(p, tile);
+        for (int it = 0; !(p.dbg & 32) && it < ntiles; ++it) {
+            const TileCoord tc = tile_get(p, titer, tile_tab, it);
             const int m0 = (tc.m_blk * PAIR + static_cast<int>(crank)) * BM;
             const int row0 = m0 + quarter * 32;
             const int n0 = tc.n_blk * p.BN;
@@ -530,7 +600,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
             } else {
-                const int nvalid = min(p.BN, p.N - n0);
+                const int nvalid = (p.dbg & 4) ? 0 : min(p.BN, p.N - n0);  // dbg 4: empty epilogue
                 const int parts = p.out_lo_off > 0 ? 2 : 1;
                 // column chunks of CW elements; chunk j of this warp starts at col = (half + 2 j) * CW
                 const int CW = p.c_box_w;
@@ -580,7 +650,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
             }
-            if (trace && ew == 0 && lane == 0 && it < 24) trace[40 + it] = ptx::globaltimer();  // epilogue done
+            if (trace && ew == 0 && lane == 0 && it < 24) trace[40 + it] = clock64();  // epilogue done
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -589,16 +659,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
         }
-        if (trace && ew == 0 && lane == 0) trace[5] = ptx::globaltimer();
+        if (trace && ew == 0 && lane == 0) trace[5] = clock64();
         if (lane == 0) ptx::bulk_wait<0>();
         __syncwarp();
-        if (trace && ew == 0 && lane == 0) trace[6] = ptx::globaltimer();
+        if (trace && ew == 0 && lane == 0) trace[6] = clock64();
     }
 
     ptx::tc_fence_before();
     __syncthreads();
     if constexpr (PAIR == 2) ptx::cluster_sync();  // the peer's MMAs / remote arrivals are done
-    if (trace && threadIdx.x == 0) trace[7] = ptx::globaltimer();
+    if (trace && threadIdx.x == 0) trace[7] = clock64();
     if (warp == 1) {
         ptx::tc_fence_after();
         if constexpr (PAIR == 2) ptx::tmem_dealloc_pair<TMEM_COLS>(tmem_base);

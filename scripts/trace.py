@@ -22,8 +22,22 @@ X = synth.make_x(n, L.i, device=dev)
 run(X); run(X); torch.cuda.synchronize()
 buf = torch.zeros(4 * 256 * 128, dtype=torch.int64, device=dev)
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev); flush.zero_()
+fmode = os.environ.get("TRACE_FLUSH", "zero")  # zero: dirty L2 (bench default) | read: clean L2 | none
+if fmode == "read":
+    torch.cuda.synchronize(); flush.view(torch.float32).sum()
+elif fmode == "none":
+    run(X)
 lib.blr_debug_trace(buf.data_ptr()); run(X); lib.blr_debug_trace(None); torch.cuda.synchronize()
-t = buf.view(4, 256, 128).cpu()
+t = buf.view(4, 256, 128).cpu().clone()
+# stamps other than [0] (globaltimer ns) and [8] (clock64 at entry) are clock64 values
+ghz = float(os.environ.get("TRACE_GHZ", "1.92"))
+for k in range(4):
+    for c in range(256):
+        row = t[k, c]
+        if row[0] == 0: continue
+        for f in range(1, 128):
+            if f != 8 and row[f] != 0:
+                row[f] = row[0] + int((int(row[f]) - int(row[8])) / ghz)
 print(f"{L.model}.{L.name}.{L.method} n={n}")
 for k in range(4):
     tk = t[k]; ctas = tk[:, 0] > 0
@@ -31,6 +45,7 @@ for k in range(4):
     tk = tk[ctas].double(); t0 = tk[:, 0].min()
     rel = (tk - t0) / 1000.0  # us
     names = ["entry", "setup", "gdwait", "1stfull", "lastmma", "epidone", "drained", "exit"]
+    if os.environ.get("TRACE_BRIEF"): names = ["gdwait", "lastmma", "drained"]
     print(f" launch {k}: {int(ctas.sum())} CTAs; us since first CTA entry (min/med/max):")
     for c, nm in enumerate(names):
         col = rel[:, c][tk[:, c] > 0]
