@@ -660,7 +660,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
         }
         if (trace && ew == 0 && lane == 0) trace[5] = clock64();
-        if (lane == 0) ptx::bulk_wait<0>();
+        // only the staging smem must outlive the stores: wait for their smem reads, not for the
+        // global writes (those complete with the grid, before any dependent grid proceeds)
+        if (lane == 0) ptx::bulk_wait_read<0>();
         __syncwarp();
         if (trace && ew == 0 && lane == 0) trace[6] = clock64();
     }
