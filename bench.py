@@ -404,6 +404,9 @@ def main():
             "traffic": traffic, "kernel": f"{phase_kind(Ld, phase)} ({Ld.model}.{Ld.name}.{Ld.method} {phase})",
             "algorithmic_bytes": alg["bytes"], "algorithmic_flops": alg["flops"], "launch_ms": launch_ms[jmax],
             "share_of_step": launch_ms[jmax] / t_ms, "peak_source": peaks.get("source", "measured")}
+    io = phase_io_bytes(Ld, n, phase)
+    roof["kernel_io_bytes"] = io  # incl. the intermediate this design moves
+    roof["kernel_io_gbs"] = io / dt_s / 1e9
 
     # ---- cuBLAS dense bf16 comparator on the same shapes (X @ W, W reconstructed once)
     dense = None
@@ -463,6 +466,25 @@ def phase_counts(L, n, phase):
         return {"bytes": B * (n * L.i + pb), "flops": fl}
     fl = 2 * n * L.r * L.o
     return {"bytes": B * (L.r * L.o + n * L.o), "flops": fl}
+
+
+def phase_io_bytes(L, n, phase):
+    """Bytes the phase's kernel must move in this implementation: its inputs and outputs
+    including the intermediate it reads or writes (the compensated hi|lo intermediate counts
+    twice; the BLAST split path's S1 output is fp32).  Context for the fused-roofline figure."""
+    B = roofline.BF16
+    k3 = L.r if L.method != "monarch" else L.b1 * L.r_blk      # S3 contraction length
+    comp = 2 if k3 < 128 else 1
+    inter = n * L.r * comp if L.method == "lowrank" else (n * L.b * L.r * comp if L.method == "monarch"
+                                                          else n * L.b2 * L.r * comp)
+    x_v = n * L.i + L.i * L.r
+    if phase == "s1":
+        return B * x_v + 4 * n * L.b1 * L.r
+    if phase == "s2":
+        return 4 * n * L.b1 * L.r + B * (L.b1 * L.b2 * L.r + inter)
+    if phase == "proj":
+        return B * (x_v + inter + (L.b1 * L.b2 * L.r if L.method == "blast" else 0))
+    return B * (inter + L.r * L.o + n * L.o)
 
 
 def profiled_traffic(L, phase, cfg_key):
