@@ -62,6 +62,78 @@ __global__ void __launch_bounds__(512, 1) k(int iters, unsigned long long* out, 
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
 }
 
+
+// Emulates the BLAST fused epilogue's TMEM access: 8 warps (2 per lane quarter), each walks
+// W=32 columns in 8-column steps; per step it loads b1=6 blocks (columns l*BN + col) in batches
+// of 4 x8 loads per wait, and sums them (no smem).
+__global__ void __launch_bounds__(320, 1) blast_like(int reps, int b1, int BN, unsigned long long* out, float* sink,
+                                                     int mma_first) {
+    __shared__ uint32_t slot;
+    __shared__ __align__(8) uint64_t bar;
+    extern __shared__ __align__(1024) uint8_t dsm[];
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    if (mma_first && threadIdx.x == 32) {  // write the accumulators with the tensor core first
+        const uint32_t a = (smem_u32(dsm) + 1023) & ~1023u;
+        auto desc = [](uint32_t addr) {
+            uint64_t d = (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)64 << 32) | (1ull << 46) | (2ull << 61);
+            return d;
+        };
+        const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+        for (int h = 0; h < 2; ++h)
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 0, 0;\n\t"
+                         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(slot + 256 * h),
+                         "l"(desc(a)), "l"(desc(a + 16384)), "r"(idesc));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0,1,0,p; }"
+                         : "=r"(ok) : "r"(smem_u32(&bar)));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    float acc = 0.f;
+    unsigned long long t0 = clock64();
+    if (warp >= 2) {
+        const int ew = warp - 2, quarter = warp & 3, half = ew >> 2;
+        const uint32_t tbase = slot + ((uint32_t)(quarter * 32) << 16);
+        const int W = BN / 2;
+        for (int r = 0; r < reps; ++r)
+            for (int sc = 0; sc < W / 8; ++sc) {
+                const int col = half * W + sc * 8;
+                for (int lb = 0; lb < b1; lb += 4) {
+                    uint32_t z[4][8];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (lb + j < b1) ld<8>(tbase + (lb + j) * BN + col, z[j]);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if (lb + j < b1)
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) acc += __uint_as_float(z[j][e]);
+                }
+            }
+    }
+    unsigned long long t1 = clock64();
+    __syncthreads();
+    if (threadIdx.x == 64) out[blockIdx.x] = t1 - t0;
+    sink[blockIdx.x * 320 + threadIdx.x] = acc;
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
+}
+
 template <int X>
 void run(int warps) {
     unsigned long long* d;
@@ -84,6 +156,22 @@ void run(int warps) {
 }
 
 int main() {
+    {
+        unsigned long long* d;
+        float* sink;
+        cudaMalloc(&d, 8 * 148);
+        cudaMalloc(&sink, 4 * 148 * 320);
+        cudaFuncSetAttribute(blast_like, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        for (int mf = 0; mf <= 1; ++mf) {
+            for (int rep = 0; rep < 2; ++rep) blast_like<<<148, 320, 64 * 1024>>>(100, 6, 64, d, sink, mf);
+            cudaDeviceSynchronize();
+            unsigned long long h;
+            cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+            printf("blast-like epilogue loads (b1=6, BN=64, 8 warps, %s): %.0f clk per 8-column step (%s)\n",
+                   mf ? "TMEM written by tcgen05.mma first" : "TMEM never written", double(h) / (100 * 4),
+                   cudaGetErrorString(cudaGetLastError()));
+        }
+    }
     for (int w : {4, 8, 16}) {
         run<8>(w);
         run<32>(w);

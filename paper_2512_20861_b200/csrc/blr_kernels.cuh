@@ -177,9 +177,9 @@ __device__ __forceinline__ uint2 tile_pack(const TileCoord& c) {
     return make_uint2(static_cast<uint32_t>(c.m_blk), (static_cast<uint32_t>(c.g) << 16) | static_cast<uint32_t>(c.n_blk));
 }
 // Coordinates of this CTA's tile `it` (< tile_count): from the table, else computed.
-__device__ __forceinline__ TileCoord tile_get(const KParams& p, const TileIter& t, const uint2* tab, int it) {
+__device__ __forceinline__ TileCoord tile_get(const KParams& p, const TileIter& t, uint32_t tab, int it) {
     if (it < TILE_TAB) {
-        const uint2 e = tab[it];
+        const uint2 e = ptx::ld_shared_v2u32(tab + 8u * it);
         TileCoord c;
         c.m_blk = static_cast<int>(e.x);
         c.g = static_cast<int>(e.y >> 16);
@@ -248,7 +248,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t a_base = sbase + L.a_off;
     const uint32_t b_base = sbase + L.b_off;
-    float* s_tile = reinterpret_cast<float*>(smem + L.s_off);
+    // S tile (BLAST fused epilogue), addressed through the shared window explicitly: a generic
+    // pointer here compiled to generic LD.E loads with global-load latency (3 us per 8 columns)
+    const uint32_t s_tile = sbase + L.s_off;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bar_off);
     const uint32_t full_bar = ptx::smem_u32(bars);
     const uint32_t empty_bar = full_bar + 8 * MAX_STAGES;
@@ -292,9 +294,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     const TileIter titer = tile_iter(p, PAIR);
     const int ntiles = tile_count(p, titer);
-    uint2* tile_tab = reinterpret_cast<uint2*>(smem + L.tab_off);
+    const uint32_t tile_tab = sbase + L.tab_off;  // explicit shared-window addressing (see s_tile)
     for (int e = threadIdx.x; e < ntiles && e < TILE_TAB; e += NUM_THREADS)
-        tile_tab[e] = tile_pack(tile_coord(p, tile_at(p, titer, e)));
+        ptx::st_shared_v2u32(tile_tab + 8u * e, tile_pack(tile_coord(p, tile_at(p, titer, e))));
     ptx::tc_fence_before();
     __syncthreads();
     if constexpr (PAIR == 2) ptx::cluster_sync();  // peer barriers initialised before any remote use
@@ -536,12 +538,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     const int rho = e % p.BN;
                     const int lk = e / p.BN;
                     const int rr = n0 + rho;
-                    s_tile[e] = rr < p.r ? __bfloat162float(p.S[static_cast<long long>(lk) * p.r + rr]) : 0.f;
+                    ptx::st_shared_f32(s_tile + 4u * e,
+                                       rr < p.r ? __bfloat162float(p.S[static_cast<long long>(lk) * p.r + rr]) : 0.f);
                 }
                 ptx::named_bar_sync(1, 32 * NUM_EPI_WARPS);
+                if (trace && ew == 0 && lane == 0 && it == 0) trace[9] = clock64();
             }
             ptx::mbar_wait(tfull_bar + 8 * acc, acc_phase);
             ptx::tc_fence_after();
+            if (trace && ew == 0 && lane == 0 && it == 0) trace[10] = clock64();
             const uint32_t tbase = tmem_base + acc * acc_stride + lane_addr;
 
             if constexpr (KIND == KIND_BLAST_PROJ) {
@@ -556,41 +561,56 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     __syncwarp();
                     for (int sc = 0; sc < W / 8; ++sc) {
                         const int col = half * W + sc * 8;  // column within the tile
-                        unsigned long long acc2[16][4];
+                        // output blocks k in groups of 8 (64 accumulator registers), inputs l in
+                        // batches of 4 TMEM loads per wait (the loads' latency is paid once per
+                        // batch, not once per l)
+                        for (int kb0 = 0; kb0 < p.b2; kb0 += 8) {
+                            unsigned long long acc2[8][4];
 #pragma unroll
-                        for (int k = 0; k < 16; ++k)
+                            for (int k = 0; k < 8; ++k)
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) acc2[k][e] = 0ull;
-                        for (int l = 0; l < p.b1; ++l) {
-                            float z[8];
-                            ptx::tmem_ld_x8(tbase + l * p.BN + col, z);
-                            ptx::tmem_wait_ld();
-                            unsigned long long z2[4];
+                                for (int e = 0; e < 4; ++e) acc2[k][e] = 0ull;
+                            for (int lb = 0; lb < p.b1; lb += 4) {
+                                float z[4][8];
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) z2[e] = ptx::pack_f32x2(z[2 * e], z[2 * e + 1]);
-                            const float* srow = s_tile + (l * p.b2) * p.BN + col;
+                                for (int j = 0; j < 4; ++j)
+                                    if (lb + j < p.b1) ptx::tmem_ld_x8(tbase + (lb + j) * p.BN + col, z[j]);
+                                ptx::tmem_wait_ld();
+                                if (trace && ew == 0 && lane == 0 && it == 0 && sc == 0 && lb == 0) trace[12] = clock64();
 #pragma unroll
-                            for (int k = 0; k < 16; ++k) {
-                                if (k < p.b2) {
-                                    const ulonglong2 sa = *reinterpret_cast<const ulonglong2*>(srow + k * p.BN);
-                                    const ulonglong2 sb = *reinterpret_cast<const ulonglong2*>(srow + k * p.BN + 4);
-                                    ptx::ffma2(acc2[k][0], sa.x, z2[0]);
-                                    ptx::ffma2(acc2[k][1], sa.y, z2[1]);
-                                    ptx::ffma2(acc2[k][2], sb.x, z2[2]);
-                                    ptx::ffma2(acc2[k][3], sb.y, z2[3]);
+                                for (int j = 0; j < 4; ++j) {
+                                    if (lb + j < p.b1) {
+                                        unsigned long long z2[4];
+#pragma unroll
+                                        for (int e = 0; e < 4; ++e) z2[e] = ptx::pack_f32x2(z[j][2 * e], z[j][2 * e + 1]);
+                                        const uint32_t srow = s_tile + 4u * (((lb + j) * p.b2 + kb0) * p.BN + col);
+#pragma unroll
+                                        for (int k = 0; k < 8; ++k) {
+                                            if (kb0 + k < p.b2) {
+                                                const ulonglong2 sa = ptx::ld_shared_v2u64(srow + 4u * k * p.BN);
+                                                const ulonglong2 sb = ptx::ld_shared_v2u64(srow + 4u * k * p.BN + 16u);
+                                                ptx::ffma2(acc2[k][0], sa.x, z2[0]);
+                                                ptx::ffma2(acc2[k][1], sa.y, z2[1]);
+                                                ptx::ffma2(acc2[k][2], sb.x, z2[2]);
+                                                ptx::ffma2(acc2[k][3], sb.y, z2[3]);
+                                            }
+                                        }
+                                    }
+                                }
+                            }
+#pragma unroll
+                            for (int k = 0; k < 8; ++k) {
+                                if (kb0 + k < p.b2) {
+                                    float f[8];
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) ptx::unpack_f32x2(acc2[k][e], f[2 * e], f[2 * e + 1]);
+                                    stage_row8(stg + (kb0 + k) * kstride, lane, sc, row_bytes, p.c_swz, f, part);
                                 }
                             }
                         }
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) {
-                            if (k < p.b2) {
-                                float f[8];
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) ptx::unpack_f32x2(acc2[k][e], f[2 * e], f[2 * e + 1]);
-                                stage_row8(stg + k * kstride, lane, sc, row_bytes, p.c_swz, f, part);
-                            }
-                        }
+                        if (trace && ew == 0 && lane == 0 && it == 0 && sc < 2) trace[13 + sc] = clock64();
                     }
+                    if (trace && ew == 0 && lane == 0 && it == 0) trace[11] = clock64();
                     ptx::fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {

@@ -53,6 +53,8 @@ for k in range(4):
     c0 = tk[0]
     mm = [(c0[16 + i] - t0).item() / 1000 for i in range(24) if c0[16 + i] > 0]
     ep = [(c0[40 + i] - t0).item() / 1000 for i in range(24) if c0[40 + i] > 0]
+    extra = [(c0[f] - t0).item() / 1000 for f in (9, 10, 12, 13, 14, 11) if c0[f] > 0]
+    if extra: print("   CTA0 epilogue tile0 (S staged / tfull / 1st ld / sc0 / sc1 / computed) us:", " ".join(f"{v:.2f}" for v in extra))
     print("   CTA0 per-tile MMA-commit us:", " ".join(f"{v:.2f}" for v in mm))
     print("   CTA0 per-tile epilogue-done us:", " ".join(f"{v:.2f}" for v in ep))
     pi = [(c0[64 + i] - t0).item() / 1000 for i in range(32) if c0[64 + i] > 0]
