@@ -340,8 +340,9 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     } else if (force != 1) {
         if (!plan_gemm(p, 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp)) return BLR_ERR_UNSUPPORTED;
         // a CTA pair halves each CTA's streamed weight bytes; worth its coupling only when a
-        // tile's B (K x BN) outweighs its A (BM x K), i.e. BN > BM
-        if (!p.b_resident && n_tok >= 1024 && p.BN > blr::BM) pair = 2;
+        // tile's B (K x BN) is about twice its A (BM x K), i.e. full-width BN = 256 tiles
+        // (measured: GPT2-S BLAST c_proj S1 with BN = 192 is faster unpaired)
+        if (!p.b_resident && n_tok >= 1024 && p.BN >= 2 * blr::BM) pair = 2;
     }
     if (!plan_gemm(p, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp)) {
         if (pair == 1 || !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp))
@@ -690,7 +691,9 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        // S2 is launched without programmatic dependent launch: its blocks, started early on the
+        // few SMs the S1 grid leaves idle, measured ~4 us slower per GPT2-S layer
+        attr[0].val.programmaticStreamSerializationAllowed = 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
