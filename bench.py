@@ -195,8 +195,23 @@ def cpu_baseline(w, target_s=10.0):
     dt = run(rows)
     rows = int(max(16, min(w.n, rows * target_s / max(dt, 1e-3))))
     dt = run(rows)
-    return {"value": rows * len(chains) / dt, "unit": "tokens/s", "cores": orc.num_threads(), "kind": "oracle",
-            "sample": f"{rows} token rows of {w.key} through every layer ({dt:.1f} s fp64 on host)"}
+    # single-thread figure on a smaller sample (report the 1-thread run too)
+    cores = orc.num_threads()
+    orc.set_num_threads(1)
+    rows1 = max(4, rows // max(1, cores) // 4)
+    dt1 = run(rows1)
+    orc.set_num_threads(0)
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"value": rows * len(chains) / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+            "sample": f"{rows} token rows of {w.key} through every layer ({dt:.1f} s fp64 on host)",
+            "single_thread_value": rows1 * len(chains) / dt1, "cpu_model": model}
 
 
 # ------------------------------------------------------------------------------- main bench ---
@@ -366,6 +381,17 @@ def main():
 
     step_ms = [a.elapsed_time(b) for a, b in step_ev]
     t_ms = sum(step_ms) / K
+    srt = sorted(step_ms)
+    step_stats = {"mean": t_ms, "median": srt[len(srt) // 2], "min": srt[0],
+                  "p90": srt[min(len(srt) - 1, int(0.9 * len(srt)))]}
+    # warm-L2 figure (no flush between steps), reported separately
+    wev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(min(K, 10))]
+    for a, b in wev:
+        a.record(stream)
+        run_step()
+        b.record(stream)
+    torch.cuda.synchronize()
+    step_stats["warm_l2_mean"] = sum(a.elapsed_time(b) for a, b in wev) / len(wev)
     launch_ms = [v / K for v in launch_tot]
     if ws > 1:
         from paper_2512_20861_b200 import dist as bdist
@@ -425,7 +451,8 @@ def main():
                        "l2": "flushed between timed steps (write of 2x L2), outside the step events",
                        "launch": "eager" if args.eager else "CUDA graph replay of the step (both arms)",
                        "parallelism": f"token-sharded dp{ws}, no data-path collective"},
-            "roofline": roof, "per_layer": per_layer, "ms_per_step_with_launch_events": prof_step_ms, "gpu_launches": launches,
+            "roofline": roof, "per_layer": per_layer, "ms_per_step_stats": step_stats,
+            "ms_per_step_with_launch_events": prof_step_ms, "gpu_launches": launches,
             "clocks": sampler.summary(), "e2e": e2e}
     if dense is not None:
         line["cublas_dense_bf16"] = dense

@@ -190,3 +190,16 @@ int orc_num_threads(void)
     return 1;
 #endif
 }
+
+/* Thread count for subsequent calls (timing only: the arithmetic and its order per output element
+   do not depend on it).  n <= 0 restores the OpenMP default. */
+void orc_set_num_threads(int n)
+{
+#ifdef _OPENMP
+    extern void omp_set_num_threads(int);
+    extern int omp_get_num_procs(void);
+    omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+#else
+    (void)n;
+#endif
+}

@@ -47,6 +47,7 @@ def _load():
         lib.orc_blast_weight.argtypes = [i64, i64, i64, i64, i64, dp, dp, dp, dp]
         lib.orc_blast_forward.argtypes = [i64, i64, i64, i64, i64, i64, dp, dp, dp, dp, dp, dp]
         lib.orc_num_threads.restype = ctypes.c_int
+        lib.orc_set_num_threads.argtypes = [ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -62,6 +63,11 @@ def _p(a: np.ndarray):
 
 def num_threads() -> int:
     return int(_load().orc_num_threads())
+
+
+def set_num_threads(n: int) -> None:
+    """Thread count of later calls (timing only; results do not depend on it). n <= 0: default."""
+    _load().orc_set_num_threads(int(n))
 
 
 # ---------------------------------------------------------------- dense ------------------------

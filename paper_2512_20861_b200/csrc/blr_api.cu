@@ -680,9 +680,9 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         const int in = static_cast<int>(n_tok), ib1 = static_cast<int>(b1), ib2 = static_cast<int>(b2),
                   ir = static_cast<int>(r);
         cudaLaunchConfig_t cfg = {};
-        // rows per block: ~2 resident blocks per SM over the whole grid, multiple of 16
+        // rows per block: ~3 blocks per SM over the whole grid, multiple of 16
         const int64_t chunks = cdiv(r, 64);
-        const int64_t target_blocks = 2LL * d.sm_count;
+        const int64_t target_blocks = 3LL * d.sm_count;  // measured best of 1..8 per SM (GPT2-S)
         const int rpb = static_cast<int>(std::max<int64_t>(blr::S2_ROWS,
                                           rup(cdiv(n_tok * chunks, target_blocks), blr::S2_ROWS)));
         cfg.gridDim = dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(cdiv(n_tok, rpb)));
