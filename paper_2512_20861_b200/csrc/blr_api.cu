@@ -12,6 +12,7 @@
 
 #include "../../include/blr.h"
 #include "blr_kernels.cuh"
+#include "blr_decode.cuh"
 
 namespace {
 
@@ -403,6 +404,178 @@ bool encode_x_blocked(CUtensorMap* m, const void* X, int64_t n_tok, int64_t b1, 
     return encode(m, X, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// ------------------------------------------------------------------ decode (small n) path ----
+// Small n runs the weight-streaming CUDA-core kernels of blr_decode.cuh up to a
+// per-method token count where they measured faster than the tcgen05 path (scripts/decode_bench.py,
+// profiles/r01_decode.txt): LR n <= 4, BLAST n <= 2, Monarch never by default.  BLR_DECODE=1
+// forces the decode path for every n <= DECODE_MAX_TOKENS, BLR_DECODE=0 disables it (tests cover
+// both paths at every small n).
+bool use_decode(int64_t n_tok, int64_t default_max) {
+    if (n_tok > blr::DECODE_MAX_TOKENS) return false;
+    const char* e = getenv("BLR_DECODE");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    return n_tok <= default_max;
+}
+constexpr int64_t DECODE_TARGET_BLOCKS = 2 * 148;  // fixed (workspace sizes must not query the device)
+
+struct MNPlan {
+    int splits, k_chunk;
+};
+MNPlan mn_plan(int64_t K, int64_t N, int64_t groups) {
+    const int64_t blocks = cdiv(N, blr::DECODE_MN_COLS) * groups;
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(cdiv(DECODE_TARGET_BLOCKS, blocks), cdiv(K, 64)));
+    const int64_t kc = rup(cdiv(K, splits), 8);
+    splits = cdiv(K, kc);
+    return {static_cast<int>(splits), static_cast<int>(kc)};
+}
+size_t mn_part_bytes(int64_t n_tok, int64_t K, int64_t N, int64_t groups) {
+    const MNPlan pl = mn_plan(K, N, groups);
+    return pl.splits > 1 ? static_cast<size_t>(pl.splits) * groups * n_tok * N * 4 : 0;
+}
+inline int decode_nt(int64_t n_tok) { return n_tok <= 4 ? 4 : n_tok <= 8 ? 8 : 16; }
+
+size_t lowrank_decode_ws(int64_t n, int64_t i, int64_t o, int64_t r) {
+    return static_cast<size_t>(n) * r * 4 + std::max(mn_part_bytes(n, i, r, 1), mn_part_bytes(n, r, o, 1));
+}
+size_t blast_decode_ws(int64_t n, int64_t i, int64_t o, int64_t b1, int64_t b2, int64_t r) {
+    return static_cast<size_t>(b1 + b2) * n * r * 4 +
+           std::max(mn_part_bytes(n, i / b1, r, b1), mn_part_bytes(n, r, o / b2, b2));
+}
+size_t monarch_decode_ws(int64_t n, int64_t b1, int64_t b2, int64_t r_blk) {
+    return static_cast<size_t>(b2) * n * b1 * r_blk * 4;
+}
+
+template <typename K, typename P>
+blr_status decode_launch(K kfn, dim3 grid, size_t smem, const P& prm, cudaStream_t st) {
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT) != cudaSuccess)
+        return BLR_ERR_CUDA;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(blr::DECODE_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+    if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, kfn, prm) != cudaSuccess) return BLR_ERR_CUDA;
+    if (prof) {
+        if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+        ++t_prof_n;
+    }
+    ++t_last_launches;
+    return BLR_OK;
+}
+
+// out[g][t][c] = sum_k A[g][t][k] B[g][k][c], B MN-major; split-K through `part` when planned.
+blr_status decode_mn(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int64_t a_gs, const void* B,
+                     int64_t b_rs, int64_t b_gs, void* out, int out_bf16, int64_t o_rs, int64_t o_gs, int64_t n,
+                     int64_t K, int64_t N, int64_t groups, float* part) {
+    const MNPlan pl = mn_plan(K, N, groups);
+    blr::DecodeMN d = {};
+    d.A = A;
+    d.a_f32 = a_f32;
+    d.a_rs = a_rs;
+    d.a_gs = a_gs;
+    d.B = static_cast<const __nv_bfloat16*>(B);
+    d.b_rs = b_rs;
+    d.b_gs = b_gs;
+    d.n_tok = static_cast<int>(n);
+    d.K = static_cast<int>(K);
+    d.N = static_cast<int>(N);
+    d.k_chunk = pl.k_chunk;
+    if (pl.splits > 1) {  // fp32 partials [split][g][t][c], reduced below in a fixed order
+        d.out = part;
+        d.out_bf16 = 0;
+        d.o_rs = N;
+        d.o_gs = n * N;
+        d.o_zs = groups * n * N;
+    } else {
+        d.out = out;
+        d.out_bf16 = out_bf16;
+        d.o_rs = o_rs;
+        d.o_gs = o_gs;
+        d.o_zs = 0;
+    }
+    const int nt = decode_nt(n);
+    const size_t smem = static_cast<size_t>(nt) * std::max<int>(pl.k_chunk, 4 * blr::DECODE_MN_COLS) * 4;
+    const dim3 grid(static_cast<unsigned>(cdiv(N, blr::DECODE_MN_COLS)), static_cast<unsigned>(groups),
+                    static_cast<unsigned>(pl.splits));
+    blr_status s = nt == 4    ? decode_launch(blr::decode_mn_kernel<4>, grid, smem, d, st)
+                   : nt == 8 ? decode_launch(blr::decode_mn_kernel<8>, grid, smem, d, st)
+                             : decode_launch(blr::decode_mn_kernel<16>, grid, smem, d, st);
+    if (s != BLR_OK || pl.splits == 1) return s;
+    struct RedArgs {
+        const float* part;
+        int splits, groups, n_tok, N;
+        void* out;
+        int out_bf16;
+        long long o_rs, o_gs;
+    };
+    cudaLaunchConfig_t cfg = {};
+    const int64_t count = groups * n * N;
+    cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(cdiv(count, blr::DECODE_THREADS), 4 * 148)));
+    cfg.blockDim = dim3(blr::DECODE_THREADS);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+    if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, blr::decode_reduce, static_cast<const float*>(part), pl.splits,
+                           static_cast<int>(groups), static_cast<int>(n), static_cast<int>(N), out, out_bf16,
+                           static_cast<long long>(o_rs), static_cast<long long>(o_gs)) != cudaSuccess)
+        return BLR_ERR_CUDA;
+    if (prof) {
+        if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+        ++t_prof_n;
+    }
+    ++t_last_launches;
+    return BLR_OK;
+}
+
+// out[g][t][c] = sum_k A[g][t][k] B[g][c][k], B K-major (one warp per output column).
+blr_status decode_k(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int64_t a_gs, const void* B,
+                    int64_t b_rs, int64_t b_gs, void* out, int out_bf16, int64_t o_rs, int64_t o_gs, int64_t n,
+                    int64_t K, int64_t N, int64_t groups, int col_map, int64_t mon_b2, int64_t mon_r) {
+    blr::DecodeK d = {};
+    d.A = A;
+    d.a_f32 = a_f32;
+    d.a_rs = a_rs;
+    d.a_gs = a_gs;
+    d.B = static_cast<const __nv_bfloat16*>(B);
+    d.b_rs = b_rs;
+    d.b_gs = b_gs;
+    d.out = out;
+    d.out_bf16 = out_bf16;
+    d.o_rs = o_rs;
+    d.o_gs = o_gs;
+    d.n_tok = static_cast<int>(n);
+    d.K = static_cast<int>(K);
+    d.N = static_cast<int>(N);
+    d.col_map = col_map;
+    d.mon_b2 = static_cast<int>(mon_b2);
+    d.mon_r = static_cast<int>(mon_r);
+    // enough blocks for the SMs, >= 64 columns per block (the A stage is re-read per block)
+    int64_t cpb = std::max<int64_t>(64, rup(cdiv(N * groups, DECODE_TARGET_BLOCKS), 8));
+    cpb = std::min<int64_t>(cpb, rup(N, 8));
+    d.cols_per_block = static_cast<int>(cpb);
+    const int nt = decode_nt(n);
+    const size_t smem = static_cast<size_t>(nt) * K * 4;
+    if (smem + 1024 > static_cast<size_t>(SMEM_LIMIT)) return BLR_ERR_UNSUPPORTED;
+    const dim3 grid(static_cast<unsigned>(cdiv(N, cpb)), static_cast<unsigned>(groups));
+    return nt == 4   ? decode_launch(blr::decode_k_kernel<4>, grid, smem, d, st)
+           : nt == 8 ? decode_launch(blr::decode_k_kernel<8>, grid, smem, d, st)
+                     : decode_launch(blr::decode_k_kernel<16>, grid, smem, d, st);
+}
+
 size_t blast_ws_bytes(int64_t n_tok, int64_t b1, int64_t b2, int64_t r) {
     const size_t zpp = static_cast<size_t>(b2) * n_tok * r * 2 * comp_factor(r);
     if (blast_fused(b1, r)) return zpp;
@@ -454,16 +627,27 @@ void blr_clear_cache(void) {
     g_encode = nullptr;
 }
 
-size_t blr_lowrank_workspace_size(int64_t n_tok, int64_t, int64_t, int64_t r) {
-    return (n_tok > 0 && r > 0) ? static_cast<size_t>(n_tok) * r * 2 * comp_factor(r) : 0;
+// Workspace: the tcgen05 path's intermediate; for n_tok <= DECODE_MAX_TOKENS also enough for the
+// decode path's fp32 intermediates and split-K partials (either path may run: BLR_DECODE=0).
+size_t blr_lowrank_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, int64_t r) {
+    if (n_tok <= 0 || r <= 0) return 0;
+    size_t b = static_cast<size_t>(n_tok) * r * 2 * comp_factor(r);
+    if (n_tok <= blr::DECODE_MAX_TOKENS && d_in > 0 && d_out > 0)
+        b = std::max(b, lowrank_decode_ws(n_tok, d_in, d_out, r));
+    return b;
 }
 size_t blr_monarch_workspace_size(int64_t n_tok, int64_t, int64_t, int64_t b1, int64_t b2, int64_t r_blk) {
-    return (n_tok > 0 && b1 > 0 && b2 > 0 && r_blk > 0)
-               ? static_cast<size_t>(b2) * n_tok * b1 * r_blk * 2 * comp_factor(b1 * r_blk)
-               : 0;
+    if (n_tok <= 0 || b1 <= 0 || b2 <= 0 || r_blk <= 0) return 0;
+    size_t b = static_cast<size_t>(b2) * n_tok * b1 * r_blk * 2 * comp_factor(b1 * r_blk);
+    if (n_tok <= blr::DECODE_MAX_TOKENS) b = std::max(b, monarch_decode_ws(n_tok, b1, b2, r_blk));
+    return b;
 }
-size_t blr_blast_workspace_size(int64_t n_tok, int64_t, int64_t, int64_t b1, int64_t b2, int64_t r) {
-    return (n_tok > 0 && b1 > 0 && b2 > 0 && r > 0) ? blast_ws_bytes(n_tok, b1, b2, r) : 0;
+size_t blr_blast_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2, int64_t r) {
+    if (n_tok <= 0 || b1 <= 0 || b2 <= 0 || r <= 0) return 0;
+    size_t b = blast_ws_bytes(n_tok, b1, b2, r);
+    if (n_tok <= blr::DECODE_MAX_TOKENS && d_in > 0 && d_out > 0 && d_in % b1 == 0 && d_out % b2 == 0)
+        b = std::max(b, blast_decode_ws(n_tok, d_in, d_out, b1, b2, r));
+    return b;
 }
 
 blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t r,
@@ -482,20 +666,19 @@ blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     blr_status s = device_info(d, dev);
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (use_decode(n_tok, 4)) {  // weight-streaming small-n path, fp32 Z [n][r]
+        float* zf = static_cast<float*>(workspace);
+        float* part = zf + n_tok * r;
+        s = decode_mn(st, X, 0, d_in, 0, V, r, 0, zf, 0, r, 0, n_tok, d_in, r, 1, part);
+        if (s != BLR_OK) return s;
+        return decode_mn(st, zf, 1, r, 0, U, d_out, 0, Y, 1, d_out, 0, n_tok, r, d_out, 1, part);
+    }
     const int comp = comp_factor(r);
     // S1: Z = X V  (V is [d_in][r]: MN-major B); Z rows [hi | lo] when compensated
-    if (const char* e = getenv("BLR_DBG_SKIP_S1"); e && e[0] == '1') {  // debug: S3 only
-        ++t_last_launches;
-    } else
     s = gemm_phase(d, dev, st, X, 0, d_in, 0, n_tok, d_in, 1, r, V, true,
                    OutMap{workspace, 0, comp, r, r, r * comp}, 1);
     if (s != BLR_OK) return s;
     // S3: Y = Z U  (U is [r][d_out]: MN-major B)
-    if (const char* e = getenv("BLR_DBG_DOUBLE"); e && e[0] == '1') {  // debug: run S3 twice
-        s = gemm_phase(d, dev, st, workspace, 0, r * comp, 0, n_tok, r, 1, d_out, U, true,
-                       OutMap{Y, 0, 1, d_out, d_out, d_out}, comp);
-        if (s != BLR_OK) return s;
-    }
     return gemm_phase(d, dev, st, workspace, 0, r * comp, 0, n_tok, r, 1, d_out, U, true,
                       OutMap{Y, 0, 1, d_out, d_out, d_out}, comp);
 }
@@ -520,6 +703,13 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     blr_status s = device_info(d, dev);
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (use_decode(n_tok, 0)) {  // small-n path: fp32 Z' [b2][n][b1 r'], permutations in the index maps
+        float* zp = static_cast<float*>(workspace);
+        s = decode_k(st, X, 0, d_in, pdim, V, pdim, r_blk * b2 * pdim, zp, 0, K2, n_tok * K2, n_tok, pdim,
+                     r_blk * b2, b1, v_layout == BLR_MON_V_B2_FASTEST ? 1 : 2, b2, r_blk);
+        if (s != BLR_OK) return s;
+        return decode_k(st, zp, 1, K2, n_tok * K2, U, K2, qdim * K2, Y, 1, d_out, qdim, n_tok, K2, qdim, b2, 0, 1, 1);
+    }
     const int comp = comp_factor(K2);
 
     // ---- phase 1: Z'[k][t][l r' + rho] = (X_l V_{l,k})[t, rho]  (block-diagonal S1 + permutations)
@@ -622,6 +812,37 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
     blr_status s = device_info(d, dev);
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (use_decode(n_tok, 2)) {  // small-n path: fp32 Z [b1][n][r] and Z'' [b2][n][r]
+        float* z = static_cast<float*>(workspace);
+        float* zp2 = z + b1 * n_tok * r;
+        float* part = zp2 + b2 * n_tok * r;
+        s = decode_mn(st, X, 0, d_in, pdim, V, r, pdim * r, z, 0, r, n_tok * r, n_tok, pdim, r, b1, part);
+        if (s != BLR_OK) return s;
+        {
+            cudaLaunchConfig_t cfg = {};
+            const int64_t count = b2 * n_tok * r;
+            cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(cdiv(count, blr::DECODE_THREADS), 4 * 148)));
+            cfg.blockDim = dim3(blr::DECODE_THREADS);
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+            if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+            if (cudaLaunchKernelEx(&cfg, blr::decode_s2_kernel, static_cast<const float*>(z),
+                                   static_cast<const __nv_bfloat16*>(S), zp2, static_cast<int>(n_tok),
+                                   static_cast<int>(b1), static_cast<int>(b2), static_cast<int>(r)) != cudaSuccess)
+                return BLR_ERR_CUDA;
+            if (prof) {
+                if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+                ++t_prof_n;
+            }
+            ++t_last_launches;
+        }
+        return decode_mn(st, zp2, 1, r, n_tok * r, U, qdim, r * qdim, Y, 1, d_out, qdim, n_tok, r, qdim, b2, part);
+    }
     const int comp = comp_factor(r);
     void* zpp = workspace;  // Z'' [b2][n][r*comp]
 

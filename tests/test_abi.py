@@ -55,6 +55,17 @@ def test_workspace_sizes():
     assert lib.blr_blast_workspace_size(0, 64, 64, 4, 2, 16) == 0
 
 
+def test_workspace_sizes_cover_the_decode_path():
+    """n <= 16 (decode path): fp32 intermediates (+ split-K partials) must fit too."""
+    lib = blr.load()
+    n, i, o, r = 8, 4096, 11008, 1488
+    assert lib.blr_lowrank_workspace_size(n, i, o, r) >= n * r * 4          # fp32 Z
+    assert lib.blr_blast_workspace_size(n, i, o, 16, 16, r) >= (16 + 16) * n * r * 4  # fp32 Z, Z''
+    assert lib.blr_monarch_workspace_size(n, i, o, 16, 16, 96) >= 16 * n * 16 * 96 * 4  # fp32 Z'
+    # above the decode threshold only the tcgen05 path's bf16 intermediate is needed
+    assert lib.blr_lowrank_workspace_size(17, i, o, r) == 17 * r * 2
+
+
 FAKE = 0x10000  # 16-B aligned, never dereferenced: validation fails before any CUDA call
 
 
