@@ -60,3 +60,68 @@ def test_gloo_world2_shard_gather_and_max():
     res = sorted(q.get(timeout=10) for _ in range(world))
     assert all(ok for _, ok, _ in res)
     assert all(t == 2.0 for _, _, t in res)  # max over ranks of (1 + rank)
+
+
+# ------------------------------------------- output-block sharding, host logic --
+def _blast_dense_ref(X, V, S, U):
+    """fp64 reference through the oracle (the GPU kernels replace this on a device)."""
+    from oracle import oracle as orc
+    return torch.from_numpy(orc.blast_forward(X.numpy(), V.numpy(), S.numpy(), U.numpy()))
+
+
+def _worker_cols(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(3)
+        n, b1, b2, r, p, qd = 5, 3, 5, 8, 4, 6   # b2 = 5 blocks over 2 ranks: uneven split
+        X = torch.randn(n, b1 * p, generator=g, dtype=torch.float64)
+        V = torch.randn(b1, p, r, generator=g, dtype=torch.float64)
+        S = torch.randn(b1, b2, r, generator=g, dtype=torch.float64)
+        U = torch.randn(b2, r, qd, generator=g, dtype=torch.float64)
+
+        def local(k0, k1):
+            Vl, Sl, Ul = bdist.blast_local_factors(V, S, U, k0, k1)
+            if k1 == k0:
+                return torch.zeros((n, 0), dtype=torch.float64)
+            return _blast_dense_ref(X, Vl, Sl, Ul)
+
+        y = bdist.output_sharded_forward(local, b2, qd)
+        ok = torch.allclose(y, _blast_dense_ref(X, V, S, U), rtol=1e-12, atol=1e-12)
+        q.put((rank, ok, tuple(y.shape)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_output_block_sharded_blast():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_cols, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    assert all(ok for _, ok, _ in res), res
+    assert all(shape == (5, 30) for _, _, shape in res)
+
+
+def test_monarch_local_factors_select_the_block_rows():
+    """The V rows of output blocks [k0, k1) in both layouts (pure index bookkeeping)."""
+    from oracle import oracle as orc
+    b1, b2, rp, p, qd, n = 2, 4, 3, 5, 6, 3
+    g = torch.Generator().manual_seed(4)
+    X = torch.randn(n, b1 * p, generator=g, dtype=torch.float64)
+    V = torch.randn(b1, rp * b2, p, generator=g, dtype=torch.float64)
+    U = torch.randn(b2, qd, b1 * rp, generator=g, dtype=torch.float64)
+    for layout in (orc.B2_FASTEST, orc.RPRIME_FASTEST):
+        full = orc.monarch_forward(X.numpy(), V.numpy(), U.numpy(), b1, b2, layout)
+        for k0, k1 in ((0, 1), (1, 3), (2, 4)):
+            Vl, Ul = bdist.monarch_local_factors(V, U, b2, rp, k0, k1, layout)
+            part = orc.monarch_forward(X.numpy(), Vl.numpy(), Ul.numpy(), b1, k1 - k0, layout)
+            assert abs(part - full[:, k0 * qd:k1 * qd]).max() < 1e-12, (layout, k0, k1)
+
