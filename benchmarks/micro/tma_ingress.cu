@@ -142,20 +142,11 @@ int main() {
 
     struct Case { const char* name; int mode; int grid; size_t footprint; int csize; int nst; int bps; int smem_kb; int wide = 1; };
     std::vector<Case> cases = {
-        {"HBM 148 SMs 1x16KB in flight", 0, sms, size_t(2) << 30, 1, 1, 1, 0},
-        {"HBM 148 SMs 2x16KB in flight", 0, sms, size_t(2) << 30, 1, 2, 1, 0},
-        {"HBM 148 SMs 4x16KB in flight", 0, sms, size_t(2) << 30, 1, 4, 1, 0},
-        {"HBM 148 SMs 8x16KB in flight", 0, sms, size_t(2) << 30, 1, 8, 1, 0},
-        {"HBM 148 SMs 2x32KB in flight", 0, sms, size_t(2) << 30, 1, 2, 2, 0},
-        {"HBM 148 SMs 4x32KB in flight", 0, sms, size_t(2) << 30, 1, 4, 2, 0},
-        {"HBM 148 SMs 6x32KB in flight", 0, sms, size_t(2) << 30, 1, 6, 2, 0},
-        {"HBM 64 SMs 4x32KB in flight", 0, 64, size_t(2) << 30, 1, 4, 2, 0},
-        {"HBM 64 SMs 6x32KB in flight", 0, 64, size_t(2) << 30, 1, 6, 2, 0},
-        {"HBM 64 SMs 4x48KB in flight", 0, 64, size_t(2) << 30, 1, 4, 3, 0},
-        {"HBM 128 SMs 4x48KB in flight", 0, 128, size_t(2) << 30, 1, 4, 3, 0},
-        {"L2 148 SMs 1x16KB in flight", 0, sms, size_t(32) << 20, 1, 1, 1, 0},
-        {"L2 148 SMs 2x16KB in flight", 0, sms, size_t(32) << 20, 1, 2, 1, 0},
-        {"L2 148 SMs 2x32KB in flight", 0, sms, size_t(32) << 20, 1, 2, 2, 0},
+        {"L2 32MiB 4x32KB, no cluster", 0, sms, size_t(32) << 20, 1, 4, 2, 0},
+        {"L2 multicast cluster 2, 8x16KB", 2, 148, size_t(32) << 20, 2, 8, 1, 0},
+        {"L2 multicast cluster 4, 8x16KB", 2, 148, size_t(32) << 20, 4, 8, 1, 0},
+        {"HBM 2GiB 4x32KB, no cluster", 0, sms, size_t(2) << 30, 1, 4, 2, 0},
+        {"HBM multicast cluster 2, 8x16KB", 2, 148, size_t(2) << 30, 2, 8, 1, 0},
     };
     for (auto& c : cases) {
         const uint64_t total_rows = c.footprint / 128;

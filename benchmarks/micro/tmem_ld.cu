@@ -67,10 +67,15 @@ __global__ void __launch_bounds__(512, 1) k(int iters, unsigned long long* out, 
 // W=32 columns in 8-column steps; per step it loads b1=6 blocks (columns l*BN + col) in batches
 // of 4 x8 loads per wait, and sums them (no smem).
 __global__ void __launch_bounds__(320, 1) blast_like(int reps, int b1, int BN, unsigned long long* out, float* sink,
-                                                     int mma_first) {
+                                                     int mma_first, int mode) {
+    const int b2 = b1;
+    const int lane = threadIdx.x & 31;
     __shared__ uint32_t slot;
     __shared__ __align__(8) uint64_t bar;
     extern __shared__ __align__(1024) uint8_t dsm[];
+    float* s_sm = reinterpret_cast<float*>(dsm + 49152);               // S tile [b1][b2][BN] fp32
+    uint8_t* stg_sm = dsm + 49152 + 16384;                             // staging, 8 warps x b2 x 32 x W x 2
+    for (int e = threadIdx.x; e < b1 * b2 * BN; e += blockDim.x) s_sm[e] = 0.5f + (e & 7);
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&slot)));
@@ -107,11 +112,17 @@ __global__ void __launch_bounds__(320, 1) blast_like(int reps, int b1, int BN, u
     unsigned long long t0 = clock64();
     if (warp >= 2) {
         const int ew = warp - 2, quarter = warp & 3, half = ew >> 2;
+        (void)lane;
         const uint32_t tbase = slot + ((uint32_t)(quarter * 32) << 16);
         const int W = BN / 2;
         for (int r = 0; r < reps; ++r)
             for (int sc = 0; sc < W / 8; ++sc) {
                 const int col = half * W + sc * 8;
+                unsigned long long acc2[8][4];
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) acc2[k][e] = 0ull;
                 for (int lb = 0; lb < b1; lb += 4) {
                     uint32_t z[4][8];
 #pragma unroll
@@ -119,11 +130,61 @@ __global__ void __launch_bounds__(320, 1) blast_like(int reps, int b1, int BN, u
                         if (lb + j < b1) ld<8>(tbase + (lb + j) * BN + col, z[j]);
                     asm volatile("tcgen05.wait::ld.sync.aligned;");
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        if (lb + j < b1)
+                    for (int j = 0; j < 4; ++j) {
+                        if (lb + j < b1) {
+                            if (mode & 1) {  // the BLAST epilogue's S-weighted sums (S from smem)
+                                unsigned long long z2[4];
 #pragma unroll
-                            for (int e = 0; e < 8; ++e) acc += __uint_as_float(z[j][e]);
+                                for (int e = 0; e < 4; ++e)
+                                    z2[e] = ((unsigned long long)z[j][2 * e + 1] << 32) | z[j][2 * e];
+                                const float* srow = s_sm + ((lb + j) * b2) * BN + col;
+#pragma unroll
+                                for (int k = 0; k < 8; ++k) {
+                                    if (k < b2) {
+                                        ulonglong2 sa, sb;
+                                        if (mode & 4) {  // S from registers (no shared loads)
+                                            sa = make_ulonglong2(0x3f0000003f000000ull + k, 0x3f0000003f000000ull + lb + j);
+                                            sb = make_ulonglong2(0x3f0000003f000000ull + 2 * k, 0x3f0000003f000000ull + j);
+                                        } else {
+                                            sa = *reinterpret_cast<const ulonglong2*>(srow + k * BN);
+                                            sb = *reinterpret_cast<const ulonglong2*>(srow + k * BN + 4);
+                                        }
+                                        if (mode & 8) {  // plain FFMA on the low halves instead of FFMA2
+                                            float a0 = __uint_as_float((uint32_t)acc2[k][0]);
+                                            a0 = fmaf(__uint_as_float((uint32_t)sa.x), __uint_as_float((uint32_t)z2[0]), a0);
+                                            float a1 = __uint_as_float((uint32_t)(acc2[k][0] >> 32));
+                                            a1 = fmaf(__uint_as_float((uint32_t)(sa.x >> 32)), __uint_as_float((uint32_t)(z2[0] >> 32)), a1);
+                                            acc2[k][0] = ((unsigned long long)__float_as_uint(a1) << 32) | __float_as_uint(a0);
+                                            continue;
+                                        }
+                                        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[k][0]) : "l"(sa.x), "l"(z2[0]));
+                                        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[k][1]) : "l"(sa.y), "l"(z2[1]));
+                                        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[k][2]) : "l"(sb.x), "l"(z2[2]));
+                                        asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc2[k][3]) : "l"(sb.y), "l"(z2[3]));
+                                    }
+                                }
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < 8; ++e) acc += __uint_as_float(z[j][e]);
+                            }
+                        }
+                    }
                 }
+                if (mode & 2) {  // stage b2 rows of 8 bf16 (16 B) per lane, 64-B swizzled rows
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        if (k >= b2) break;
+                        uint32_t off = lane * (W * 2) + sc * 16;
+                        off ^= ((off >> 7) & 3u) << 4;
+                        const uint32_t a = smem_u32(stg_sm) + (ew * b2 + k) * 32 * W * 2 + off;
+                        const uint32_t w0 = (uint32_t)acc2[k][0], w1 = (uint32_t)acc2[k][1], w2 = (uint32_t)acc2[k][2],
+                                       w3 = (uint32_t)acc2[k][3];
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w0), "r"(w1), "r"(w2), "r"(w3)
+                                     : "memory");
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 8; ++k) acc += __uint_as_float((uint32_t)acc2[k][0]);
             }
     }
     unsigned long long t1 = clock64();
@@ -161,16 +222,20 @@ int main() {
         float* sink;
         cudaMalloc(&d, 8 * 148);
         cudaMalloc(&sink, 4 * 148 * 320);
-        cudaFuncSetAttribute(blast_like, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-        for (int mf = 0; mf <= 1; ++mf) {
-            for (int rep = 0; rep < 2; ++rep) blast_like<<<148, 320, 64 * 1024>>>(100, 6, 64, d, sink, mf);
-            cudaDeviceSynchronize();
-            unsigned long long h;
-            cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-            printf("blast-like epilogue loads (b1=6, BN=64, 8 warps, %s): %.0f clk per 8-column step (%s)\n",
-                   mf ? "TMEM written by tcgen05.mma first" : "TMEM never written", double(h) / (100 * 4),
-                   cudaGetErrorString(cudaGetLastError()));
-        }
+        cudaFuncSetAttribute(blast_like, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        const char* names[16] = {"TMEM loads only", "+ S-weighted FFMA2 (S in smem)", "+ staging stores only",
+                                 "+ FFMA2 + staging (full epilogue body)", "", "+ FFMA2 with S in registers", "", "",
+                                 "", "+ FFMA (scalar) with S in smem", "", "", "", "+ FFMA (scalar) S in registers"};
+        for (int mode : {0, 1, 5, 9, 13, 3})
+            for (int mf = 1; mf <= 1; ++mf) {
+                for (int rep = 0; rep < 2; ++rep) blast_like<<<148, 320, 180 * 1024>>>(100, 6, 64, d, sink, mf, mode);
+                cudaDeviceSynchronize();
+                unsigned long long h;
+                cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+                printf("blast-like epilogue (b1=b2=6, BN=64, 8 warps, %s, %s): %.0f clk per 8-column step (%s)\n",
+                       names[mode], mf ? "TMEM written by tcgen05.mma" : "TMEM never written", double(h) / (100 * 4),
+                       cudaGetErrorString(cudaGetLastError()));
+            }
     }
     for (int w : {4, 8, 16}) {
         run<8>(w);
