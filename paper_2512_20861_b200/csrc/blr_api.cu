@@ -908,7 +908,10 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
                                           rup(cdiv(n_tok * chunks, target_blocks), blr::S2_ROWS)));
         cfg.gridDim = dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(cdiv(n_tok, rpb)));
         cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = static_cast<size_t>(b1 * b2 * 64 * 4 + 2 * b1 * 256 * 16);
+        // accumulators per thread: the smallest instantiated count >= b2 (S rows beyond b2 are zero)
+        const int64_t maxb = b2 <= 1 ? 1 : b2 <= 2 ? 2 : b2 <= 3 ? 3 : b2 <= 4 ? 4 : b2 <= 6 ? 6 : b2 <= 8 ? 8
+                             : b2 <= 9 ? 9 : b2 <= 12 ? 12 : 16;
+        cfg.dynamicSmemBytes = static_cast<size_t>(b1 * maxb * 64 * 4 + 2 * b1 * 256 * 16);
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -924,21 +927,28 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             std::lock_guard<std::mutex> lk(g_mu);
             if (!g_attr_set[7][dev]) {
                 const int mx = 16 * 16 * 64 * 4 + 2 * 16 * 256 * 16;
-                if (cudaFuncSetAttribute(blr::blast_s2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+                if (cudaFuncSetAttribute(blr::blast_s2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
                     cudaFuncSetAttribute(blr::blast_s2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
                     cudaFuncSetAttribute(blr::blast_s2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess)
                     return BLR_ERR_CUDA;
                 g_attr_set[7][dev] = true;
             }
         }
         cudaError_t le;
-        const int64_t bmax = std::max(b1, b2);
-        if (bmax <= 4)
-            le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<4>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb);
-        else if (bmax <= 8)
-            le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<8>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb);
-        else
-            le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<16>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb);
+        switch (maxb) {
+#define BLR_S2_CASE(KB) \
+    case KB: le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<KB>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb); break;
+            BLR_S2_CASE(1) BLR_S2_CASE(2) BLR_S2_CASE(3) BLR_S2_CASE(4) BLR_S2_CASE(6) BLR_S2_CASE(8)
+            BLR_S2_CASE(9) BLR_S2_CASE(12)
+#undef BLR_S2_CASE
+            default: le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<16>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb);
+        }
         if (le != cudaSuccess) return BLR_ERR_CUDA;
         if (cudaGetLastError() != cudaSuccess) return BLR_ERR_CUDA;
         if (prof) {

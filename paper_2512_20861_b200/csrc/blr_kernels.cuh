@@ -708,19 +708,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // Z is the unrounded fp32 S1 output; fp32 accumulation in a fixed l order and one RNE rounding
 // (plus the compensation term when comp == 2) -- the same single rounding as the fused path.
 constexpr int S2_ROWS = 16;  // rows per pass (256 threads / 16 threads per 64-rho row segment)
+// MAXB = the number of output-block accumulators per thread: the smallest instantiated size >= b2
+// (host dispatch); the S rows beyond b2 are zero.
 template <int MAXB>
 __global__ void __launch_bounds__(256)
     blast_s2_kernel(const float* __restrict__ Z, const __nv_bfloat16* __restrict__ S,
                     __nv_bfloat16* __restrict__ Zpp, int n_tok, int b1, int b2, int r, int comp,
                     int rows_per_block) {
     extern __shared__ __align__(16) float s2_smem[];
-    float* s_sm = s2_smem;                          // [b1][b2][64] fp32
-    float4* zbuf = reinterpret_cast<float4*>(s2_smem + b1 * b2 * 64);  // [2][b1][256] float4
+    // S chunk [b1][MAXB][64] fp32, zero-padded for k >= b2 so the k loop below carries no bounds
+    // branch (the compiler can batch its shared loads; FMAs on the zero rows are discarded)
+    float* s_sm = s2_smem;
+    float4* zbuf = reinterpret_cast<float4*>(s2_smem + b1 * MAXB * 64);  // [2][b1][256] float4
     const int rho_base = blockIdx.x * 64;
-    for (int v = threadIdx.x; v < b1 * b2 * 8; v += blockDim.x) {
-        const int lk = v >> 3, c8 = (v & 7) * 8;
-        float* dst = s_sm + lk * 64 + c8;
-        if (rho_base + c8 < r) {
+    for (int v = threadIdx.x; v < b1 * MAXB * 8; v += blockDim.x) {
+        const int lkp = v >> 3, c8 = (v & 7) * 8;
+        const int l = lkp / MAXB, k = lkp % MAXB;
+        const int lk = l * b2 + k;
+        float* dst = s_sm + lkp * 64 + c8;
+        if (k < b2 && rho_base + c8 < r) {
             const uint4 w = __ldg(reinterpret_cast<const uint4*>(S + static_cast<long long>(lk) * r + rho_base + c8));
             const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -761,20 +767,17 @@ __global__ void __launch_bounds__(256)
         unsigned long long acc2[MAXB][2];
 #pragma unroll
         for (int k = 0; k < MAXB; ++k) acc2[k][0] = acc2[k][1] = 0ull;
-#pragma unroll
-        for (int l = 0; l < MAXB; ++l) {
-            if (l < b1) {
+        for (int l = 0; l < b1; ++l) {
+            {
                 const float4 z = zbuf[(buf * b1 + l) * 256 + threadIdx.x];
                 const unsigned long long za = ptx::pack_f32x2(z.x, z.y);
                 const unsigned long long zb = ptx::pack_f32x2(z.z, z.w);
-                const float* srow = s_sm + (l * b2) * 64 + c4 * 4;
+                const float* srow = s_sm + (l * MAXB) * 64 + c4 * 4;
 #pragma unroll
                 for (int k = 0; k < MAXB; ++k) {
-                    if (k < b2) {
-                        const ulonglong2 sv = *reinterpret_cast<const ulonglong2*>(srow + k * 64);
-                        ptx::ffma2(acc2[k][0], sv.x, za);
-                        ptx::ffma2(acc2[k][1], sv.y, zb);
-                    }
+                    const ulonglong2 sv = *reinterpret_cast<const ulonglong2*>(srow + k * 64);
+                    ptx::ffma2(acc2[k][0], sv.x, za);
+                    ptx::ffma2(acc2[k][1], sv.y, zb);
                 }
             }
         }
