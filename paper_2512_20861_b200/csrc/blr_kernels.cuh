@@ -105,7 +105,7 @@ __host__ __device__ inline SmemLayout smem_layout(const KParams& p) {
     L.c_off = L.b_off + b_region_bytes(p);  // all multiples of 1024
     L.s_off = L.c_off + p.stage_warp_bytes * NUM_EPI_WARPS;
     uint32_t s_bytes = 0;
-    if (p.S != nullptr) s_bytes = p.b1 * p.b2 * p.BN * 4;
+    if (p.S != nullptr) s_bytes = p.b1 * ((p.b2 + 7) / 8 * 8) * p.BN * 4;  // k rows zero-padded to 8
     L.bar_off = (L.s_off + s_bytes + 15) & ~15u;
     L.tab_off = L.bar_off + 8 * (2 * MAX_STAGES + 6 + MAX_BRES) + 16;
     L.total = L.tab_off + TILE_TAB * 8;
@@ -533,13 +533,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if constexpr (KIND == KIND_BLAST_PROJ) {
                 // stage S[l][k][n0 : n0+BN] (fp32) for the S-weighted block sum
                 ptx::named_bar_sync(1, 32 * NUM_EPI_WARPS);
-                const int cnt = p.b1 * p.b2 * p.BN;
+                // k rows zero-padded to a multiple of 8: the accumulation loop below has no k bound
+                const int b2p = (p.b2 + 7) / 8 * 8;
+                const int cnt = p.b1 * b2p * p.BN;
                 for (int e = ew * 32 + lane; e < cnt; e += 32 * NUM_EPI_WARPS) {
                     const int rho = e % p.BN;
-                    const int lk = e / p.BN;
+                    const int lkp = e / p.BN;
+                    const int l = lkp / b2p, k = lkp - l * b2p;
                     const int rr = n0 + rho;
                     ptx::st_shared_f32(s_tile + 4u * e,
-                                       rr < p.r ? __bfloat162float(p.S[static_cast<long long>(lk) * p.r + rr]) : 0.f);
+                                       (k < p.b2 && rr < p.r)
+                                           ? __bfloat162float(p.S[static_cast<long long>(l * p.b2 + k) * p.r + rr])
+                                           : 0.f);
                 }
                 ptx::named_bar_sync(1, 32 * NUM_EPI_WARPS);
                 if (trace && ew == 0 && lane == 0 && it == 0) trace[9] = clock64();
@@ -583,17 +588,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                         unsigned long long z2[4];
 #pragma unroll
                                         for (int e = 0; e < 4; ++e) z2[e] = ptx::pack_f32x2(z[j][2 * e], z[j][2 * e + 1]);
-                                        const uint32_t srow = s_tile + 4u * (((lb + j) * p.b2 + kb0) * p.BN + col);
+                                        const uint32_t srow =
+                                            s_tile + 4u * (((lb + j) * ((p.b2 + 7) / 8 * 8) + kb0) * p.BN + col);
 #pragma unroll
-                                        for (int k = 0; k < 8; ++k) {
-                                            if (kb0 + k < p.b2) {
-                                                const ulonglong2 sa = ptx::ld_shared_v2u64(srow + 4u * k * p.BN);
-                                                const ulonglong2 sb = ptx::ld_shared_v2u64(srow + 4u * k * p.BN + 16u);
-                                                ptx::ffma2(acc2[k][0], sa.x, z2[0]);
-                                                ptx::ffma2(acc2[k][1], sa.y, z2[1]);
-                                                ptx::ffma2(acc2[k][2], sb.x, z2[2]);
-                                                ptx::ffma2(acc2[k][3], sb.y, z2[3]);
-                                            }
+                                        for (int k = 0; k < 8; ++k) {  // rows k >= b2 of the S tile are zero
+                                            const ulonglong2 sa = ptx::ld_shared_v2u64(srow + 4u * k * p.BN);
+                                            const ulonglong2 sb = ptx::ld_shared_v2u64(srow + 4u * k * p.BN + 16u);
+                                            ptx::ffma2(acc2[k][0], sa.x, z2[0]);
+                                            ptx::ffma2(acc2[k][1], sa.y, z2[1]);
+                                            ptx::ffma2(acc2[k][2], sb.x, z2[2]);
+                                            ptx::ffma2(acc2[k][3], sb.y, z2[3]);
                                         }
                                     }
                                 }
