@@ -13,6 +13,8 @@ echo "launch list rc=$?"
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"blr_gemm|blast_s2" -c $N \
   -o gpurun_out/prof_$CFG -f python bench.py --config $CFG --steps 1 --warmup 0 --no-dense --no-cpu-baseline --eager > gpurun_out/ncu_full_$CFG.log 2>&1
 echo "full rc=$?"
-python scripts/profile_summary.py list gpurun_out/launches_$CFG.csv profiles/${TAG}_${CFG}_launches.txt
-python scripts/profile_summary.py full gpurun_out/prof_$CFG.ncu-rep profiles/${TAG}_${CFG}_ncu_full.txt gpurun_out/phases_$CFG.json profiles/ncu_traffic_$CFG.json
-head -30 profiles/${TAG}_${CFG}_ncu_full.txt
+# summaries go to gpurun_out/ (only that directory comes back from the box); copy them into
+# profiles/ locally:  python scripts/profile_summary.py list|full ... profiles/...
+python scripts/profile_summary.py list gpurun_out/launches_$CFG.csv gpurun_out/${TAG}_${CFG}_launches.txt
+python scripts/profile_summary.py full gpurun_out/prof_$CFG.ncu-rep gpurun_out/${TAG}_${CFG}_ncu_full.txt gpurun_out/phases_$CFG.json gpurun_out/ncu_traffic_$CFG.json
+head -30 gpurun_out/${TAG}_${CFG}_ncu_full.txt
