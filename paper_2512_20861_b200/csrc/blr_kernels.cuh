@@ -272,31 +272,39 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         trace[8] = clock64();
     }
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < p.stages; ++s) {
+    if (warp == 0) {
+        // the lanes of warp 0 initialise the barriers this plan uses in parallel (a single thread
+        // initialising all of them sat on the critical path of every kernel boundary, ~1 us)
+        const int nres = p.b_resident ? kb_resident(p) : 0;
+        for (int s = lane; s < p.stages; s += 32) {
             ptx::mbar_init(full_bar + 8 * s, 1);
             ptx::mbar_init(empty_bar + 8 * s, 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            ptx::mbar_init(tfull_bar + 8 * b, 1);
-            ptx::mbar_init(tempty_bar + 8 * b, NUM_EPI_WARPS * PAIR);  // leader's: both CTAs drain
+        if (lane < 2) {
+            ptx::mbar_init(tfull_bar + 8 * lane, 1);
+            ptx::mbar_init(tempty_bar + 8 * lane, NUM_EPI_WARPS * PAIR);  // leader's: both CTAs drain
         }
-        for (int kb = 0; kb < MAX_BRES; ++kb) ptx::mbar_init(bfull_bar + 8 * kb, 1);
-        ptx::mbar_init(bfree_bar, 1);
+        for (int kb = lane; kb < nres; kb += 32) ptx::mbar_init(bfull_bar + 8 * kb, 1);
+        if (lane == 0) ptx::mbar_init(bfree_bar, 1);
         ptx::fence_barrier_init();
-        ptx::prefetch_tmap(&tmA);
-        ptx::prefetch_tmap(&tmB);
-        ptx::prefetch_tmap(&tmC);
+        if (lane == 0) {
+            ptx::prefetch_tmap(&tmA);
+            ptx::prefetch_tmap(&tmB);
+            ptx::prefetch_tmap(&tmC);
+            if (trace && KIND != KIND_BLAST_PROJ) trace[13] = clock64();
+        }
     }
     if (warp == 1) {
         if constexpr (PAIR == 2) ptx::tmem_alloc_pair<TMEM_COLS>(ptx::smem_u32(tmem_slot));
         else ptx::tmem_alloc<TMEM_COLS>(ptx::smem_u32(tmem_slot));
+        if (trace && lane == 0 && KIND != KIND_BLAST_PROJ) trace[14] = clock64();
     }
     const TileIter titer = tile_iter(p, PAIR);
     const int ntiles = tile_count(p, titer);
     const uint32_t tile_tab = sbase + L.tab_off;  // explicit shared-window addressing (see s_tile)
     for (int e = threadIdx.x; e < ntiles && e < TILE_TAB; e += NUM_THREADS)
         ptx::st_shared_v2u32(tile_tab + 8u * e, tile_pack(tile_coord(p, tile_at(p, titer, e))));
+    if (trace && threadIdx.x == 64 && KIND != KIND_BLAST_PROJ) trace[15] = clock64();
     ptx::tc_fence_before();
     __syncthreads();
     if constexpr (PAIR == 2) ptx::cluster_sync();  // peer barriers initialised before any remote use

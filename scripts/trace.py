@@ -42,7 +42,8 @@ print(f"{L.model}.{L.name}.{L.method} n={n}")
 for k in range(4):
     tk = t[k]; ctas = tk[:, 0] > 0
     if not ctas.any(): break
-    tk = tk[ctas].double(); t0 = tk[:, 0].min()
+    tk = tk[ctas].double()
+    t0 = tk[:, 0].min() if not os.environ.get("TRACE_COMMON_T0") else t[:, :, 0][t[:, :, 0] > 0].double().min()
     rel = (tk - t0) / 1000.0  # us
     names = ["entry", "setup", "gdwait", "1stfull", "lastmma", "epidone", "drained", "exit"]
     if os.environ.get("TRACE_BRIEF"): names = ["gdwait", "lastmma", "drained"]
@@ -53,6 +54,8 @@ for k in range(4):
     c0 = tk[0]
     mm = [(c0[16 + i] - t0).item() / 1000 for i in range(24) if c0[16 + i] > 0]
     ep = [(c0[40 + i] - t0).item() / 1000 for i in range(24) if c0[40 + i] > 0]
+    setup = [(tk[:, f][tk[:, f] > 0] - tk[:, 0][tk[:, f] > 0]).median().item() / 1000 for f in (13, 14, 15) if (tk[:, f] > 0).any()]
+    if setup and L.method != "blast": print("   median since own entry: barriers init / TMEM alloc / tile table us:", " ".join(f"{v:.2f}" for v in setup))
     extra = [(c0[f] - t0).item() / 1000 for f in (9, 10, 12, 13, 14, 11) if c0[f] > 0]
     if extra: print("   CTA0 epilogue tile0 (S staged / tfull / 1st ld / sc0 / sc1 / computed) us:", " ".join(f"{v:.2f}" for v in extra))
     print("   CTA0 per-tile MMA-commit us:", " ".join(f"{v:.2f}" for v in mm))
