@@ -61,11 +61,15 @@ blr_status device_info(DevInfo& out, int& dev) {
     return BLR_OK;
 }
 
-// bf16 tensor map of rank R: dims[0] innermost, strides in bytes for dims 1..R-1.
+// Tensor map of rank R (dt: 0 bf16, 1 fp32, 2 fp16): dims[0] innermost, strides in bytes for
+// dims 1..R-1.
 bool encode(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, const uint64_t* strides,
-            const uint32_t* box, CUtensorMapSwizzle sw, bool f32 = false) {
+            const uint32_t* box, CUtensorMapSwizzle sw, int dt = 0) {
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    CUresult r = g_encode(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr),
+    const CUtensorMapDataType t = dt == 1   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                  : dt == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                            : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    CUresult r = g_encode(m, t, rank, const_cast<void*>(ptr),
                           reinterpret_cast<const cuuint64_t*>(dims), reinterpret_cast<const cuuint64_t*>(strides),
                           reinterpret_cast<const cuuint32_t*>(box), estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -85,6 +89,14 @@ inline int comp_factor(int64_t k_s3) { return k_s3 < COMP_K_THRESHOLD ? 2 : 1; }
 
 // BLAST runs S1 and S2 fused (b1 TMEM accumulators per token tile) when all b1 * r columns fit
 // TMEM, so X is read once; otherwise S1 (grouped GEMM), S2 (streaming) and S3 run separately.
+// Precision of the split path's S1 output Z (R13): fp16 by default (RNE, 11-bit
+// significand: half the intermediate traffic of fp32, rounding error ~1/8 of a bf16 rounding;
+// finite range |Z| <= 65504), fp32 with BLR_BLAST_Z=f32.
+inline bool blast_z_f16() {
+    const char* e = getenv("BLR_BLAST_Z");
+    return !(e && !strcmp(e, "f32"));
+}
+
 inline bool blast_fused(int64_t b1, int64_t r) {
     const char* e = getenv("BLR_BLAST_PATH");
     if (e && !strcmp(e, "fused")) return true;
@@ -283,7 +295,7 @@ int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int sms, int pair) {
 
 struct OutMap {  // 4-D view (N, comp, groups, rows) of a GEMM phase's output
     void* ptr;
-    int f32;               // 1: fp32 output (unrounded), else bf16
+    int f32;               // output type: 0 bf16, 1 fp32 (unrounded), 2 fp16
     int64_t comp;          // 1, or 2 for a compensated [hi | lo] intermediate
     int64_t comp_stride;   // elements between hi and lo
     int64_t group_stride;  // elements between groups
@@ -317,7 +329,7 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     p.BN = bn_full;
     p.out_lo_off = out.comp == 2 ? out.comp_stride : 0;
     p.out_f32 = out.f32;
-    const int esz = out.f32 ? 4 : 2;
+    const int esz = out.f32 == 1 ? 4 : 2;
     p.c_box_w = chunk_width(p.BN);
     while (p.c_box_w * esz > 128) p.c_box_w /= 2;  // staged rows <= 128 B
     p.c_swz = pick_swz(p.c_box_w * esz).mask;
@@ -349,7 +361,7 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
         if (pair == 1 || !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp))
             return BLR_ERR_UNSUPPORTED;
     }
-    const int esz = out.f32 ? 4 : 2;
+    const int esz = out.f32 == 1 ? 4 : 2;
     const Swz cs = pick_swz(p.c_box_w * esz);
 
     CUtensorMap ta, tb, tc;
@@ -390,7 +402,7 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
         const uint64_t strb[3] = {static_cast<uint64_t>(out.comp_stride) * es, static_cast<uint64_t>(out.group_stride) * es,
                                   static_cast<uint64_t>(out.row_stride) * es};
         const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32};
-        if (!encode(&tc, out.ptr, 4, dims, strb, box, cs.mode, out.f32 != 0)) return BLR_ERR_CUDA;
+        if (!encode(&tc, out.ptr, 4, dims, strb, box, cs.mode, out.f32)) return BLR_ERR_CUDA;
     }
     if (pair == 2) return launch<blr::KIND_GEMM, 2>(ta, tb, tc, p, d, dev, st);
     return launch<blr::KIND_GEMM, 1>(ta, tb, tc, p, d, dev, st);
@@ -579,7 +591,7 @@ blr_status decode_k(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int
 size_t blast_ws_bytes(int64_t n_tok, int64_t b1, int64_t b2, int64_t r) {
     const size_t zpp = static_cast<size_t>(b2) * n_tok * r * 2 * comp_factor(r);
     if (blast_fused(b1, r)) return zpp;
-    return zpp + static_cast<size_t>(b1) * n_tok * r * 4;  // + fp32 Z_l of the separate S1
+    return zpp + static_cast<size_t>(b1) * n_tok * r * (blast_z_f16() ? 2 : 4);  // + Z_l of the separate S1
 }
 
 }  // namespace
@@ -890,28 +902,51 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         if (s != BLR_OK) return s;
     } else {
         // ---- S1: Z[l][t][rho] = (X_l V_l)[t, rho]  -- grouped GEMM over l (A = X viewed (p, b1, n))
+        const bool zh = blast_z_f16();
         void* zl = static_cast<char*>(workspace) + static_cast<size_t>(b2) * n_tok * r * 2 * comp;
         s = gemm_phase(d, dev, st, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true,
-                       OutMap{zl, 1, 1, r, n_tok * r, r}, 1);
+                       OutMap{zl, zh ? 2 : 1, 1, r, n_tok * r, r}, 1);
         if (s != BLR_OK) return s;
         // ---- S2: Z''[k][t][rho] = sum_l S[l,k,rho] Z[l][t][rho]
-        const auto* zb = static_cast<const float*>(zl);
-        const auto* sb = static_cast<const __nv_bfloat16*>(S);
-        auto* ob = static_cast<__nv_bfloat16*>(zpp);
-        const int in = static_cast<int>(n_tok), ib1 = static_cast<int>(b1), ib2 = static_cast<int>(b2),
-                  ir = static_cast<int>(r);
+        CUtensorMap tz;
+        {  // Z viewed (rho, t, l); box (64, S2_ROWS, b1): one item's b1 row segments per request
+            const uint64_t es = zh ? 2 : 4;
+            const uint64_t dims[3] = {static_cast<uint64_t>(r), static_cast<uint64_t>(n_tok), static_cast<uint64_t>(b1)};
+            const uint64_t str[2] = {static_cast<uint64_t>(r) * es, static_cast<uint64_t>(r * n_tok) * es};
+            const uint32_t box[3] = {64, static_cast<uint32_t>(blr::S2_ROWS), static_cast<uint32_t>(b1)};
+            if (!encode(&tz, zl, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, zh ? 2 : 1)) return BLR_ERR_CUDA;
+        }
+        // KG output blocks per consumer warp (S held in registers: NL x KG packed pairs per lane;
+        // NL = b1 rounded up to 4/8/16, the extra planes are zero)
+        const char* ke = getenv("BLR_S2_KG");
+        const int kg = b2 == 1 ? 1 : (ke ? std::max(1, std::min(2, atoi(ke))) : 2);
+        const int nw = static_cast<int>(cdiv(b2, kg)) * blr::S2_RSPLIT;
+        const int nl = b1 <= 4 ? 4 : b1 <= 8 ? 8 : 16;
+        const int slabs = static_cast<int>(cdiv(n_tok, blr::S2_ROWS));
+        const int nchunks = static_cast<int>(cdiv(r, 64));
+        const int total = nchunks * slabs;
+        const char* me = getenv("BLR_S2_MAP");
+        const int map_mode = me ? atoi(me) : 1;
+        const char* be = getenv("BLR_S2_BPS");
+        // blocks per SM: up to 16 consumer warps per SM (<= 128 registers per thread)
+        const int bps = be ? atoi(be) : std::max(1, std::min(4, 16 / nw));
+        int grid = std::min<int>(total, bps * d.sm_count);
+        int ipb = static_cast<int>(cdiv(total, grid));
+        if (map_mode == 1) {  // a multiple of nchunks, at most bps block-slots per SM, >= 1 per chunk
+            const int gpc = std::max(1, std::min(slabs, bps * d.sm_count / nchunks));
+            grid = gpc * nchunks;
+        } else {
+            grid = static_cast<int>(cdiv(total, ipb));
+        }
+        const size_t stage_bytes = static_cast<size_t>(nl) * blr::S2_ROWS * 64 * (zh ? 2 : 4);
+        const char* se = getenv("BLR_S2_SMEM");  // ring bytes per block (default ~192 KB)
+        const size_t ring_bytes = std::min<size_t>(216u << 10, se ? static_cast<size_t>(atol(se)) : (192u << 10) / bps);
+        const int nst = static_cast<int>(std::max<size_t>(2, std::min<size_t>(blr::S2_MAX_STAGES, ring_bytes / stage_bytes)));
+        const size_t smem = nst * stage_bytes + 16 * nst;
         cudaLaunchConfig_t cfg = {};
-        // rows per block: ~3 blocks per SM over the whole grid, multiple of 16
-        const int64_t chunks = cdiv(r, 64);
-        const int64_t target_blocks = 3LL * d.sm_count;  // measured best of 1..8 per SM (GPT2-S)
-        const int rpb = static_cast<int>(std::max<int64_t>(blr::S2_ROWS,
-                                          rup(cdiv(n_tok * chunks, target_blocks), blr::S2_ROWS)));
-        cfg.gridDim = dim3(static_cast<unsigned>(chunks), static_cast<unsigned>(cdiv(n_tok, rpb)));
-        cfg.blockDim = dim3(256);
-        // accumulators per thread: the smallest instantiated count >= b2 (S rows beyond b2 are zero)
-        const int64_t maxb = b2 <= 1 ? 1 : b2 <= 2 ? 2 : b2 <= 3 ? 3 : b2 <= 4 ? 4 : b2 <= 6 ? 6 : b2 <= 8 ? 8
-                             : b2 <= 9 ? 9 : b2 <= 12 ? 12 : 16;
-        cfg.dynamicSmemBytes = static_cast<size_t>(b1 * maxb * 64 * 4 + 2 * b1 * 256 * 16);
+        cfg.gridDim = dim3(static_cast<unsigned>(grid));
+        cfg.blockDim = dim3(static_cast<unsigned>(32 * nw));
+        cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -926,28 +961,33 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         {
             std::lock_guard<std::mutex> lk(g_mu);
             if (!g_attr_set[7][dev]) {
-                const int mx = 16 * 16 * 64 * 4 + 2 * 16 * 256 * 16;
-                if (cudaFuncSetAttribute(blr::blast_s2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
-                    cudaFuncSetAttribute(blr::blast_s2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
-                    cudaFuncSetAttribute(blr::blast_s2_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
-                    cudaFuncSetAttribute(blr::blast_s2_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
-                    cudaFuncSetAttribute(blr::blast_s2_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
-                    cudaFuncSetAttribute(blr::blast_s2_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
-                    cudaFuncSetAttribute(blr::blast_s2_kernel<9>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
-                    cudaFuncSetAttribute(blr::blast_s2_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess ||
-                    cudaFuncSetAttribute(blr::blast_s2_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess)
+                const int mx = 220 << 10;
+#define BLR_S2_ATTR(KG, NL) \
+    cudaFuncSetAttribute(blr::blast_s2_kernel<KG, NL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess || \
+        cudaFuncSetAttribute(blr::blast_s2_kernel<KG, NL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
+                if (BLR_S2_ATTR(1, 4) || BLR_S2_ATTR(1, 8) || BLR_S2_ATTR(1, 16) || BLR_S2_ATTR(2, 4) ||
+                    BLR_S2_ATTR(2, 8) || BLR_S2_ATTR(2, 16))
                     return BLR_ERR_CUDA;
+#undef BLR_S2_ATTR
                 g_attr_set[7][dev] = true;
             }
         }
+        const auto* sb = static_cast<const __nv_bfloat16*>(S);
+        auto* ob = static_cast<__nv_bfloat16*>(zpp);
+        const int in = static_cast<int>(n_tok), ib1 = static_cast<int>(b1), ib2 = static_cast<int>(b2),
+                  ir = static_cast<int>(r);
         cudaError_t le;
-        switch (maxb) {
-#define BLR_S2_CASE(KB) \
-    case KB: le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<KB>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb); break;
-            BLR_S2_CASE(1) BLR_S2_CASE(2) BLR_S2_CASE(3) BLR_S2_CASE(4) BLR_S2_CASE(6) BLR_S2_CASE(8)
-            BLR_S2_CASE(9) BLR_S2_CASE(12)
+        switch ((kg * 32 + nl) * 2 + (zh ? 1 : 0)) {
+#define BLR_S2_CASE(KG, NL, H) \
+    case (KG * 32 + NL) * 2 + H: \
+        le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<KG, NL, H != 0>, tz, sb, ob, in, ib1, ib2, ir, comp, \
+                                slabs, total, ipb, nchunks, map_mode, nst); \
+        break;
+            BLR_S2_CASE(1, 4, 0) BLR_S2_CASE(1, 4, 1) BLR_S2_CASE(1, 8, 0) BLR_S2_CASE(1, 8, 1)
+            BLR_S2_CASE(1, 16, 0) BLR_S2_CASE(1, 16, 1) BLR_S2_CASE(2, 4, 0) BLR_S2_CASE(2, 4, 1)
+            BLR_S2_CASE(2, 8, 0) BLR_S2_CASE(2, 8, 1) BLR_S2_CASE(2, 16, 0) BLR_S2_CASE(2, 16, 1)
 #undef BLR_S2_CASE
-            default: le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<16>, zb, sb, ob, in, ib1, ib2, ir, comp, rpb);
+            default: return BLR_ERR_UNSUPPORTED;
         }
         if (le != cudaSuccess) return BLR_ERR_CUDA;
         if (cudaGetLastError() != cudaSuccess) return BLR_ERR_CUDA;

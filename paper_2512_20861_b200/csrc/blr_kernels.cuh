@@ -70,7 +70,7 @@ struct KParams {
     uint32_t c_swz;        // staging swizzle mask (7: 128 B, 3: 64 B, 1: 32 B, 0: none) = TMA map's
     uint32_t stage_warp_bytes;  // staging bytes per epilogue warp
     int stage_bufs;        // staging buffers per warp (GEMM / Monarch kinds)
-    int out_f32;           // GEMM kind: store fp32 (no rounding; BLAST split-path S1 output)
+    int out_f32;           // GEMM kind output type: 0 bf16, 1 fp32 (unrounded), 2 fp16 (BLAST split S1)
     int r_blk;             // Monarch: r'
     int kb_per_tile;       // Monarch: output blocks k per N tile
     int b1, b2;            // BLAST block counts
@@ -193,13 +193,14 @@ __device__ __forceinline__ TileCoord tile_get(const KParams& p, const TileIter& 
 // Stage 8 fp32 values (one 16-B chunk `chunk` of row `row`) as bf16 RNE into a row-major staging
 // tile whose rows are `row_bytes` long, applying the TMA swizzle (16-B chunk index XOR address
 // bits [7, 7+log2(mask+1)) ).  part 1 stages the compensation term lo = bf16(v - bf16(v)).
+// F16: store IEEE fp16 RNE instead (the BLAST split path's S1 output Z, R13).
 __device__ __forceinline__ void stage_row8(uint32_t buf, int row, int chunk, uint32_t row_bytes, uint32_t swz,
-                                           const float (&f)[8], int part) {
+                                           const float (&f)[8], int part, uint32_t f16 = 0) {
     uint4 w;
-    w.x = ptx::pack_bf16x2(f[0], f[1]);
-    w.y = ptx::pack_bf16x2(f[2], f[3]);
-    w.z = ptx::pack_bf16x2(f[4], f[5]);
-    w.w = ptx::pack_bf16x2(f[6], f[7]);
+    w.x = ptx::pack_16x2(f[0], f[1], f16);
+    w.y = ptx::pack_16x2(f[2], f[3], f16);
+    w.z = ptx::pack_16x2(f[4], f[5], f16);
+    w.w = ptx::pack_16x2(f[6], f[7], f16);
     if (part) {
         const uint32_t hw[4] = {w.x, w.y, w.z, w.w};
         float r[8];
@@ -636,7 +637,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const int parts = p.out_lo_off > 0 ? 2 : 1;
                 // column chunks of CW elements; chunk j of this warp starts at col = (half + 2 j) * CW
                 const int CW = p.c_box_w;
-                const uint32_t row_bytes = CW * (p.out_f32 ? 4 : 2);
+                const uint32_t row_bytes = CW * (p.out_f32 == 1 ? 4 : 2);
                 const uint32_t buf_bytes = 32 * row_bytes;
                 for (int c0 = half * CW; c0 < nvalid; c0 += 2 * CW) {
                     // TMEM -> registers: CW fp32 columns of this warp's 32 rows (CW <= 64, mult. of 8)
@@ -657,12 +658,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
                             if (j * 8 < CW && !(p.dbg & 2)) {
-                                if (p.out_f32)
+                                if (p.out_f32 == 1)
                                     stage_row8_f32(buf, lane, j, row_bytes, p.c_swz,
                                                    *reinterpret_cast<const float(*)[8]>(&fv[j * 8]));
                                 else
                                     stage_row8(buf, lane, j, row_bytes, p.c_swz,
-                                               *reinterpret_cast<const float(*)[8]>(&fv[j * 8]), part);
+                                               *reinterpret_cast<const float(*)[8]>(&fv[j * 8]), part,
+                                               p.out_f32 == 2);
                             }
                         }
                         ptx::fence_async_smem();
@@ -713,112 +715,160 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // ------------------------------------------------------------------------- BLAST S2 kernel -----
 // Z''[k][t][rho] = sum_l S[l,k,rho] * Z[l][t][rho]   (the S-weighted block sum)
 // Used when b1 * r does not fit TMEM, between the S1 grouped GEMM and the S3 expand.
-// Bandwidth-bound streaming kernel.  Block = 256 threads = 16 token rows x a 64-wide rho chunk;
-// it stages the chunk's S slice once in smem (fp32) and walks `rows_per_block` rows in passes of
-// 16.  Thread (row, 4 rho) prefetches its next row's b1 fp32 chunks with cp.async into a
-// double-buffered smem ring (no register cost), then accumulates the current row from smem.
-// Z is the unrounded fp32 S1 output; fp32 accumulation in a fixed l order and one RNE rounding
-// (plus the compensation term when comp == 2) -- the same single rounding as the fused path.
-constexpr int S2_ROWS = 16;  // rows per pass (256 threads / 16 threads per 64-rho row segment)
-// MAXB = the number of output-block accumulators per thread: the smallest instantiated size >= b2
-// (host dispatch); the S rows beyond b2 are zero.
-template <int MAXB>
-__global__ void __launch_bounds__(256)
-    blast_s2_kernel(const float* __restrict__ Z, const __nv_bfloat16* __restrict__ S,
+// Bandwidth-bound streaming kernel:
+//  * work item = (64-wide rho chunk, S2_ROWS token rows); items are enumerated chunk-major and
+//    each block walks a contiguous run of them, so it reloads its S slice at most twice;
+//  * warp 0 is the TMA producer: one 3-D box (64 rho, S2_ROWS rows, b1 blocks) of Z per item into
+//    an mbarrier ring of up to S2_MAX_STAGES -- all b1 blocks of the item in flight in one request;
+//  * warps 1..NW each own KG output blocks k and keep their S[l, k, rho pair] for all l in
+//    registers (packed fp32x2), so shared memory carries only Z: lane = 2 rho, a warp's read of
+//    one (l, row) is one conflict-free 128/256-B line, and each Z value feeds KG packed FMAs;
+//  * Z''_k rows are written straight from registers (bf16x2 per lane: one 128-B line per warp).
+// Z is S1's output in fp16 (ZF16, the default: 11-bit significand, R13) or fp32.
+// fp32 accumulation in ascending l, one RNE rounding to bf16 (plus the compensation term lo when
+// comp == 2) -- the same single rounding of Z'' as the fused path; no atomics (deterministic).
+constexpr int S2_ROWS = 8;
+constexpr int S2_MAX_STAGES = 16;  // ring depth is chosen at launch (<= ~200 KB of smem)
+constexpr int S2_MAXL = 16;
+constexpr int S2_RU = 4;     // rows accumulated together per warp (independent FMA chains)
+constexpr int S2_RSPLIT = 2; // warps sharing a k-group split the item's rows (S2_ROWS = RU x RSPLIT)
+
+template <int KG, int NL, bool ZF16>
+__global__ void __launch_bounds__(32 * 16, 1)
+    blast_s2_kernel(const __grid_constant__ CUtensorMap tmZ, const __nv_bfloat16* __restrict__ S,
                     __nv_bfloat16* __restrict__ Zpp, int n_tok, int b1, int b2, int r, int comp,
-                    int rows_per_block) {
-    extern __shared__ __align__(16) float s2_smem[];
-    // S chunk [b1][MAXB][64] fp32, zero-padded for k >= b2 so the k loop below carries no bounds
-    // branch (the compiler can batch its shared loads; FMAs on the zero rows are discarded)
-    float* s_sm = s2_smem;
-    float4* zbuf = reinterpret_cast<float4*>(s2_smem + b1 * MAXB * 64);  // [2][b1][256] float4
-    const int rho_base = blockIdx.x * 64;
-    for (int v = threadIdx.x; v < b1 * MAXB * 8; v += blockDim.x) {
-        const int lkp = v >> 3, c8 = (v & 7) * 8;
-        const int l = lkp / MAXB, k = lkp % MAXB;
-        const int lk = l * b2 + k;
-        float* dst = s_sm + lkp * 64 + c8;
-        if (k < b2 && rho_base + c8 < r) {
-            const uint4 w = __ldg(reinterpret_cast<const uint4*>(S + static_cast<long long>(lk) * r + rho_base + c8));
-            const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                dst[2 * e] = __uint_as_float(ww[e] << 16);
-                dst[2 * e + 1] = __uint_as_float(ww[e] & 0xFFFF0000u);
-            }
-        } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e) dst[e] = 0.f;
-        }
+                    int slabs, int total_items, int items_per_block, int nchunks, int map_mode, int nst) {
+    extern __shared__ __align__(1024) uint8_t s2_smem[];
+    constexpr uint32_t ESZ = ZF16 ? 2 : 4;
+    constexpr uint32_t ROW_BYTES = 64 * ESZ;
+    // a stage holds NL planes [l][row][64 rho]; planes b1..NL-1 are zeroed once (never loaded)
+    constexpr uint32_t STAGE_BYTES = NL * S2_ROWS * ROW_BYTES;
+    const uint32_t tx_bytes = static_cast<uint32_t>(b1) * S2_ROWS * ROW_BYTES;
+    const uint32_t ring = ptx::smem_u32(s2_smem);
+    const uint32_t bars = ring + nst * STAGE_BYTES;  // full[nst], empty[nst]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x / 32;  // consumer warps: (k-group, row half) pairs
+    // item j of this block -> (rho chunk, slab of S2_ROWS rows)
+    //   map_mode 0: a contiguous run of the chunk-major item list
+    //   map_mode 1: a fixed chunk (blockIdx % nchunks) and every (grid/nchunks)-th slab, so the
+    //               blocks running at any moment read all chunks of the same rows (whole Z rows
+    //               from DRAM rather than 128-B pieces of many)
+    int it0, cnt, slab_step = 1;
+    if (map_mode == 1) {
+        const int gpc = gridDim.x / nchunks;
+        it0 = (blockIdx.x % nchunks) * slabs + blockIdx.x / nchunks;
+        cnt = (slabs - static_cast<int>(blockIdx.x / nchunks) + gpc - 1) / gpc;
+        slab_step = gpc;
+    } else {
+        it0 = blockIdx.x * items_per_block;
+        cnt = max(0, min(total_items, it0 + items_per_block) - it0);
     }
-    const int c4 = threadIdx.x & 15;
-    const int rho0 = rho_base + c4 * 4;
-    const bool col_ok = rho0 < r;
-    const int row_lo = blockIdx.y * rows_per_block;
-    const int row_hi = min(n_tok, row_lo + rows_per_block);
-    const int npass = (row_hi - row_lo + S2_ROWS - 1) / S2_ROWS;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < nst; ++s) {
+            ptx::mbar_init(bars + 8 * s, 1);
+            ptx::mbar_init(bars + 8 * (nst + s), nw);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (b1 < NL) {
+        const uint32_t pad = (NL - b1) * S2_ROWS * ROW_BYTES;
+        for (int s = 0; s < nst; ++s)
+            for (uint32_t o = threadIdx.x * 16; o < pad; o += blockDim.x * 16)
+                ptx::st_shared_v4(ring + s * STAGE_BYTES + tx_bytes + o, make_uint4(0, 0, 0, 0));
+    }
+    __syncthreads();
     ptx::griddep_wait();  // Z is the previous kernel's output
-    auto prefetch = [&](int pass, int buf) {
-        const int t = row_lo + pass * S2_ROWS + (threadIdx.x >> 4);
-        if (col_ok && t < row_hi) {
-            for (int l = 0; l < b1; ++l)
-                ptx::cp_async16(ptx::smem_u32(zbuf + (buf * b1 + l) * 256 + threadIdx.x),
-                                Z + (static_cast<long long>(l) * n_tok + t) * r + rho0);
-        }
-        ptx::cp_async_commit();
+    // producer: lane 0 of warp 0 (also a consumer) keeps nst - 1 items in flight; it
+    // refills a slot once every consumer warp has released that slot's previous item
+    auto produce = [&](int j) {
+        const int it = it0 + j * slab_step;
+        const int s = j % nst;
+        if (j >= nst) ptx::mbar_wait(bars + 8 * (nst + s), ((j / nst) - 1) & 1);
+        ptx::mbar_arrive_expect_tx(bars + 8 * s, tx_bytes);
+        ptx::tma_load_3d(ring + s * STAGE_BYTES, &tmZ, bars + 8 * s, (it / slabs) * 64, (it % slabs) * S2_ROWS, 0);
     };
-    prefetch(0, 0);
-    __syncthreads();  // S staged
-    for (int pass = 0; pass < npass; ++pass) {
-        const int buf = pass & 1;
-        if (pass + 1 < npass) prefetch(pass + 1, buf ^ 1);
-        else ptx::cp_async_commit();
-        ptx::cp_async_wait<1>();  // this thread's chunks of `pass` have landed (own data only)
-        const int t = row_lo + pass * S2_ROWS + (threadIdx.x >> 4);
-        if (!col_ok || t >= row_hi) continue;
-        unsigned long long acc2[MAXB][2];
-#pragma unroll
-        for (int k = 0; k < MAXB; ++k) acc2[k][0] = acc2[k][1] = 0ull;
-        for (int l = 0; l < b1; ++l) {
-            {
-                const float4 z = zbuf[(buf * b1 + l) * 256 + threadIdx.x];
-                const unsigned long long za = ptx::pack_f32x2(z.x, z.y);
-                const unsigned long long zb = ptx::pack_f32x2(z.z, z.w);
-                const float* srow = s_sm + (l * MAXB) * 64 + c4 * 4;
-#pragma unroll
-                for (int k = 0; k < MAXB; ++k) {
-                    const ulonglong2 sv = *reinterpret_cast<const ulonglong2*>(srow + k * 64);
-                    ptx::ffma2(acc2[k][0], sv.x, za);
-                    ptx::ffma2(acc2[k][1], sv.y, zb);
-                }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < MAXB; ++k) {
-            if (k < b2) {
-                float f[4];
-                ptx::unpack_f32x2(acc2[k][0], f[0], f[1]);
-                ptx::unpack_f32x2(acc2[k][1], f[2], f[3]);
-                uint2 w;
-                w.x = ptx::pack_bf16x2(f[0], f[1]);
-                w.y = ptx::pack_bf16x2(f[2], f[3]);
-                __nv_bfloat16* dst = Zpp + ((static_cast<long long>(k) * n_tok + t) * comp) * r + rho0;
-                *reinterpret_cast<uint2*>(dst) = w;
-                if (comp == 2) {
-                    float q[4];
-                    q[0] = f[0] - __uint_as_float(w.x << 16);
-                    q[1] = f[1] - __uint_as_float(w.x & 0xFFFF0000u);
-                    q[2] = f[2] - __uint_as_float(w.y << 16);
-                    q[3] = f[3] - __uint_as_float(w.y & 0xFFFF0000u);
-                    uint2 lo;
-                    lo.x = ptx::pack_bf16x2(q[0], q[1]);
-                    lo.y = ptx::pack_bf16x2(q[2], q[3]);
-                    *reinterpret_cast<uint2*>(dst + r) = lo;
-                }
-            }
-        }
+    if (threadIdx.x == 0) {
+        ptx::prefetch_tmap(&tmZ);
+        for (int j = 0; j < min(cnt, nst - 1); ++j) produce(j);
     }
-    ptx::cp_async_wait<0>();
+    const int k0 = (warp % (nw / S2_RSPLIT)) * KG;
+    const int rbase = (warp / (nw / S2_RSPLIT)) * S2_RU;
+    const int row_stride = comp * r;  // elements between Z'' rows
+    unsigned long long sreg[NL][KG];
+    __nv_bfloat16* kbase[KG];         // Z''[k0 + kk][0][rho0]
+    int cur_chunk = -1;
+    for (int j = 0; j < cnt; ++j) {
+        const int it = it0 + j * slab_step;
+        const int chunk = it / slabs;
+        const int rho0 = chunk * 64 + 2 * lane;
+        const bool col_ok = rho0 < r;
+        if (chunk != cur_chunk) {  // S[l, k0 + kk, rho0 .. rho0 + 1] for this warp's blocks
+            cur_chunk = chunk;
+#pragma unroll
+            for (int kk = 0; kk < KG; ++kk)
+                kbase[kk] = Zpp + static_cast<long long>(k0 + kk) * n_tok * row_stride + rho0;
+#pragma unroll
+            for (int l = 0; l < NL; ++l)
+#pragma unroll
+                for (int kk = 0; kk < KG; ++kk) {
+                    uint32_t w = 0;
+                    if (l < b1 && k0 + kk < b2 && col_ok)
+                        w = __ldg(reinterpret_cast<const uint32_t*>(S + (static_cast<long long>(l) * b2 + k0 + kk) * r + rho0));
+                    sreg[l][kk] = ptx::pack_f32x2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+                }
+        }
+        if (threadIdx.x == 0 && j + nst - 1 < cnt) produce(j + nst - 1);
+        const int s = j % nst;
+        ptx::mbar_wait(bars + 8 * s, (j / nst) & 1);
+        const uint8_t* buf = s2_smem + s * STAGE_BYTES + lane * 2 * ESZ;
+        const int row0 = (it % slabs) * S2_ROWS;
+        {
+            const int rr = rbase;
+            unsigned long long acc[S2_RU][KG];
+#pragma unroll
+            for (int u = 0; u < S2_RU; ++u)
+#pragma unroll
+                for (int kk = 0; kk < KG; ++kk) acc[u][kk] = 0ull;
+#pragma unroll
+            for (int l = 0; l < NL; ++l) {
+#pragma unroll
+                for (int u = 0; u < S2_RU; ++u) {
+                    const uint8_t* a = buf + (l * S2_ROWS + rr + u) * ROW_BYTES;
+                    unsigned long long z2;
+                    if constexpr (ZF16) {
+                        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(a));
+                        z2 = ptx::pack_f32x2(f.x, f.y);
+                    } else {
+                        z2 = *reinterpret_cast<const unsigned long long*>(a);
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < KG; ++kk) ptx::ffma2(acc[u][kk], sreg[l][kk], z2);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < S2_RU; ++u) {
+                const int t = row0 + rr + u;
+                if (col_ok && t < n_tok) {
+                    const long long roff = static_cast<long long>(t) * row_stride;
+#pragma unroll
+                    for (int kk = 0; kk < KG; ++kk) {
+                        if (k0 + kk < b2) {
+                            float f0, f1;
+                            ptx::unpack_f32x2(acc[u][kk], f0, f1);
+                            const uint32_t hi = ptx::pack_bf16x2(f0, f1);
+                            __nv_bfloat16* dst = kbase[kk] + roff;
+                            *reinterpret_cast<uint32_t*>(dst) = hi;
+                            if (comp == 2)
+                                *reinterpret_cast<uint32_t*>(dst + r) = ptx::pack_bf16x2(
+                                    f0 - __uint_as_float(hi << 16), f1 - __uint_as_float(hi & 0xFFFF0000u));
+                        }
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(bars + 8 * (nst + s));
+    }
 }
 
 }  // namespace blr

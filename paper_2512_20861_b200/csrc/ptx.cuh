@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace blr {
 namespace ptx {
@@ -276,6 +277,19 @@ __host__ __device__ __forceinline__ uint32_t idesc_bf16(uint32_t M, uint32_t N, 
            ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+__device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);  // cvt.rn.f16x2.f32 (RNE)
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+// bf16x2 (f16 == 0) or fp16x2 (f16 != 0) RNE pack of (a -> low half, b -> high half), selected by
+// predication (no branch: keeps the epilogue's register allocation unchanged)
+__device__ __forceinline__ uint32_t pack_16x2(float a, float b, uint32_t f16) {
+    uint32_t d;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
+        "@p cvt.rn.f16x2.f32 %0, %2, %1;\n\t@!p cvt.rn.bf16x2.f32 %0, %2, %1;\n\t}"
+        : "=r"(d) : "f"(a), "f"(b), "r"(f16));
+    return d;
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // cvt.rn.bf16x2.f32 (RNE)
     return *reinterpret_cast<uint32_t*>(&h);
