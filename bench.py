@@ -226,6 +226,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--eager", action="store_true", help="launch every step from the host (no CUDA graph)")
+    ap.add_argument("--flush", default="write+read", choices=["write+read", "write"],
+                    help="L2 flush between timed steps (see L2Flush)")
     args = ap.parse_args()
     w = configs.WORKLOADS[args.config]
     if args.impl == "reference":
@@ -294,7 +296,7 @@ def main():
 
     # ---- per-launch events (C-ABI profiling hook) and L2 flush buffer
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
+    flush = L2Flush(max(2 * l2, 256 << 20), dev, args.flush)
     K, W = args.steps, args.warmup
     gev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_launch)]
     for e in gev:
@@ -344,7 +346,7 @@ def main():
         lib.blr_profile_end()
 
     for _ in range(W):
-        flush.zero_()
+        flush()
         run_step()
     torch.cuda.synchronize()
 
@@ -355,7 +357,7 @@ def main():
     torch.cuda.synchronize()
     with sampler:
         for s in range(K):
-            flush.zero_()  # L2 flush between timed steps (outside the step events)
+            flush()  # L2 flush between timed steps (outside the step events)
             step_ev[s][0].record(stream)
             launches += run_step()
             step_ev[s][1].record(stream)
@@ -369,7 +371,7 @@ def main():
     prof_step_ms = 0.0
     pe = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
     for s in range(kp):
-        flush.zero_()
+        flush()
         pe[0].record(stream)
         run_step_profiled()
         pe[1].record(stream)
@@ -448,7 +450,7 @@ def main():
             "config": {"workload": f"{w.key}: {w.desc}", "n_tokens_per_gpu": n,
                        "value_def": f"tokens/s; one step = {len(chains)} BLR MLPs/layer chains x {n} tokens",
                        "layers": [f"{L.model}.{L.name}.{L.method}(r={L.r},b={L.b})" for L in w.layers],
-                       "l2": "flushed between timed steps (write of 2x L2), outside the step events",
+                       "l2": flush.describe(),
                        "launch": "eager" if args.eager else "CUDA graph replay of the step (both arms)",
                        "parallelism": f"token-sharded dp{ws}, no data-path collective"},
             "roofline": roof, "per_layer": per_layer, "ms_per_step_stats": step_stats,
@@ -543,6 +545,28 @@ def dense_weight(L, f):
     return W.reshape(L.i, L.o).to(torch.bfloat16)
 
 
+class L2Flush:
+    """L2 flush between timed steps, outside the step events.  "write": write a buffer of 2x L2.
+    "write+read" (default): the same write, then a read of a second 2x-L2 buffer, so the flush's
+    own dirty lines are written back during the flush instead of being evicted -- at HBM write
+    cost -- by the first writes of the timed step."""
+
+    def __init__(self, nbytes, dev, mode):
+        self.mode = mode
+        self.wbuf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        self.rbuf = torch.ones(nbytes // 4, dtype=torch.float32, device=dev) if mode == "write+read" else None
+
+    def __call__(self):
+        self.wbuf.zero_()
+        if self.rbuf is not None:
+            self.rbuf.sum()
+
+    def describe(self):
+        if self.mode == "write+read":
+            return "flushed between timed steps (write of 2x L2, then read of another 2x L2), outside the step events"
+        return "flushed between timed steps (write of 2x L2), outside the step events"
+
+
 def dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev, use_graph=True):
     Ws = {j: dense_weight(L, facs[j]) for j, L in enumerate(w.layers)}
     outs = {j: torch.empty((w.n, L.o), dtype=torch.bfloat16, device=dev) for j, L in enumerate(w.layers)}
@@ -554,7 +578,7 @@ def dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev, use_graph=Tr
                 h = torch.matmul(h, Ws[j], out=outs[j])
 
     for _ in range(max(W, 2)):
-        flush.zero_()
+        flush()
         step()
     torch.cuda.synchronize()
     run = step
@@ -566,7 +590,7 @@ def dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev, use_graph=Tr
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     torch.cuda.synchronize()
     for s in range(K):
-        flush.zero_()
+        flush()
         evs[s][0].record(stream)
         run()
         evs[s][1].record(stream)
@@ -609,7 +633,7 @@ def e2e_run(w, chains, facs, xs, flush, stream, K, dev):
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     for s in range(K):
-        flush.zero_()
+        flush()
         evs[s][0].record(stream)
         one()
         evs[s][1].record(stream)

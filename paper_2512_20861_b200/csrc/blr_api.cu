@@ -30,7 +30,7 @@ struct DevInfo {
 std::mutex g_mu;
 DevInfo g_dev[64];
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-bool g_attr_set[8][64] = {};
+bool g_attr_set[13][64] = {};  // kernel attribute set, per (kernel variant, device)
 thread_local int t_last_launches = 0;
 thread_local void** t_prof_events = nullptr;
 thread_local int t_prof_cap = 0;
@@ -89,13 +89,8 @@ inline int comp_factor(int64_t k_s3) { return k_s3 < COMP_K_THRESHOLD ? 2 : 1; }
 
 // BLAST runs S1 and S2 fused (b1 TMEM accumulators per token tile) when all b1 * r columns fit
 // TMEM, so X is read once; otherwise S1 (grouped GEMM), S2 (streaming) and S3 run separately.
-// Precision of the split path's S1 output Z (R13): fp16 by default (RNE, 11-bit
-// significand: half the intermediate traffic of fp32, rounding error ~1/8 of a bf16 rounding;
-// finite range |Z| <= 65504), fp32 with BLR_BLAST_Z=f32.
-inline bool blast_z_f16() {
-    const char* e = getenv("BLR_BLAST_Z");
-    return !(e && !strcmp(e, "f32"));
-}
+// The split path's S1 output Z is stored fp16 (RNE, 11-bit significand: half the intermediate
+// traffic of fp32, rounding error ~1/8 of a bf16 rounding; finite range |Z| <= 65504), R13.
 
 inline bool blast_fused(int64_t b1, int64_t r) {
     const char* e = getenv("BLR_BLAST_PATH");
@@ -216,7 +211,7 @@ cudaError_t prof_record(void* ev, cudaStream_t st) {
                                     cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault);
 }
 
-template <int KIND, int PAIR>
+template <int KIND, int PAIR, int OUTF = 0>
 blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const KParams& p_in,
                   const DevInfo& d, int dev, cudaStream_t stream) {
     KParams p = p_in;
@@ -224,15 +219,16 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     if (const char* e = getenv("BLR_DBG")) p.dbg = atoi(e);  // debug experiments only
     if (const char* e = getenv("BLR_DBG_LAUNCH"); e && atoi(e) != t_last_launches) p.dbg = 0;  // only launch k
     if (t_trace) t_trace += 128 * 256;  // next launch traces into the next slot
-    auto kfn = blr::blr_gemm_kernel<KIND, PAIR>;
+    auto kfn = blr::blr_gemm_kernel<KIND, PAIR, OUTF>;
     const blr::SmemLayout L = blr::smem_layout(p);
     const int smem = static_cast<int>(L.total + SMEM_SLACK);
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        if (!g_attr_set[KIND + 3 * (PAIR - 1)][dev]) {
+        const int slot = OUTF ? 8 + OUTF + 2 * (PAIR - 1) : KIND + 3 * (PAIR - 1);
+        if (!g_attr_set[slot][dev]) {
             if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT) != cudaSuccess)
                 return BLR_ERR_CUDA;
-            g_attr_set[KIND + 3 * (PAIR - 1)][dev] = true;
+            g_attr_set[slot][dev] = true;
         }
     }
     const int units = d.sm_count / PAIR;  // CTAs (or CTA pairs) that fit one wave
@@ -295,11 +291,12 @@ int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int sms, int pair) {
 
 struct OutMap {  // 4-D view (N, comp, groups, rows) of a GEMM phase's output
     void* ptr;
-    int f32;               // output type: 0 bf16, 1 fp32 (unrounded), 2 fp16
+    int f32;               // output type: 0 bf16, 2 fp16 (BLAST split-path Z)
     int64_t comp;          // 1, or 2 for a compensated [hi | lo] intermediate
     int64_t comp_stride;   // elements between hi and lo
     int64_t group_stride;  // elements between groups
     int64_t row_stride;    // elements between rows
+    int blocked = 0;       // 1: chunk-blocked [g][N/8][rows][8] (BLAST Z with the tensor-core S2)
 };
 
 // One plain GEMM phase: out[g](t, c) = sum_k A[g](t, k) B[g](k, c), K-major A.
@@ -328,11 +325,12 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     set_b_staging(p, b_mn_major);
     p.BN = bn_full;
     p.out_lo_off = out.comp == 2 ? out.comp_stride : 0;
-    p.out_f32 = out.f32;
-    const int esz = out.f32 == 1 ? 4 : 2;
+    p.out_ptr = out.ptr;
+    p.out_gstride = out.group_stride;
+    const int esz = 2;
     p.c_box_w = chunk_width(p.BN);
     while (p.c_box_w * esz > 128) p.c_box_w /= 2;  // staged rows <= 128 B
-    p.c_swz = pick_swz(p.c_box_w * esz).mask;
+    p.c_swz = out.blocked ? 0 : pick_swz(p.c_box_w * esz).mask;
     return finish_plan(p, true, 32 * p.c_box_w * esz, d.sm_count / pair);
 }
 
@@ -343,11 +341,12 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
 // the activation tile (BLR_PAIR=1/2 forces a mode).
 blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A, int a_gmid, int64_t a_row_stride,
                       int64_t a_group_stride, int64_t n_tok, int64_t K, int64_t groups, int64_t N, const void* B,
-                      bool b_mn_major, const OutMap& out, int comp) {
+                      bool b_mn_major, const OutMap& out, int comp, int a_blocked = 0) {
     KParams p;
     int pair = 1;
     const char* pe = getenv("BLR_PAIR");
-    const int force = pe ? atoi(pe) : 0;
+    // bulk-copied (chunk-blocked) A completes on the issuing CTA's barrier: single-CTA MMAs only
+    const int force = a_blocked ? 1 : (pe ? atoi(pe) : 0);
     if (force == 2 && n_tok >= 256) {
         pair = 2;
     } else if (force != 1) {
@@ -361,10 +360,15 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
         if (pair == 1 || !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp))
             return BLR_ERR_UNSUPPORTED;
     }
-    const int esz = out.f32 == 1 ? 4 : 2;
+    const int esz = 2;
     const Swz cs = pick_swz(p.c_box_w * esz);
+    p.a_blocked = a_blocked;
+    p.a_ptr = static_cast<const __nv_bfloat16*>(A);
+    p.a_nchunks = static_cast<int>(K / 8);
 
     CUtensorMap ta, tb, tc;
+    // (a chunk-blocked A / output moves by 1-D bulk copies in the kernel; the maps below are then
+    // encoded over the same buffer but unused)
     {
         const int64_t Ka = K * comp;  // A row length actually stored
         uint64_t dims[3], str[2];
@@ -404,6 +408,13 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
         const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32};
         if (!encode(&tc, out.ptr, 4, dims, strb, box, cs.mode, out.f32)) return BLR_ERR_CUDA;
     }
+    // fp16 output (BLAST split-path Z) is a separate instantiation: the bf16 epilogue stays as is
+    if (out.f32 == 2 && out.blocked)
+        return pair == 2 ? launch<blr::KIND_GEMM, 2, 2>(ta, tb, tc, p, d, dev, st)
+                         : launch<blr::KIND_GEMM, 1, 2>(ta, tb, tc, p, d, dev, st);
+    if (out.f32 == 2)
+        return pair == 2 ? launch<blr::KIND_GEMM, 2, 1>(ta, tb, tc, p, d, dev, st)
+                         : launch<blr::KIND_GEMM, 1, 1>(ta, tb, tc, p, d, dev, st);
     if (pair == 2) return launch<blr::KIND_GEMM, 2>(ta, tb, tc, p, d, dev, st);
     return launch<blr::KIND_GEMM, 1>(ta, tb, tc, p, d, dev, st);
 }
@@ -591,7 +602,7 @@ blr_status decode_k(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int
 size_t blast_ws_bytes(int64_t n_tok, int64_t b1, int64_t b2, int64_t r) {
     const size_t zpp = static_cast<size_t>(b2) * n_tok * r * 2 * comp_factor(r);
     if (blast_fused(b1, r)) return zpp;
-    return zpp + static_cast<size_t>(b1) * n_tok * r * (blast_z_f16() ? 2 : 4);  // + Z_l of the separate S1
+    return zpp + static_cast<size_t>(b1) * n_tok * r * 2;  // + fp16 Z_l of the separate S1
 }
 
 }  // namespace
@@ -902,34 +913,75 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         if (s != BLR_OK) return s;
     } else {
         // ---- S1: Z[l][t][rho] = (X_l V_l)[t, rho]  -- grouped GEMM over l (A = X viewed (p, b1, n))
-        const bool zh = blast_z_f16();
+        const char* s2e = getenv("BLR_S2");
+        // tensor-core S2 (single-rounded Z''): Z and Z'' chunk-blocked [g][r/8][n][8]
+        const bool s2_mma = comp == 1 && !(s2e && !strcmp(s2e, "cuda"));
         void* zl = static_cast<char*>(workspace) + static_cast<size_t>(b2) * n_tok * r * 2 * comp;
-        s = gemm_phase(d, dev, st, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true,
-                       OutMap{zl, zh ? 2 : 1, 1, r, n_tok * r, r}, 1);
+        OutMap zmap{zl, 2, 1, r, n_tok * r, r};
+        zmap.blocked = s2_mma ? 1 : 0;
+        s = gemm_phase(d, dev, st, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true, zmap, 1);
         if (s != BLR_OK) return s;
         // ---- S2: Z''[k][t][rho] = sum_l S[l,k,rho] Z[l][t][rho]
+        if (s2_mma) {
+            // tensor-core S2 (blast_s2_mma_kernel): chunk-blocked fp16 Z [l][r/8][n][8] in,
+            // chunk-blocked bf16 Z'' [k][r/8][n][8] out (2-KB panels, 1-D bulk copies)
+            const blr::S2MLayout sl = blr::s2m_layout(static_cast<int>(b1), static_cast<int>(b2));
+            const int64_t items = cdiv(n_tok, 128) * (r / 8);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(items, d.sm_count)));
+            cfg.blockDim = dim3(blr::S2M_THREADS);
+            cfg.dynamicSmemBytes = sl.total + 1024;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 0;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            {
+                std::lock_guard<std::mutex> lk(g_mu);
+                if (!g_attr_set[8][dev]) {
+                    if (cudaFuncSetAttribute(blr::blast_s2_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             232448) != cudaSuccess)
+                        return BLR_ERR_CUDA;
+                    g_attr_set[8][dev] = true;
+                }
+            }
+            const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+            if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+            if (cudaLaunchKernelEx(&cfg, blr::blast_s2_mma_kernel, static_cast<const __half*>(zl),
+                                   static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
+                                   static_cast<int>(n_tok), static_cast<int>(b1), static_cast<int>(b2),
+                                   static_cast<int>(r)) != cudaSuccess)
+                return BLR_ERR_CUDA;
+            if (cudaGetLastError() != cudaSuccess) return BLR_ERR_CUDA;
+            if (prof) {
+                if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+                ++t_prof_n;
+            }
+            ++t_last_launches;
+            return gemm_phase(d, dev, st, zpp, 0, r, n_tok * r, n_tok, r, b2, qdim, U, true,
+                              OutMap{Y, 0, 1, d_out, qdim, d_out}, 1, /*a_blocked=*/1);
+        }
+        // CUDA-core S2 (blast_s2_kernel; used for compensated Z'' (r < 128) or with BLR_S2=cuda):
+        // fp16 Z viewed (rho, t, l), box (64, S2_ROWS, b1): one item's b1 row segments per request
         CUtensorMap tz;
-        {  // Z viewed (rho, t, l); box (64, S2_ROWS, b1): one item's b1 row segments per request
-            const uint64_t es = zh ? 2 : 4;
+        {
             const uint64_t dims[3] = {static_cast<uint64_t>(r), static_cast<uint64_t>(n_tok), static_cast<uint64_t>(b1)};
-            const uint64_t str[2] = {static_cast<uint64_t>(r) * es, static_cast<uint64_t>(r * n_tok) * es};
+            const uint64_t str[2] = {static_cast<uint64_t>(r) * 2, static_cast<uint64_t>(r * n_tok) * 2};
             const uint32_t box[3] = {64, static_cast<uint32_t>(blr::S2_ROWS), static_cast<uint32_t>(b1)};
-            if (!encode(&tz, zl, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, zh ? 2 : 1)) return BLR_ERR_CUDA;
+            if (!encode(&tz, zl, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, 2)) return BLR_ERR_CUDA;
         }
         // KG output blocks per consumer warp (S held in registers: NL x KG packed pairs per lane;
         // NL = b1 rounded up to 4/8/16, the extra planes are zero)
-        const char* ke = getenv("BLR_S2_KG");
-        const int kg = b2 == 1 ? 1 : (ke ? std::max(1, std::min(2, atoi(ke))) : 2);
+        const int kg = b2 == 1 ? 1 : 2;
         const int nw = static_cast<int>(cdiv(b2, kg)) * blr::S2_RSPLIT;
         const int nl = b1 <= 4 ? 4 : b1 <= 8 ? 8 : 16;
         const int slabs = static_cast<int>(cdiv(n_tok, blr::S2_ROWS));
         const int nchunks = static_cast<int>(cdiv(r, 64));
         const int total = nchunks * slabs;
-        const char* me = getenv("BLR_S2_MAP");
-        const int map_mode = me ? atoi(me) : 1;
-        const char* be = getenv("BLR_S2_BPS");
+        const int map_mode = 1;
         // blocks per SM: up to 16 consumer warps per SM (<= 128 registers per thread)
-        const int bps = be ? atoi(be) : std::max(1, std::min(4, 16 / nw));
+        const int bps = std::max(1, std::min(4, 16 / nw));
         int grid = std::min<int>(total, bps * d.sm_count);
         int ipb = static_cast<int>(cdiv(total, grid));
         if (map_mode == 1) {  // a multiple of nchunks, at most bps block-slots per SM, >= 1 per chunk
@@ -938,9 +990,8 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         } else {
             grid = static_cast<int>(cdiv(total, ipb));
         }
-        const size_t stage_bytes = static_cast<size_t>(nl) * blr::S2_ROWS * 64 * (zh ? 2 : 4);
-        const char* se = getenv("BLR_S2_SMEM");  // ring bytes per block (default ~192 KB)
-        const size_t ring_bytes = std::min<size_t>(216u << 10, se ? static_cast<size_t>(atol(se)) : (192u << 10) / bps);
+        const size_t stage_bytes = static_cast<size_t>(nl) * blr::S2_ROWS * 64 * 2;
+        const size_t ring_bytes = (192u << 10) / bps;  // ~192 KB of ring per SM
         const int nst = static_cast<int>(std::max<size_t>(2, std::min<size_t>(blr::S2_MAX_STAGES, ring_bytes / stage_bytes)));
         const size_t smem = nst * stage_bytes + 16 * nst;
         cudaLaunchConfig_t cfg = {};
@@ -963,8 +1014,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             if (!g_attr_set[7][dev]) {
                 const int mx = 220 << 10;
 #define BLR_S2_ATTR(KG, NL) \
-    cudaFuncSetAttribute(blr::blast_s2_kernel<KG, NL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess || \
-        cudaFuncSetAttribute(blr::blast_s2_kernel<KG, NL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
+    cudaFuncSetAttribute(blr::blast_s2_kernel<KG, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
                 if (BLR_S2_ATTR(1, 4) || BLR_S2_ATTR(1, 8) || BLR_S2_ATTR(1, 16) || BLR_S2_ATTR(2, 4) ||
                     BLR_S2_ATTR(2, 8) || BLR_S2_ATTR(2, 16))
                     return BLR_ERR_CUDA;
@@ -977,15 +1027,13 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         const int in = static_cast<int>(n_tok), ib1 = static_cast<int>(b1), ib2 = static_cast<int>(b2),
                   ir = static_cast<int>(r);
         cudaError_t le;
-        switch ((kg * 32 + nl) * 2 + (zh ? 1 : 0)) {
-#define BLR_S2_CASE(KG, NL, H) \
-    case (KG * 32 + NL) * 2 + H: \
-        le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<KG, NL, H != 0>, tz, sb, ob, in, ib1, ib2, ir, comp, \
-                                slabs, total, ipb, nchunks, map_mode, nst); \
+        switch (kg * 32 + nl) {
+#define BLR_S2_CASE(KG, NL) \
+    case KG * 32 + NL: \
+        le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<KG, NL>, tz, sb, ob, in, ib1, ib2, ir, comp, slabs, total, \
+                                ipb, nchunks, map_mode, nst); \
         break;
-            BLR_S2_CASE(1, 4, 0) BLR_S2_CASE(1, 4, 1) BLR_S2_CASE(1, 8, 0) BLR_S2_CASE(1, 8, 1)
-            BLR_S2_CASE(1, 16, 0) BLR_S2_CASE(1, 16, 1) BLR_S2_CASE(2, 4, 0) BLR_S2_CASE(2, 4, 1)
-            BLR_S2_CASE(2, 8, 0) BLR_S2_CASE(2, 8, 1) BLR_S2_CASE(2, 16, 0) BLR_S2_CASE(2, 16, 1)
+            BLR_S2_CASE(1, 4) BLR_S2_CASE(1, 8) BLR_S2_CASE(1, 16) BLR_S2_CASE(2, 4) BLR_S2_CASE(2, 8) BLR_S2_CASE(2, 16)
 #undef BLR_S2_CASE
             default: return BLR_ERR_UNSUPPORTED;
         }

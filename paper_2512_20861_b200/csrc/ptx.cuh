@@ -74,6 +74,23 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* m, 
         : "memory");
 }
 
+// 1-D bulk copies (contiguous bytes, 16-B aligned, size a multiple of 16)
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(m)),
+        "r"(src), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2,
                                              int c3) {
     asm volatile(
@@ -270,6 +287,13 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
+// Instruction descriptor, kind::f16 with fp16 A and B (type code 0), fp32 D, both K-major.
+__host__ __device__ __forceinline__ uint32_t idesc_f16(uint32_t M, uint32_t N) {
+    return (1u << 4) | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
+}
 // Instruction descriptor, kind::f16: D=f32 [4,6)=1, A=bf16 [7,10)=1, B=bf16 [10,13)=1,
 // a_major [15], b_major [16] (0 = K-major, 1 = MN-major), N>>3 [17,23), M>>4 [24,29).
 __host__ __device__ __forceinline__ uint32_t idesc_bf16(uint32_t M, uint32_t N, uint32_t b_mn_major) {
@@ -280,15 +304,6 @@ __host__ __device__ __forceinline__ uint32_t idesc_bf16(uint32_t M, uint32_t N, 
 __device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);  // cvt.rn.f16x2.f32 (RNE)
     return *reinterpret_cast<uint32_t*>(&h);
-}
-// bf16x2 (f16 == 0) or fp16x2 (f16 != 0) RNE pack of (a -> low half, b -> high half), selected by
-// predication (no branch: keeps the epilogue's register allocation unchanged)
-__device__ __forceinline__ uint32_t pack_16x2(float a, float b, uint32_t f16) {
-    uint32_t d;
-    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\t"
-        "@p cvt.rn.f16x2.f32 %0, %2, %1;\n\t@!p cvt.rn.bf16x2.f32 %0, %2, %1;\n\t}"
-        : "=r"(d) : "f"(a), "f"(b), "r"(f16));
-    return d;
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // cvt.rn.bf16x2.f32 (RNE)

@@ -249,3 +249,40 @@ def test_forced_cta_pair_modes(cuda_lib, monkeypatch, pair, method):
     rows = sample_rows(n, 200)
     ridx = torch.as_tensor(rows, device=DEV)
     assert_parity(Y[ridx], _layer_ref(L, to64(X[ridx]), fac), f"pair={pair} {method}")
+
+
+# ------------------------------------------------------------------- BLAST split-path S2 variants --
+@pytest.mark.parametrize("s2", ["mma", "cuda"])
+@pytest.mark.parametrize("n,b1,b2,r,p,q", [(1000, 16, 16, 272, 64, 88),   # ragged rows, r % 64 != 0
+                                           (300, 6, 6, 192, 128, 512),    # GPT2-S c_fc shape
+                                           (257, 9, 7, 136, 32, 40),      # odd b1 / b2
+                                           (130, 16, 16, 1488, 256, 688)])  # Llama-7B gate/up (C4)
+def test_blast_split_s2_variants(cuda_lib, monkeypatch, s2, n, b1, b2, r, p, q):
+    """The split path's S2 (tensor-core block-diagonal GEMM on chunk-blocked fp16 Z, or the
+    CUDA-core streaming kernel on fp16 Z) against the oracle, ragged tails included."""
+    monkeypatch.setenv("BLR_S2", s2)
+    monkeypatch.setenv("BLR_BLAST_PATH", "split")
+    i, o = b1 * p, b2 * q
+    X = synth.make_x(n, i, seed=5)
+    V, S, U = synth.blast_factors(i, o, b1, b2, r, seed=5)
+    Y = cuda_lib.blast_matmul(X.to(DEV), V.to(DEV), S.to(DEV), U.to(DEV))
+    torch.cuda.synchronize()
+    rows = sample_rows(n, 130)
+    ref = orc.blast_forward(to64(X[rows]), to64(V), to64(S), to64(U))
+    assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"S2={s2} {n,b1,b2,r,p,q}")
+
+
+def test_blast_split_s2_mma_close_to_cuda(cuda_lib, monkeypatch):
+    """fp16 Z, fp32 accumulation in both S2 kernels: the tensor core's exact fp16 products summed
+    in fp32 and the CUDA cores' ascending-l fp32 FMAs may differ in the last bit of Z'' only, so
+    the two Y agree to within one bf16 ulp of Y (|dY| <= 2^-7 |Y| + tiny)."""
+    monkeypatch.setenv("BLR_BLAST_PATH", "split")
+    n, b1, b2, r, p, q = 512, 16, 16, 272, 64, 88
+    X = synth.make_x(n, b1 * p, seed=6).to(DEV)
+    V, S, U = [t.to(DEV) for t in synth.blast_factors(b1 * p, b2 * q, b1, b2, r, seed=6)]
+    monkeypatch.setenv("BLR_S2", "mma")
+    Ym = cuda_lib.blast_matmul(X, V, S, U).float()
+    monkeypatch.setenv("BLR_S2", "cuda")
+    Yc = cuda_lib.blast_matmul(X, V, S, U).float()
+    torch.cuda.synchronize()
+    assert torch.all((Ym - Yc).abs() <= 2.0 ** -6 * Yc.abs() + 1e-2)
