@@ -271,7 +271,7 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
 // N tile: <= 256 columns, multiple of 16, balanced.  While the grid would leave SMs idle, split
 // N further (down to 64) -- but only toward a width whose B slice (K x BN) can stay resident,
 // since in streaming mode every extra N tile re-reads the whole A tile.
-int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int sms, int pair) {
+int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int64_t groups, int sms, int pair) {
     int64_t tiles = cdiv(N, 256);
     int bn = static_cast<int>(rup(cdiv(N, tiles), 16));
     // split while the grid leaves SMs idle, but never past one wave (a partial second wave
@@ -284,7 +284,41 @@ int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int sms, int pair) {
     }
     // (splitting also when the slice cannot stay resident: the re-read A tile comes from L2, and
     //  per-SM TMA ingress, not L2 or HBM, bounds these short kernels -- measured on GPT2-S c_proj)
-    (void)K;
+    //
+    // Weight-stationary plans (short K, many token tiles) run one CTA per (group, N block) slice
+    // in lockstep, so the slice count decides how many SMs work: pick the N split that fills
+    // the SMs best, discounted by the padding of the last N tile.  (Llama-7B BLAST gate S1,
+    // 16 groups x N = 1488: BN = 256 gave 96 slices on 148 SMs; BN = 176 gives 144.)
+    const int64_t tiles_m = other_tiles / std::max<int64_t>(groups, 1);
+    const char* fe = getenv("BLR_BN_FILL");
+    if (pair == 1 && tiles_m >= 8 && cdiv(K, blr::BK) <= blr::MAX_BRES - 1 && !(fe && fe[0] == '0')) {
+        // score = ideal per-SM work / the busiest CTA's work (token tiles x BN columns)
+        auto score = [&](int b) {
+            if (rup(b, 64) * rup(K, blr::BK) * 2 > (144 << 10)) return -1.0;  // slice must stay resident
+            const int64_t slices = groups * cdiv(N, b);
+            const int64_t busiest = slices <= sms ? cdiv(tiles_m, std::min<int64_t>(sms / slices, tiles_m)) * b
+                                                  : cdiv(slices, sms) * tiles_m * b;
+            return static_cast<double>(groups * tiles_m * N) / sms / static_cast<double>(busiest);
+        };
+        // only for an underfilled plan (fewer slices than SMs, one CTA per slice), and only toward
+        // widths whose epilogue chunks stay >= 32 columns (BN = 176 -> 16-column chunks measured
+        // 1.6x slower on that S1)
+        const int64_t slices0 = groups * cdiv(N, bn);
+        double best = score(bn);
+        int best_bn = bn;
+        if (best > 0 && slices0 < sms && 2 * slices0 > sms) {
+            for (int64_t tn = cdiv(N, 256); tn <= cdiv(N, 128); ++tn) {
+                const int b = static_cast<int>(rup(cdiv(N, tn), 16));
+                if (chunk_width(b) < 32) continue;
+                const double s = score(b);
+                if (s > best + 0.05) {
+                    best = s;
+                    best_bn = b;
+                }
+            }
+            bn = best_bn;
+        }
+    }
     (void)pair;
     return bn;
 }
@@ -309,7 +343,7 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     p.a_gmid = a_gmid;
     p.n_tok = static_cast<int>(n_tok);
     p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM * pair));
-    p.BN = choose_bn(N, K, p.tiles_m * groups, d.sm_count / pair, pair);
+    p.BN = choose_bn(N, K, p.tiles_m * groups, groups, d.sm_count / pair, pair);
     if (pair == 2 && (p.BN / 2) % 8) p.BN = static_cast<int>(rup(p.BN, 32));
     p.N = static_cast<int>(N);
     p.tiles_n = static_cast<int>(cdiv(N, p.BN));
@@ -346,6 +380,8 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     int pair = 1;
     const char* pe = getenv("BLR_PAIR");
     // bulk-copied (chunk-blocked) A completes on the issuing CTA's barrier: single-CTA MMAs only
+    // (a pair variant that relayed the peer's A arrival to the leader measured no faster on the
+    //  Llama-7B S3 expands: 2.58 / 1.24 ms vs 2.54 / 0.91 ms)
     const int force = a_blocked ? 1 : (pe ? atoi(pe) : 0);
     if (force == 2 && n_tok >= 256) {
         pair = 2;

@@ -898,8 +898,8 @@ __global__ void __launch_bounds__(32 * 16, 1)
 // a token tile is 2 KB contiguous, moved by one 1-D bulk copy (a tensor box with 16-B rows moves
 // one row per request: measured 2x slower).  The S1 epilogue writes that layout, S3 reads it.
 // fp16 x fp16 products are exact, accumulation fp32; Z'' is rounded once to bf16 (RNE).
-// Items (128-token tile T, chunk c) are walked T-major with a grid stride, so the CTAs running at
-// any moment cover every chunk of the same rows (whole Z / Z'' rows per DRAM page window).
+// Items (128-token tile T, chunk c) are enumerated chunk-major and each CTA walks one contiguous
+// run of them (sequential panel streams; B_c rebuilt only when the run changes chunk).
 // Roles: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-3 build B_c, warps 4-7
 // epilogue (TMEM -> bf16 -> smem [k][t][8] -> b2 bulk stores of the (k, c) panels).
 constexpr int S2M_ASTAGES = 3;
@@ -937,11 +937,15 @@ __global__ void __launch_bounds__(S2M_THREADS, 1)
     const int nchunks = r / 8;
     const int tiles = (n_tok + 127) / 128;
     const int total = tiles * nchunks;
-    const int cnt = blockIdx.x < total ? (total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    // each CTA walks one contiguous run of the chunk-major item list: its reads of every Z panel
+    // (l, c) and writes of every Z'' panel (k, c) are sequential streams, and B_c changes only
+    // when the run crosses a chunk (at most ~2 rebuilds per CTA)
+    const int it0 = static_cast<int>(static_cast<long long>(blockIdx.x) * total / gridDim.x);
+    const int cnt = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * total / gridDim.x) - it0;
     auto item = [&](int j, int& T, int& c) {
-        const int i = blockIdx.x + j * gridDim.x;
-        T = i / nchunks;
-        c = i - T * nchunks;
+        const int i = it0 + j;
+        c = i / tiles;
+        T = i - c * tiles;
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s < S2M_ASTAGES; ++s) {
@@ -1019,7 +1023,9 @@ __global__ void __launch_bounds__(S2M_THREADS, 1)
             const int bb = j & 1;
             if (j >= 2) ptx::mbar_wait(b_empty + 8 * bb, ((j >> 1) - 1) & 1);
             const uint32_t b0 = base + L.b + bb * L.b_bytes;
-            for (int lk = tb; lk < b1 * b2; lk += 64) {
+            int Tp = 0, cp = -1;
+            if (j >= 2) item(j - 2, Tp, cp);  // the item that last used this buffer
+            for (int lk = tb; lk < b1 * b2 && c != cp; lk += 64) {
                 const int l = lk / b2, k = lk - l * b2;
                 const uint4 w = __ldg(reinterpret_cast<const uint4*>(S + static_cast<long long>(lk) * r + c * 8));
                 const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
