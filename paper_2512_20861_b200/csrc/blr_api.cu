@@ -165,6 +165,11 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) 
     const char* e = getenv("BLR_NO_RESIDENT");
     const bool reuse = p.tiles_m >= 2 && p.n_sub == 1 && p.kb_half <= blr::MAX_BRES - 1 && !(e && e[0] == '1');
     const char* kb_env = getenv("BLR_KBOX");
+    const char* sc_env = getenv("BLR_SCORE");
+    // long persistent runs (>= 2 tiles per CTA) are steady-state pipelines: score the K blocks in
+    // flight behind the stage the MMA is consuming, (stages - 1) * kbox (Llama-7B Monarch down S1
+    // 3.67 -> 3.05 ms); short one-tile kernels keep the plain ring depth (GPT2-S c_proj S1 24 vs 28 us)
+    const bool score_new = sc_env ? sc_env[0] != '0' : p.total_tiles >= 2 * sms;
     const int kbox_max = (kb_env && kb_env[0] == '1') ? 1 : (p.k_blocks >= 2 ? 2 : 1);
     // Per residency mode, pick (kbox, staging buffers, stages) maximising the 64-wide K blocks in
     // flight (latency hiding of the operand ring); prefer two staging buffers on ties.
@@ -181,7 +186,8 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) 
                 for (q.stages = blr::MAX_STAGES; q.stages >= 2; --q.stages)
                     if (fits(q)) break;
                 if (q.stages < 2 || !fits(q) || (resident && q.stages < 3)) continue;
-                const int score = std::min(q.stages * kbox, 8) * 4 + (bufs == 2 ? 1 : 0) + (kbox == 2 ? 2 : 0);
+                const int score = score_new ? std::min((q.stages - 1) * kbox, 8) * 4 + (bufs == 2 ? 1 : 0) + (kbox == 2 ? 2 : 0)
+                                            : std::min(q.stages * kbox, 8) * 4 + (bufs == 2 ? 1 : 0) + (kbox == 2 ? 2 : 0);
                 if (score > best_score) {
                     best_score = score;
                     best = q;
