@@ -166,6 +166,7 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) 
     const bool reuse = p.tiles_m >= 2 && p.n_sub == 1 && p.kb_half <= blr::MAX_BRES - 1 && !(e && e[0] == '1');
     const char* kb_env = getenv("BLR_KBOX");
     const char* sc_env = getenv("BLR_SCORE");
+    const char* bufs_env = getenv("BLR_BUFS");
     // long persistent runs (>= 2 tiles per CTA) are steady-state pipelines: score the K blocks in
     // flight behind the stage the MMA is consuming, (stages - 1) * kbox (Llama-7B Monarch down S1
     // 3.67 -> 3.05 ms); short one-tile kernels keep the plain ring depth (GPT2-S c_proj S1 24 vs 28 us)
@@ -178,6 +179,7 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) 
         KParams best = p;
         for (int kbox = kbox_max; kbox >= 1; --kbox) {
             for (int bufs = 2; bufs >= 1; --bufs) {
+                if (bufs_env && atoi(bufs_env) != bufs) continue;
                 KParams q = p;
                 q.b_resident = resident;
                 q.kbox = kbox;

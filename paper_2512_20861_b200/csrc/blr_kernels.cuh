@@ -660,6 +660,44 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     for (int j = 0; j < 8; ++j)
                         if (j * 8 < CW) ptx::tmem_ld_x8(tbase + c0 + j * 8, *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
                     ptx::tmem_wait_ld();
+                    if constexpr (OUTF == 2) {
+                        // chunk-blocked fp16 output [g][N/8][t][8]: the four warps of this column half
+                        // (one per TMEM lane quarter) stage the chunk's 128 rows together and one
+                        // thread stores each 8-column panel as ONE 2-KB bulk copy (per-quarter
+                        // 512-B copies made the S1 epilogue TMA-op bound: 96 copies per tile)
+                        const uint32_t hbuf_bytes = 128u * CW * 2u;
+                        const uint32_t hbuf = sbase + L.c_off + half * 4u * p.stage_warp_bytes +
+                                              (nstore % p.stage_bufs) * hbuf_bytes;
+                        ++nstore;
+                        const bool iss = (ew & 3) == 0 && lane == 0;
+                        if (iss) {
+                            if (p.stage_bufs == 2) ptx::bulk_wait_read<1>();
+                            else ptx::bulk_wait_read<0>();
+                        }
+                        ptx::named_bar_sync(2 + half, 128);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            if (j * 8 < CW) {
+                                uint4 w;
+                                w.x = ptx::pack_f16x2(fv[j * 8 + 0], fv[j * 8 + 1]);
+                                w.y = ptx::pack_f16x2(fv[j * 8 + 2], fv[j * 8 + 3]);
+                                w.z = ptx::pack_f16x2(fv[j * 8 + 4], fv[j * 8 + 5]);
+                                w.w = ptx::pack_f16x2(fv[j * 8 + 6], fv[j * 8 + 7]);
+                                ptx::st_shared_v4(hbuf + j * 2048u + (quarter * 32u + lane) * 16u, w);
+                            }
+                        }
+                        ptx::fence_async_smem();
+                        ptx::named_bar_sync(2 + half, 128);
+                        if (iss && !(p.dbg & 1)) {
+                            const int nch = p.N >> 3, rows = min(BM, p.n_tok - m0);
+                            auto* ob = static_cast<uint16_t*>(p.out_ptr) + tc.g * p.out_gstride;
+                            for (int j = 0; j < CW / 8 && ((n0 + c0) >> 3) + j < nch; ++j)
+                                ptx::bulk_store(ob + ((static_cast<long long>((n0 + c0) >> 3) + j) * p.n_tok + m0) * 8,
+                                                hbuf + j * 2048u, rows * 16);
+                            ptx::bulk_commit();
+                        }
+                        continue;
+                    }
                     for (int part = 0; part < parts; ++part) {
                         const uint32_t buf = stg + (nstore % p.stage_bufs) * buf_bytes;
                         ++nstore;
