@@ -338,7 +338,7 @@ struct OutMap {  // 4-D view (N, comp, groups, rows) of a GEMM phase's output
     int64_t comp_stride;   // elements between hi and lo
     int64_t group_stride;  // elements between groups
     int64_t row_stride;    // elements between rows
-    int blocked = 0;       // 1: chunk-blocked [g][N/8][rows][8] (BLAST Z with the tensor-core S2)
+    int blocked = 0;       // 1: tile-blocked [g][T][N/8][128][8] (BLAST Z with the tensor-core S2)
 };
 
 // One plain GEMM phase: out[g](t, c) = sum_k A[g](t, k) B[g](k, c), K-major A.
@@ -387,7 +387,7 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     KParams p;
     int pair = 1;
     const char* pe = getenv("BLR_PAIR");
-    // bulk-copied (chunk-blocked) A completes on the issuing CTA's barrier: single-CTA MMAs only
+    // bulk-copied (tile-blocked) A completes on the issuing CTA's barrier: single-CTA MMAs only
     // (a pair variant that relayed the peer's A arrival to the leader measured no faster on the
     //  Llama-7B S3 expands: 2.58 / 1.24 ms vs 2.54 / 0.91 ms)
     const int force = a_blocked ? 1 : (pe ? atoi(pe) : 0);
@@ -411,7 +411,7 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     p.a_nchunks = static_cast<int>(K / 8);
 
     CUtensorMap ta, tb, tc;
-    // (a chunk-blocked A / output moves by 1-D bulk copies in the kernel; the maps below are then
+    // (a tile-blocked A / output moves by 1-D bulk copies in the kernel; the maps below are then
     // encoded over the same buffer but unused)
     {
         const int64_t Ka = K * comp;  // A row length actually stored
@@ -644,9 +644,11 @@ blr_status decode_k(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int
 }
 
 size_t blast_ws_bytes(int64_t n_tok, int64_t b1, int64_t b2, int64_t r) {
-    const size_t zpp = static_cast<size_t>(b2) * n_tok * r * 2 * comp_factor(r);
-    if (blast_fused(b1, r)) return zpp;
-    return zpp + static_cast<size_t>(b1) * n_tok * r * 2;  // + fp16 Z_l of the separate S1
+    if (blast_fused(b1, r)) return static_cast<size_t>(b2) * n_tok * r * 2 * comp_factor(r);
+    // split path: Z'' and the fp16 Z_l of the separate S1, token count padded to whole 128-row
+    // tiles (the tensor-core S2 path stores both tile-blocked)
+    const int64_t np = rup(n_tok, blr::BM);
+    return static_cast<size_t>(b2) * np * r * 2 * comp_factor(r) + static_cast<size_t>(b1) * np * r * 2;
 }
 
 }  // namespace
@@ -958,18 +960,22 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
     } else {
         // ---- S1: Z[l][t][rho] = (X_l V_l)[t, rho]  -- grouped GEMM over l (A = X viewed (p, b1, n))
         const char* s2e = getenv("BLR_S2");
-        // tensor-core S2 (single-rounded Z''): Z and Z'' chunk-blocked [g][r/8][n][8]
+        // tensor-core S2 (single-rounded Z''): Z and Z'' tile-blocked [g][T][r/8][128][8]
         const bool s2_mma = comp == 1 && !(s2e && !strcmp(s2e, "cuda"));
-        void* zl = static_cast<char*>(workspace) + static_cast<size_t>(b2) * n_tok * r * 2 * comp;
-        OutMap zmap{zl, 2, 1, r, n_tok * r, r};
+        const int64_t n_pad = rup(n_tok, blr::BM);
+        void* zl = static_cast<char*>(workspace) + static_cast<size_t>(b2) * n_pad * r * 2 * comp;
+        // tile-blocked Z for the tensor-core S2: [l][T][r/8][128][8], group stride n_pad * r
+        OutMap zmap{zl, 2, 1, r, s2_mma ? n_pad * r : n_tok * r, r};
         zmap.blocked = s2_mma ? 1 : 0;
         s = gemm_phase(d, dev, st, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true, zmap, 1);
         if (s != BLR_OK) return s;
         // ---- S2: Z''[k][t][rho] = sum_l S[l,k,rho] Z[l][t][rho]
         if (s2_mma) {
-            // tensor-core S2 (blast_s2_mma_kernel): chunk-blocked fp16 Z [l][r/8][n][8] in,
-            // chunk-blocked bf16 Z'' [k][r/8][n][8] out (2-KB panels, 1-D bulk copies)
+            // tensor-core S2 (blast_s2_mma_kernel): tile-blocked fp16 Z [l][T][r/8][128][8] in,
+            // tile-blocked bf16 Z'' [k][T][r/8][128][8] out (2-KB panels, 1-D bulk copies)
             const blr::S2MLayout sl = blr::s2m_layout(static_cast<int>(b1), static_cast<int>(b2));
+            const char* oe = getenv("BLR_S2_ORDER");
+            const int s2_order = oe ? atoi(oe) : 0;
             const int64_t items = cdiv(n_tok, 128) * (r / 8);
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(items, d.sm_count)));
@@ -995,7 +1001,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             if (cudaLaunchKernelEx(&cfg, blr::blast_s2_mma_kernel, static_cast<const __half*>(zl),
                                    static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
                                    static_cast<int>(n_tok), static_cast<int>(b1), static_cast<int>(b2),
-                                   static_cast<int>(r)) != cudaSuccess)
+                                   static_cast<int>(r), s2_order) != cudaSuccess)
                 return BLR_ERR_CUDA;
             if (cudaGetLastError() != cudaSuccess) return BLR_ERR_CUDA;
             if (prof) {

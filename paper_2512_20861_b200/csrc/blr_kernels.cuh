@@ -51,8 +51,8 @@ struct KParams {
     int kb_half;      // K blocks per part: blocks >= kb_half read the lo half of A
     int a_lo_off;     // column offset of the lo half inside A's rows (0: not compensated)
     int a_gmid;       // A map coordinate order: 0 = (k, t, g), 1 = (k, g, t)
-    int a_blocked;    // 1: A stored chunk-blocked [g][K/8][t][8] (BLAST Z''): a 64-K block is 8
-                      //    contiguous 2-KB panels, bulk-copied to 8 no-swizzle K core-matrix columns
+    int a_blocked;    // 1: A stored tile-blocked [g][T][K/8][128][8] (BLAST Z''): a 64-K block of a
+                      //    tile is 8 adjacent 2-KB panels, one bulk copy into 8 no-swizzle K core-matrix columns
     const __nv_bfloat16* a_ptr;  // a_blocked: A base
     int a_nchunks;               // a_blocked: K / 8
     int kbox;         // 64-wide K blocks per pipeline stage (1 or 2; 2 halves the handshakes)
@@ -74,7 +74,7 @@ struct KParams {
     uint32_t c_swz;        // staging swizzle mask (7: 128 B, 3: 64 B, 1: 32 B, 0: none) = TMA map's
     uint32_t stage_warp_bytes;  // staging bytes per epilogue warp
     int stage_bufs;        // staging buffers per warp (GEMM / Monarch kinds)
-    void* out_ptr;         // OUTF 2 (chunk-blocked [g][N/8][t][8] fp16, bulk stores): output base
+    void* out_ptr;         // OUTF 2 (tile-blocked [g][T][N/8][128][8] fp16, bulk stores): output base
     long long out_gstride; // OUTF 2: elements between groups
     int r_blk;             // Monarch: r'
     int kb_per_tile;       // Monarch: output blocks k per N tile
@@ -227,8 +227,7 @@ __device__ __forceinline__ void stage_row8(uint32_t buf, int row, int chunk, uin
         w.z = ptx::pack_bf16x2(r[4], r[5]);
         w.w = ptx::pack_bf16x2(r[6], r[7]);
     }
-    // OUTF 2 (chunk-blocked output): staging [chunk][32 rows][16 B], one bulk store per chunk
-    uint32_t off = OUTF == 2 ? chunk * 512 + row * 16 : row * row_bytes + chunk * 16;
+    uint32_t off = row * row_bytes + chunk * 16;
     off ^= ((off >> 7) & swz) << 4;
     ptx::st_shared_v4(buf + off, w);
 }
@@ -236,7 +235,7 @@ __device__ __forceinline__ void stage_row8(uint32_t buf, int row, int chunk, uin
 // PAIR == 2: CTA pair (cluster of 2, tcgen05 cta_group::2): tile M = 256 tokens, each CTA loads
 // its own 128 A rows and half of B's N columns (per-SM weight ingress halves); the leader CTA
 // issues the MMAs; commits are multicast to both CTAs; each CTA drains its own TMEM rows.
-// OUTF (GEMM kind only): output 0 = bf16, 1 = fp16, 2 = fp16 chunk-blocked [g][N/8][t][8].
+// OUTF (GEMM kind only): output 0 = bf16, 1 = fp16, 2 = fp16 tile-blocked [g][T][N/8][128][8].
 template <int KIND, int PAIR, int OUTF = 0>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     blr_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -350,7 +349,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int it = 0; it < ntiles; ++it) {
                 const TileCoord tc = tile_get(p, titer, tile_tab, it);
                 const int m0 = (tc.m_blk * PAIR + static_cast<int>(crank)) * BM;
-                const int a_rows = min(BM, p.n_tok - m0);  // a_blocked: rows bulk-copied
                 const int n0 = tc.n_blk * p.BN + static_cast<int>(crank) * (p.BN / PAIR);  // this CTA's B half
                 // Monarch: first output block k of this CTA's share of the tile's k blocks
                 const int kblk0 = tc.n_blk * p.kb_per_tile + static_cast<int>(crank) * (p.kb_per_tile / PAIR);
@@ -389,7 +387,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         const uint32_t a_st = a_base + stage * (a_blk * p.kbox);
                         const uint32_t b_st = b_base + stage * (p.b_stage_bytes * p.kbox);
                         if (ptx::elect_one()) {
-                            if (leader) ptx::mbar_arrive_expect_tx(fb, p.a_blocked ? tx - p.kbox * (BM - a_rows) * 128 : tx);
+                            if (leader) ptx::mbar_arrive_expect_tx(fb, tx);  // (tile-blocked A: always full tiles)
                             if (trace && nstep_tr < 32) trace[64 + nstep_tr] = clock64();
                             for (int j = 0; j < p.kbox; ++j) {
                                 const int kb = si * p.kbox + j;
@@ -399,14 +397,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 const int part = (p.a_lo_off > 0 && kb >= p.kb_half) ? 1 : 0;
                                 const int k0 = (kb - part * p.kb_half) * BK;  // padded block: k0 >= K, zero-filled
                                 if constexpr (KIND == KIND_GEMM) {
-                                    if (p.a_blocked) {  // 8 panels [t][8] of rows m0.. (chunks past K clamped)
-                                        const int nch = a_nch;
-                                        for (int ch = 0; ch < 8; ++ch) {
-                                            const int cc = min((k0 >> 3) + ch, nch - 1);
-                                            ptx::bulk_load(a_dst + ch * (BM * 16),
-                                                           p.a_ptr + ((static_cast<long long>(tc.g) * nch + cc) * p.n_tok + m0) * 8,
-                                                           a_rows * 16, fb);
-                                        }
+                                    if (p.a_blocked) {
+                                        // tile-blocked A [g][T][K/8][128][8]: the k-block's 8 panels
+                                        // of tile T are one contiguous 16 KB (panels past K -- also
+                                        // whole padded k-blocks of a kbox pair -- repeat the last
+                                        // panel: finite values against B's zero-filled rows)
+                                        const int nch = a_nch, c0b = k0 >> 3, nv = max(0, min(8, nch - c0b));
+                                        const __nv_bfloat16* tile_a =
+                                            p.a_ptr + (static_cast<long long>(tc.g) * p.tiles_m + tc.m_blk) * nch * (BM * 8);
+                                        if (nv > 0)
+                                            ptx::bulk_load(a_dst, tile_a + static_cast<long long>(c0b) * (BM * 8),
+                                                           static_cast<uint32_t>(nv) * 2048u, fb);
+                                        for (int ch = nv; ch < 8; ++ch)
+                                            ptx::bulk_load(a_dst + ch * 2048u, tile_a + static_cast<long long>(nch - 1) * (BM * 8),
+                                                           2048u, fb);
                                     } else if (p.a_gmid)
                                         load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, tc.g, m0);
                                     else
@@ -451,7 +455,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // descriptors are built once; per-MMA only the 14-bit start-address field advances
             // (a 32-bit add on the low word: the field never carries out)
             // A: K-major 128-B swizzle (8-row groups 1024 B apart, +32 B per K=16), or for a
-            // chunk-blocked A the no-swizzle core-matrix layout [c][t][8] (LBO = BM*16 B between
+            // tile-blocked A the no-swizzle core-matrix layout [c][t][8] (LBO = BM*16 B between
             // K core matrices, SBO = 128 B between 8-row groups, +2 core matrices per K=16)
             const uint64_t a_desc0 = p.a_blocked ? ptx::smem_desc(a_base, BM * 16, 128, 0)
                                                  : ptx::smem_desc(a_base, 16, 1024, ptx::LAYOUT_SW128);
@@ -661,10 +665,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (j * 8 < CW) ptx::tmem_ld_x8(tbase + c0 + j * 8, *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
                     ptx::tmem_wait_ld();
                     if constexpr (OUTF == 2) {
-                        // chunk-blocked fp16 output [g][N/8][t][8]: the four warps of this column half
-                        // (one per TMEM lane quarter) stage the chunk's 128 rows together and one
-                        // thread stores each 8-column panel as ONE 2-KB bulk copy (per-quarter
-                        // 512-B copies made the S1 epilogue TMA-op bound: 96 copies per tile)
+                        // tile-blocked fp16 output [g][T][N/8][128][8]: the four warps of this column
+                        // half (one per TMEM lane quarter) stage the chunk's 128 rows together and one
+                        // thread stores the chunk's panels as ONE bulk copy (per-quarter 512-B copies
+                        // made the S1 epilogue TMA-op bound: 96 copies per tile)
                         const uint32_t hbuf_bytes = 128u * CW * 2u;
                         const uint32_t hbuf = sbase + L.c_off + half * 4u * p.stage_warp_bytes +
                                               (nstore % p.stage_bufs) * hbuf_bytes;
@@ -689,11 +693,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         ptx::fence_async_smem();
                         ptx::named_bar_sync(2 + half, 128);
                         if (iss && !(p.dbg & 1)) {
-                            const int nch = p.N >> 3, rows = min(BM, p.n_tok - m0);
+                            // tile-blocked [g][T][N/8][128][8]: this chunk's panels of tile T are
+                            // contiguous -> one bulk copy (rows >= n_tok are zeros: A was OOB-filled)
+                            const int nch = p.N >> 3, cc = (n0 + c0) >> 3, npan = min(CW / 8, nch - cc);
                             auto* ob = static_cast<uint16_t*>(p.out_ptr) + tc.g * p.out_gstride;
-                            for (int j = 0; j < CW / 8 && ((n0 + c0) >> 3) + j < nch; ++j)
-                                ptx::bulk_store(ob + ((static_cast<long long>((n0 + c0) >> 3) + j) * p.n_tok + m0) * 8,
-                                                hbuf + j * 2048u, rows * 16);
+                            const int T = m0 / BM;
+                            if (npan > 0)
+                                ptx::bulk_store(ob + (static_cast<long long>(T) * nch + cc) * (BM * 8), hbuf,
+                                                static_cast<uint32_t>(npan) * 2048u);
                             ptx::bulk_commit();
                         }
                         continue;
@@ -931,15 +938,16 @@ __global__ void __launch_bounds__(32 * 16, 1)
 // M = 128 tokens, K = 8 b1, N = 8 b2 (<= 128).  In the canonical no-swizzle K-major UMMA layout
 // an 8x8 core matrix of B_c is exactly diag(S[l, k, 8c .. 8c+7]), so B_c is a fixed zero
 // pattern whose 8 b1 b2 diagonal entries are rewritten per item (S converted bf16 -> fp16), and
-// the A operand is b1 panels of Z: core matrix (t/8, l) = 8 rows x 16 B.  Z and Z'' are stored
-// chunk-blocked, [l][c][t][8] and [k][c][t][8], so each (l, c) / (k, c) panel of
-// a token tile is 2 KB contiguous, moved by one 1-D bulk copy (a tensor box with 16-B rows moves
-// one row per request: measured 2x slower).  The S1 epilogue writes that layout, S3 reads it.
+// the A operand is b1 panels of Z: core matrix (t/8, l) = 8 rows x 16 B, each panel moved by one
+// 1-D bulk copy (a tensor box with 16-B rows moves one row per request: measured 2x slower).  The
+// S1 epilogue writes that layout, S3 reads it.
 // fp16 x fp16 products are exact, accumulation fp32; Z'' is rounded once to bf16 (RNE).
-// Items (128-token tile T, chunk c) are enumerated chunk-major and each CTA walks one contiguous
-// run of them (sequential panel streams; B_c rebuilt only when the run changes chunk).
+// Z and Z'' are tile-blocked, [l][T][r/8][128][8] and [k][T][r/8][128][8]: every
+// (l, T, c) panel is 2 KB contiguous and the panels c = 0.. of one tile are adjacent.  Items
+// (128-token tile T, chunk c) are enumerated tile-major and each CTA walks one contiguous run of
+// them, so its b1 panel reads and b2 panel writes are sequential streams.
 // Roles: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-3 build B_c, warps 4-7
-// epilogue (TMEM -> bf16 -> smem [k][t][8] -> b2 bulk stores of the (k, c) panels).
+// epilogue (TMEM -> bf16 -> smem [k][t][8] -> b2 bulk stores of the (k, T, c) panels).
 constexpr int S2M_ASTAGES = 3;
 constexpr int S2M_THREADS = 256;
 struct S2MLayout {  // byte offsets in dynamic smem (1024-aligned base)
@@ -963,7 +971,7 @@ __host__ __device__ inline S2MLayout s2m_layout(int b1, int b2) {
 
 __global__ void __launch_bounds__(S2M_THREADS, 1)
     blast_s2_mma_kernel(const __half* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
-                        const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r) {
+                        const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order) {
     extern __shared__ __align__(1024) uint8_t s2m_smem[];
     const S2MLayout L = s2m_layout(b1, b2);
     const int b1p = (b1 + 1) & ~1;
@@ -980,10 +988,16 @@ __global__ void __launch_bounds__(S2M_THREADS, 1)
     // when the run crosses a chunk (at most ~2 rebuilds per CTA)
     const int it0 = static_cast<int>(static_cast<long long>(blockIdx.x) * total / gridDim.x);
     const int cnt = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * total / gridDim.x) - it0;
+    const bool tile_major = order != 0;
     auto item = [&](int j, int& T, int& c) {
         const int i = it0 + j;
-        c = i / tiles;
-        T = i - c * tiles;
+        if (tile_major) {  // panels (l, T, c), c = 0.. adjacent: sequential streams
+            T = i / nchunks;
+            c = i - T * nchunks;
+        } else {  // chunk-major: B_c rebuilt only when the run changes chunk
+            c = i / tiles;
+            T = i - c * tiles;
+        }
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s < S2M_ASTAGES; ++s) {
@@ -1019,12 +1033,11 @@ __global__ void __launch_bounds__(S2M_THREADS, 1)
                 int T, c;
                 item(j, T, c);
                 const int s = j % S2M_ASTAGES;
-                const int rows = min(128, n_tok - T * 128);
                 if (j >= S2M_ASTAGES) ptx::mbar_wait(a_empty + 8 * s, ((j / S2M_ASTAGES) - 1) & 1);
-                ptx::mbar_arrive_expect_tx(a_full + 8 * s, static_cast<uint32_t>(b1 * rows * 16));
-                for (int l = 0; l < b1; ++l)  // panel (l, c), rows T*128.. : contiguous rows x 16 B
+                ptx::mbar_arrive_expect_tx(a_full + 8 * s, static_cast<uint32_t>(b1 * 2048));
+                for (int l = 0; l < b1; ++l)  // panel (l, T, c): 128 rows x 16 B contiguous
                     ptx::bulk_load(base + L.a + s * L.a_bytes + l * 2048,
-                                   Z + ((static_cast<long long>(l) * nchunks + c) * n_tok + T * 128) * 8, rows * 16,
+                                   Z + ((static_cast<long long>(l) * tiles + T) * nchunks + c) * 1024, 2048,
                                    a_full + 8 * s);
             }
         }
@@ -1066,14 +1079,15 @@ __global__ void __launch_bounds__(S2M_THREADS, 1)
             for (int lk = tb; lk < b1 * b2 && c != cp; lk += 64) {
                 const int l = lk / b2, k = lk - l * b2;
                 const uint4 w = __ldg(reinterpret_cast<const uint4*>(S + static_cast<long long>(lk) * r + c * 8));
-                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
                 const uint32_t cm = b0 + k * sbo + l * 128;  // core matrix (k, l): diag at rho*18 B
+                // every core matrix starts on bank 0, so entry rho's bank depends on rho alone:
+                // lane-rotated rho order -> 8 distinct banks per store (4-way instead of 32-way)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const __half h0 = __float2half_rn(__uint_as_float(ww[e] << 16));
-                    const __half h1 = __float2half_rn(__uint_as_float(ww[e] & 0xFFFF0000u));
-                    ptx::st_shared_u16(cm + (2 * e) * 18, __half_as_ushort(h0));
-                    ptx::st_shared_u16(cm + (2 * e + 1) * 18, __half_as_ushort(h1));
+                for (int e8 = 0; e8 < 8; ++e8) {
+                    const int rho = (e8 + lane) & 7;
+                    const uint32_t wd = (rho & 4) ? ((rho & 2) ? w.w : w.z) : ((rho & 2) ? w.y : w.x);
+                    const float f = __uint_as_float((rho & 1) ? (wd & 0xFFFF0000u) : (wd << 16));
+                    ptx::st_shared_u16(cm + rho * 18, __half_as_ushort(__float2half_rn(f)));
                 }
             }
             ptx::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
@@ -1117,10 +1131,9 @@ __global__ void __launch_bounds__(S2M_THREADS, 1)
             ptx::fence_async_smem();
             ptx::named_bar_sync(1, 128);
             if (issuer) {
-                const int rows = min(128, n_tok - T * 128);
-                for (int k = 0; k < b2; ++k)
-                    ptx::bulk_store(Zpp + ((static_cast<long long>(k) * nchunks + c) * n_tok + T * 128) * 8,
-                                    base + L.c + cb * L.c_bytes + k * 2048, rows * 16);
+                for (int k = 0; k < b2; ++k)  // panel (k, T, c)
+                    ptx::bulk_store(Zpp + ((static_cast<long long>(k) * tiles + T) * nchunks + c) * 1024,
+                                    base + L.c + cb * L.c_bytes + k * 2048, 2048);
                 ptx::bulk_commit();
             }
         }
