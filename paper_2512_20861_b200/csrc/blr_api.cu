@@ -13,6 +13,7 @@
 #include "../../include/blr.h"
 #include "blr_kernels.cuh"
 #include "blr_decode.cuh"
+#include "blr_fused.cuh"
 
 namespace {
 
@@ -30,7 +31,7 @@ struct DevInfo {
 std::mutex g_mu;
 DevInfo g_dev[64];
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-bool g_attr_set[13][64] = {};  // kernel attribute set, per (kernel variant, device)
+bool g_attr_set[16][64] = {};  // kernel attribute set, per (kernel variant, device)
 thread_local int t_last_launches = 0;
 thread_local void** t_prof_events = nullptr;
 thread_local int t_prof_cap = 0;
@@ -463,6 +464,118 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     return launch<blr::KIND_GEMM, 1>(ta, tb, tc, p, d, dev, st);
 }
 
+// ------------------------------------------------------- one-launch LR / Monarch layer ----
+// blr_fused.cuh: S1 and S3 of a token tile in one CTA, Z on chip.  Used when the intermediate
+// fits one 256-column TMEM buffer and the swizzled smem copy (128 <= k2 <= 256, k2 % 64 == 0;
+// shorter S3 contractions keep the compensated two-kernel path, R12).  BLR_FUSED=0/1
+// overrides the default.
+// Default: Monarch always (its S1 is block-diagonal, cheap to recompute per output block);
+// low rank only for expanding layers (d_in <= d_out) -- a contracting layer's S1 streams a long
+// X row and all of V per token tile, and its few tiles cannot fill the SMs (GPT2-S c_proj:
+// 46.6 us fused vs 39.7 us in two kernels, c_fc 34.3 vs 37.6 us).
+bool fused_wanted(int64_t n_tok, int64_t k2, int64_t n1, bool contracting_lr) {
+    if (k2 % 64 || k2 < 128 || k2 > 256 || n1 % 16 || n1 > 256) return false;
+    const char* e = getenv("BLR_FUSED");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    return n_tok >= 256 && !contracting_lr;
+}
+
+void fused_b_staging(bool mn, int n, int& boxes, uint32_t& bytes, uint32_t& lbo, uint32_t& sbo, uint32_t& kstep) {
+    if (mn) {  // [K][N] storage: 64-column SW128 boxes (as set_b_staging)
+        boxes = static_cast<int>(cdiv(n, 64));
+        bytes = static_cast<uint32_t>(boxes * 64 * blr::BK * 2);
+        lbo = 64 * 2 * blr::BK;
+        sbo = 1024;
+        kstep = 16 * 128;
+    } else {  // [N][K] storage: n rows x 64 K, K-major SW128
+        boxes = 1;
+        bytes = static_cast<uint32_t>(rup(static_cast<int64_t>(n) * blr::BK * 2, 1024));
+        lbo = 16;
+        sbo = 1024;
+        kstep = 32;
+    }
+}
+
+// p: n_tok, mon, g1, k1_blocks, n1, b1_mn, g2, n2, b2_mn filled by the caller.
+blr_status fused_launch(const DevInfo& d, int dev, cudaStream_t st, blr::FParams p, const CUtensorMap& ta,
+                        const CUtensorMap& tb1, const CUtensorMap& tb2, void* Y, int64_t d_out) {
+    p.tiles_m = static_cast<int>(cdiv(p.n_tok, blr::BM));
+    p.k2 = p.g1 * p.n1;
+    fused_b_staging(p.b1_mn, p.n1, p.b1_boxes, p.b1_bytes, p.b1_lbo, p.b1_sbo, p.b1_kstep);
+    const int64_t nch_tiles = cdiv(p.n2, 256);
+    p.bn2 = static_cast<int>(rup(cdiv(p.n2, nch_tiles), 16));
+    fused_b_staging(p.b2_mn, p.bn2, p.b2_boxes, p.b2_bytes, p.b2_lbo, p.b2_sbo, p.b2_kstep);
+    // Split the S3 columns into parts to fill the SMs, minimising the busiest CTA's work in
+    // units of one S3 chunk: waves x (S1 recompute + chunks per part), S1 weighted by its MACs
+    // relative to a chunk's (a partial second wave idles most SMs for a whole item).
+    const int64_t base = static_cast<int64_t>(p.tiles_m) * p.g2, nchunks = cdiv(p.n2, p.bn2);
+    const double s1_w = static_cast<double>(p.k1_blocks) * p.g1 * p.n1 / (static_cast<double>(p.k2 / 64) * p.bn2);
+    int64_t cpp = nchunks;
+    double best = 1e30;
+    for (int64_t np = 1; np <= nchunks; ++np) {
+        const int64_t c = cdiv(nchunks, np), npp = cdiv(nchunks, c);
+        const double cost = static_cast<double>(cdiv(base * npp, d.sm_count)) * (s1_w + static_cast<double>(c));
+        if (cost < best - 1e-9) {
+            best = cost;
+            cpp = c;
+        }
+    }
+    p.n2_part = static_cast<int>(cpp * p.bn2);
+    p.n_parts = static_cast<int>(cdiv(nchunks, cpp));
+    p.items = static_cast<int>(base * p.n_parts);
+    p.c_box_w = chunk_width(p.bn2);
+    p.c_swz = pick_swz(p.c_box_w * 2).mask;
+    p.stage_warp_bytes = static_cast<uint32_t>(32 * p.c_box_w * 2);
+    p.slot_bytes = static_cast<uint32_t>(rup(std::max<int64_t>(blr::BM * blr::BK * 2 + p.b1_bytes, p.b2_bytes), 1024));
+    for (p.stages = blr::MAX_STAGES; p.stages >= 2; --p.stages)
+        if (blr::fused_layout(p).total + SMEM_SLACK <= static_cast<uint32_t>(SMEM_LIMIT)) break;
+    if (p.stages < 2) return BLR_ERR_UNSUPPORTED;
+    CUtensorMap tc;
+    {
+        const uint64_t dims[4] = {static_cast<uint64_t>(p.n2), 1, static_cast<uint64_t>(p.g2), static_cast<uint64_t>(p.n_tok)};
+        const uint64_t str[3] = {static_cast<uint64_t>(p.n2) * 2, static_cast<uint64_t>(p.n2) * 2,
+                                 static_cast<uint64_t>(d_out) * 2};
+        const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32};
+        if (!encode(&tc, Y, 4, dims, str, box, pick_swz(p.c_box_w * 2).mode)) return BLR_ERR_CUDA;
+    }
+    const int smem = static_cast<int>(blr::fused_layout(p).total + SMEM_SLACK);
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_attr_set[13][dev]) {
+            if (cudaFuncSetAttribute(blr::blr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT) !=
+                cudaSuccess)
+                return BLR_ERR_CUDA;
+            g_attr_set[13][dev] = true;
+        }
+    }
+    const int grid = std::min(p.items, d.sm_count);
+    if (const char* pe = getenv("BLR_PLAN"); pe && pe[0] == '1')
+        fprintf(stderr,
+                "[blr plan] fused mon=%d grid=%d items=%dx%dx%d g1=%d k1b=%d n1=%d k2=%d n2=%d bn2=%d stages=%d "
+                "smem=%d\n",
+                p.mon, grid, p.tiles_m, p.g2, p.n_parts, p.g1, p.k1_blocks, p.n1, p.k2, p.n2, p.bn2, p.stages, smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(blr::NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+    if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, blr::blr_fused_kernel, ta, tb1, tb2, tc, p) != cudaSuccess) return BLR_ERR_CUDA;
+    if (prof) {
+        if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+        ++t_prof_n;
+    }
+    ++t_last_launches;
+    return BLR_OK;
+}
+
 // X viewed as [n_tok][b1][p] (A operand of the block-diagonal first stage).
 bool encode_x_blocked(CUtensorMap* m, const void* X, int64_t n_tok, int64_t b1, int64_t pdim) {
     const uint64_t dims[3] = {static_cast<uint64_t>(pdim), static_cast<uint64_t>(b1), static_cast<uint64_t>(n_tok)};
@@ -742,6 +855,39 @@ blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         if (s != BLR_OK) return s;
         return decode_mn(st, zf, 1, r, 0, U, d_out, 0, Y, 1, d_out, 0, n_tok, r, d_out, 1, part);
     }
+    if (fused_wanted(n_tok, r, r, d_in > d_out)) {  // one launch, Z on chip (blr_fused.cuh)
+        blr::FParams p = {};
+        p.n_tok = static_cast<int>(n_tok);
+        p.mon = 0;
+        p.g1 = 1;
+        p.k1_blocks = static_cast<int>(cdiv(d_in, blr::BK));
+        p.n1 = static_cast<int>(r);
+        p.b1_mn = 1;
+        p.g2 = 1;
+        p.n2 = static_cast<int>(d_out);
+        p.b2_mn = 1;
+        CUtensorMap ta, tb1, tb2;
+        {
+            const uint64_t dims[3] = {static_cast<uint64_t>(d_in), static_cast<uint64_t>(n_tok), 1};
+            const uint64_t str[2] = {static_cast<uint64_t>(d_in) * 2, static_cast<uint64_t>(d_in * n_tok) * 2};
+            const uint32_t box[3] = {blr::BK, blr::BM, 1};
+            if (!encode(&ta, X, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+        }
+        {
+            const uint64_t dims[3] = {static_cast<uint64_t>(r), static_cast<uint64_t>(d_in), 1};
+            const uint64_t str[2] = {static_cast<uint64_t>(r) * 2, static_cast<uint64_t>(r * d_in) * 2};
+            const uint32_t box[3] = {64, blr::BK, 1};
+            if (!encode(&tb1, V, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+        }
+        {
+            const uint64_t dims[3] = {static_cast<uint64_t>(d_out), static_cast<uint64_t>(r), 1};
+            const uint64_t str[2] = {static_cast<uint64_t>(d_out) * 2, static_cast<uint64_t>(d_out * r) * 2};
+            const uint32_t box[3] = {64, blr::BK, 1};
+            if (!encode(&tb2, U, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+        }
+        s = fused_launch(d, dev, st, p, ta, tb1, tb2, Y, d_out);
+        if (s != BLR_ERR_UNSUPPORTED) return s;
+    }
     const int comp = comp_factor(r);
     // S1: Z = X V  (V is [d_in][r]: MN-major B); Z rows [hi | lo] when compensated
     s = gemm_phase(d, dev, st, X, 0, d_in, 0, n_tok, d_in, 1, r, V, true,
@@ -778,6 +924,44 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
                      r_blk * b2, b1, v_layout == BLR_MON_V_B2_FASTEST ? 1 : 2, b2, r_blk);
         if (s != BLR_OK) return s;
         return decode_k(st, zp, 1, K2, n_tok * K2, U, K2, qdim * K2, Y, 1, d_out, qdim, n_tok, K2, qdim, b2, 0, 1, 1);
+    }
+    if (fused_wanted(n_tok, K2, r_blk, false)) {  // one launch, Z'_k on chip (blr_fused.cuh)
+        blr::FParams p = {};
+        p.n_tok = static_cast<int>(n_tok);
+        p.mon = 1;
+        p.g1 = static_cast<int>(b1);
+        p.k1_blocks = static_cast<int>(cdiv(pdim, blr::BK));
+        p.n1 = static_cast<int>(r_blk);
+        p.b1_mn = 0;
+        p.g2 = static_cast<int>(b2);
+        p.n2 = static_cast<int>(qdim);
+        p.b2_mn = 0;
+        CUtensorMap ta, tb1, tb2;
+        if (!encode_x_blocked(&ta, X, n_tok, b1, pdim)) return BLR_ERR_CUDA;
+        {   // V viewed 4-D (a, rho', k, l): box (64, r', 1, 1) = the r' rows m(rho, k) of block (l, k)
+            const uint64_t dims[4] = {static_cast<uint64_t>(pdim), static_cast<uint64_t>(r_blk),
+                                      static_cast<uint64_t>(b2), static_cast<uint64_t>(b1)};
+            uint64_t str[3];
+            if (v_layout == BLR_MON_V_B2_FASTEST) {  // m = rho*b2 + k
+                str[0] = static_cast<uint64_t>(b2 * pdim) * 2;
+                str[1] = static_cast<uint64_t>(pdim) * 2;
+            } else {  // m = k*r' + rho
+                str[0] = static_cast<uint64_t>(pdim) * 2;
+                str[1] = static_cast<uint64_t>(r_blk * pdim) * 2;
+            }
+            str[2] = static_cast<uint64_t>(r_blk * b2 * pdim) * 2;
+            const uint32_t box[4] = {blr::BK, static_cast<uint32_t>(r_blk), 1, 1};
+            if (!encode(&tb1, V, 4, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+        }
+        {   // U [b2][q][b1 r'] K-major; box (64 K, bn2 rows, 1)
+            const int64_t bn2 = rup(cdiv(qdim, cdiv(qdim, 256)), 16);
+            const uint64_t dims[3] = {static_cast<uint64_t>(K2), static_cast<uint64_t>(qdim), static_cast<uint64_t>(b2)};
+            const uint64_t str[2] = {static_cast<uint64_t>(K2) * 2, static_cast<uint64_t>(K2 * qdim) * 2};
+            const uint32_t box[3] = {blr::BK, static_cast<uint32_t>(bn2), 1};
+            if (!encode(&tb2, U, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+        }
+        s = fused_launch(d, dev, st, p, ta, tb1, tb2, Y, d_out);
+        if (s != BLR_ERR_UNSUPPORTED) return s;
     }
     const int comp = comp_factor(K2);
 
