@@ -47,11 +47,12 @@ def test_workspace_sizes():
     assert lib.blr_monarch_workspace_size(100, 64, 64, 4, 2, 32) == 2 * 100 * 4 * 32 * 2
     # BLAST with b1*r <= 512 fuses S1+S2 (only Z''); larger b1*r also keeps the S1 output Z_l
     assert lib.blr_blast_workspace_size(100, 64, 64, 2, 2, 192) == 2 * 100 * 192 * 2
-    assert lib.blr_blast_workspace_size(100, 64, 64, 4, 2, 192) == 2 * 100 * 192 * 2 + 4 * 100 * 192 * 2  # fp16 Z (R13)
+    # split path: Z'' and fp16 Z (R13), token rows padded to whole 128-row tiles (tile-blocked, §5.4)
+    assert lib.blr_blast_workspace_size(100, 64, 64, 4, 2, 192) == 2 * 128 * 192 * 2 + 4 * 128 * 192 * 2
     # shorter contractions keep a compensated hi|lo pair: twice the bytes
     assert lib.blr_lowrank_workspace_size(100, 64, 64, 16) == 2 * 100 * 16 * 2
     assert lib.blr_monarch_workspace_size(100, 64, 64, 4, 2, 8) == 2 * 2 * 100 * 4 * 8 * 2
-    assert lib.blr_blast_workspace_size(100, 64, 64, 4, 2, 16) == 2 * 2 * 100 * 16 * 2
+    assert lib.blr_blast_workspace_size(100, 64, 64, 4, 2, 16) == 2 * 2 * 100 * 16 * 2  # fused (b1 r <= 512)
     assert lib.blr_blast_workspace_size(0, 64, 64, 4, 2, 16) == 0
 
 
