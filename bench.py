@@ -286,7 +286,8 @@ def main():
         for j, L in chain:
             h = call(L, j, h)
             nl = lib.blr_last_launch_count()
-            names = ["proj", "expand"] if nl == 2 else ["s1", "s2", "expand"] if nl == 3 else [f"k{i}" for i in range(nl)]
+            names = (["layer"] if nl == 1 else ["proj", "expand"] if nl == 2 else ["s1", "s2", "expand"] if nl == 3
+                     else [f"k{i}" for i in range(nl)])
             phases += [(j, nm) for nm in names]
     torch.cuda.synchronize()
     n_launch = len(phases)
@@ -469,10 +470,12 @@ def main():
 
 
 def phase_kind(L, phase):
+    if phase == "layer":   # one-launch low-rank / Monarch layer (csrc/blr_fused.cuh)
+        return "blr_fused_kernel"
     if phase in ("expand", "s1"):
         return "blr_gemm_kernel<KIND_GEMM>"
-    if phase == "s2":
-        return "blast_s2_kernel"
+    if phase == "s2":      # tensor-core S2 unless the intermediate is compensated (r < 128)
+        return "blast_s2_mma_kernel" if L.r >= 128 else "blast_s2_kernel"
     return "blr_gemm_kernel<%s>" % {"lowrank": "KIND_GEMM", "monarch": "KIND_MONARCH_PROJ",
                                     "blast": "KIND_BLAST_PROJ"}[L.method]
 
@@ -481,6 +484,10 @@ def phase_counts(L, n, phase):
     """Algorithmic bytes / FLOPs of one phase: proj reads X and the first-stage
     factors (V, and S for BLAST); expand reads U and writes Y.  The intermediate is excluded."""
     B = roofline.BF16
+    if phase == "layer":  # fused layer: X, every factor, Y
+        p1 = phase_counts(L, n, "proj")
+        p3 = phase_counts(L, n, "expand")
+        return {"bytes": p1["bytes"] + p3["bytes"], "flops": p1["flops"] + p3["flops"]}
     if phase == "s1":   # BLAST split path: Z_l = X_l V_l
         return {"bytes": B * (n * L.i + L.i * L.r), "flops": 2 * n * L.i * L.r}
     if phase == "s2":   # BLAST split path: S-weighted block sum (reads S only, algorithmically)
@@ -500,17 +507,19 @@ def phase_counts(L, n, phase):
 def phase_io_bytes(L, n, phase):
     """Bytes the phase's kernel must move in this implementation: its inputs and outputs
     including the intermediate it reads or writes (the compensated hi|lo intermediate counts
-    twice; the BLAST split path's S1 output is fp32).  Context for the fused-roofline figure."""
+    twice; the BLAST split path's S1 output is fp16).  Context for the fused-roofline figure."""
     B = roofline.BF16
     k3 = L.r if L.method != "monarch" else L.b1 * L.r_blk      # S3 contraction length
     comp = 2 if k3 < 128 else 1
     inter = n * L.r * comp if L.method == "lowrank" else (n * L.b * L.r * comp if L.method == "monarch"
                                                           else n * L.b2 * L.r * comp)
     x_v = n * L.i + L.i * L.r
-    if phase == "s1":
-        return B * x_v + 4 * n * L.b1 * L.r
+    if phase == "layer":  # the intermediate stays on chip
+        return B * (x_v + L.r * L.o + n * L.o)
+    if phase == "s1":     # fp16 Z_l (DESIGN.md R13)
+        return B * x_v + 2 * n * L.b1 * L.r
     if phase == "s2":
-        return 4 * n * L.b1 * L.r + B * (L.b1 * L.b2 * L.r + inter)
+        return 2 * n * L.b1 * L.r + B * (L.b1 * L.b2 * L.r + inter)
     if phase == "proj":
         return B * (x_v + inter + (L.b1 * L.b2 * L.r if L.method == "blast" else 0))
     return B * (inter + L.r * L.o + n * L.o)

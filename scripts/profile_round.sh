@@ -7,10 +7,10 @@ mkdir -p gpurun_out profiles
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 BLR_DUMP_PHASES=gpurun_out/phases_$CFG.json python bench.py --config $CFG --steps 1 --warmup 0 --no-dense --no-cpu-baseline --eager > /dev/null 2>&1
 N=$(python -c "import json;print(len(json.load(open('gpurun_out/phases_$CFG.json'))))")
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"blr_gemm|blast_s2" -c $((3*N)) --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"blr_gemm|blast_s2|blr_fused" -c $((3*N)) --csv \
   --log-file gpurun_out/launches_$CFG.csv python bench.py --config $CFG --steps 2 --warmup 0 --no-dense --no-cpu-baseline --eager > /dev/null 2>&1
 echo "launch list rc=$?"
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"blr_gemm|blast_s2" -c $N \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"blr_gemm|blast_s2|blr_fused" -c $N \
   -o gpurun_out/prof_$CFG -f python bench.py --config $CFG --steps 1 --warmup 0 --no-dense --no-cpu-baseline --eager > gpurun_out/ncu_full_$CFG.log 2>&1
 echo "full rc=$?"
 # summaries go to gpurun_out/ (only that directory comes back from the box); copy them into
