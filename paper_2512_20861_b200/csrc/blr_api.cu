@@ -481,6 +481,17 @@ bool fused_wanted(int64_t n_tok, int64_t k2, int64_t n1, bool contracting_lr) {
     return n_tok >= 256 && !contracting_lr;
 }
 
+// BLAST S2 + S3 in one launch (blr_fused.cuh mode 2): few blocks (each item reads b1 Z_l tiles
+// per output block k), 128 <= r <= 256 (Z'' of a tile fits the smem A operand).  Opt-in only
+// (BLR_FUSED=1): measured slower than the tensor-core S2 + S3 kernels on GPT2-S BLAST (c_fc 44.4 vs
+// 17.9 + 23.9 us; the CUDA-core block sum serialises ahead of each item's S3).
+bool blast_s23_wanted(int64_t n_tok, int64_t b1, int64_t r) {
+    if (r % 64 || r < 128 || r > 256 || b1 * r * 4 > (32 << 10)) return false;
+    const char* e = getenv("BLR_FUSED");
+    (void)n_tok;
+    return e && e[0] == '1';
+}
+
 void fused_b_staging(bool mn, int n, int& boxes, uint32_t& bytes, uint32_t& lbo, uint32_t& sbo, uint32_t& kstep) {
     if (mn) {  // [K][N] storage: 64-column SW128 boxes (as set_b_staging)
         boxes = static_cast<int>(cdiv(n, 64));
@@ -527,7 +538,8 @@ blr_status fused_launch(const DevInfo& d, int dev, cudaStream_t st, blr::FParams
     p.c_box_w = chunk_width(p.bn2);
     p.c_swz = pick_swz(p.c_box_w * 2).mask;
     p.stage_warp_bytes = static_cast<uint32_t>(32 * p.c_box_w * 2);
-    p.slot_bytes = static_cast<uint32_t>(rup(std::max<int64_t>(blr::BM * blr::BK * 2 + p.b1_bytes, p.b2_bytes), 1024));
+    if (p.mon != 2) p.s1_bytes = static_cast<uint32_t>(blr::BM * blr::BK * 2) + p.b1_bytes;
+    p.slot_bytes = static_cast<uint32_t>(rup(std::max<int64_t>(p.s1_bytes, p.b2_bytes), 1024));
     for (p.stages = blr::MAX_STAGES; p.stages >= 2; --p.stages)
         if (blr::fused_layout(p).total + SMEM_SLACK <= static_cast<uint32_t>(SMEM_LIMIT)) break;
     if (p.stages < 2) return BLR_ERR_UNSUPPORTED;
@@ -1153,6 +1165,35 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         zmap.blocked = s2_mma ? 1 : 0;
         s = gemm_phase(d, dev, st, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true, zmap, 1);
         if (s != BLR_OK) return s;
+        // ---- S2 + S3 in one launch for few blocks (blr_fused.cuh mode 2): Z'' stays on chip
+        if (s2_mma && blast_s23_wanted(n_tok, b1, r)) {
+            blr::FParams p = {};
+            p.n_tok = static_cast<int>(n_tok);
+            p.mon = 2;
+            p.z = static_cast<const __half*>(zl);
+            p.S = static_cast<const __nv_bfloat16*>(S);
+            p.b1 = static_cast<int>(b1);
+            p.r = static_cast<int>(r);
+            p.s1_bytes = static_cast<uint32_t>(b1) * 8192u;
+            p.stab_bytes = static_cast<uint32_t>(b1 * r * 4);
+            p.g1 = 1;
+            p.k1_blocks = static_cast<int>(r / 32);
+            p.n1 = static_cast<int>(r);
+            p.b1_mn = 1;
+            p.g2 = static_cast<int>(b2);
+            p.n2 = static_cast<int>(qdim);
+            p.b2_mn = 1;
+            CUtensorMap tb2;
+            {   // U [b2][r][q]: MN-major, box (64 cols, 64 K rows, 1)
+                const uint64_t dims[3] = {static_cast<uint64_t>(qdim), static_cast<uint64_t>(r), static_cast<uint64_t>(b2)};
+                const uint64_t str[2] = {static_cast<uint64_t>(qdim) * 2, static_cast<uint64_t>(qdim * r) * 2};
+                const uint32_t box[3] = {64, blr::BK, 1};
+                if (!encode(&tb2, U, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+            }
+            // (the A / B1 maps are unused in mode 2: pass U's map in their place)
+            s = fused_launch(d, dev, st, p, tb2, tb2, tb2, Y, d_out);
+            if (s != BLR_ERR_UNSUPPORTED) return s;
+        }
         // ---- S2: Z''[k][t][rho] = sum_l S[l,k,rho] Z[l][t][rho]
         if (s2_mma) {
             // tensor-core S2 (blast_s2_mma_kernel): tile-blocked fp16 Z [l][T][r/8][128][8] in,

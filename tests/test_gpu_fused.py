@@ -89,3 +89,37 @@ def test_fused_matches_two_kernel_path_and_is_deterministic(cuda_lib, monkeypatc
     assert torch.equal(Yf, Yf2)
     d = (Yf.float() - Ys.float()).abs()
     assert torch.all(d <= 2.0 ** -6 * Ys.float().abs() + 1e-2)
+
+
+BLAST_S23 = [  # (n, b1, b2, r, p, q): split path (b1 r > 512) with the S2 + S3 launch (mode 2)
+    (1000, 6, 6, 192, 128, 512),   # GPT2-S c_fc BLAST
+    (300, 6, 6, 192, 512, 128),    # GPT2-S c_proj BLAST
+    (257, 5, 3, 128, 40, 200),     # b1 != b2, q % 16 != 0, ragged tail
+    (700, 8, 8, 256, 128, 256),
+]
+
+
+@pytest.mark.parametrize("n,b1,b2,r,p,q", BLAST_S23)
+def test_blast_s2_s3_fused_parity(cuda_lib, monkeypatch, n, b1, b2, r, p, q):
+    """S2 (fp32 on CUDA cores, ascending l) formed straight into the S3 operand in shared memory."""
+    monkeypatch.setenv("BLR_FUSED", "1")
+    X = synth.make_x(n, b1 * p, seed=25)
+    V, S, U = synth.blast_factors(b1 * p, b2 * q, b1, b2, r, seed=25)
+    Y = cuda_lib.blast_matmul(X.to(DEV), V.to(DEV), S.to(DEV), U.to(DEV))
+    torch.cuda.synchronize()
+    rows = sample_rows(n, 160)
+    ref = orc.blast_forward(to64(X[rows]), to64(V), to64(S), to64(U))
+    assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"BLAST S2+S3 {n, b1, b2, r, p, q}")
+
+
+def test_blast_s2_s3_fused_asymmetric_S(cuda_lib, monkeypatch):
+    """An S with distinct (l, k) blocks: a swapped index in the on-chip block sum cannot pass."""
+    monkeypatch.setenv("BLR_FUSED", "1")
+    n, b1, b2, r, p, q = 300, 6, 4, 128, 64, 96
+    X = synth.make_x(n, b1 * p, seed=26)
+    V, S, U = synth.blast_factors(b1 * p, b2 * q, b1, b2, r, seed=26)
+    S = (S.float() * torch.arange(1, b1 * b2 + 1, dtype=torch.float32).view(b1, b2, 1) / (b1 * b2)).to(torch.bfloat16)
+    Y = cuda_lib.blast_matmul(X.to(DEV), V.to(DEV), S.to(DEV), U.to(DEV))
+    torch.cuda.synchronize()
+    ref = orc.blast_forward(to64(X), to64(V), to64(S), to64(U))
+    assert_parity(Y, ref, "BLAST S2+S3 asymmetric S")
