@@ -537,12 +537,19 @@ blr_status fused_launch(const DevInfo& d, int dev, cudaStream_t st, blr::FParams
     p.items = static_cast<int>(base * p.n_parts);
     p.c_box_w = chunk_width(p.bn2);
     p.c_swz = pick_swz(p.c_box_w * 2).mask;
-    p.stage_warp_bytes = static_cast<uint32_t>(32 * p.c_box_w * 2);
     if (p.mon != 2) p.s1_bytes = static_cast<uint32_t>(blr::BM * blr::BK * 2) + p.b1_bytes;
     p.slot_bytes = static_cast<uint32_t>(rup(std::max<int64_t>(p.s1_bytes, p.b2_bytes), 1024));
-    for (p.stages = blr::MAX_STAGES; p.stages >= 2; --p.stages)
-        if (blr::fused_layout(p).total + SMEM_SLACK <= static_cast<uint32_t>(SMEM_LIMIT)) break;
-    if (p.stages < 2) return BLR_ERR_UNSUPPORTED;
+    // two staging buffers per epilogue warp (Y stores overlap the next chunk's staging) when the
+    // ring still gets >= 3 slots, else one (BLR_FUSED_BUFS=1/2 forces)
+    const char* fb_env = getenv("BLR_FUSED_BUFS");
+    for (p.stage_bufs = 2; p.stage_bufs >= 1; --p.stage_bufs) {
+        if (fb_env && atoi(fb_env) != p.stage_bufs) continue;
+        p.stage_warp_bytes = static_cast<uint32_t>(p.stage_bufs * 32 * p.c_box_w * 2);
+        for (p.stages = blr::MAX_STAGES; p.stages >= 2; --p.stages)
+            if (blr::fused_layout(p).total + SMEM_SLACK <= static_cast<uint32_t>(SMEM_LIMIT)) break;
+        if (p.stages >= (p.stage_bufs == 2 && !fb_env ? 3 : 2)) break;
+    }
+    if (p.stages < 2 || p.stage_bufs < 1) return BLR_ERR_UNSUPPORTED;
     CUtensorMap tc;
     {
         const uint64_t dims[4] = {static_cast<uint64_t>(p.n2), 1, static_cast<uint64_t>(p.g2), static_cast<uint64_t>(p.n_tok)};
@@ -565,8 +572,9 @@ blr_status fused_launch(const DevInfo& d, int dev, cudaStream_t st, blr::FParams
     if (const char* pe = getenv("BLR_PLAN"); pe && pe[0] == '1')
         fprintf(stderr,
                 "[blr plan] fused mon=%d grid=%d items=%dx%dx%d g1=%d k1b=%d n1=%d k2=%d n2=%d bn2=%d stages=%d "
-                "smem=%d\n",
-                p.mon, grid, p.tiles_m, p.g2, p.n_parts, p.g1, p.k1_blocks, p.n1, p.k2, p.n2, p.bn2, p.stages, smem);
+                "bufs=%d smem=%d\n",
+                p.mon, grid, p.tiles_m, p.g2, p.n_parts, p.g1, p.k1_blocks, p.n1, p.k2, p.n2, p.bn2, p.stages,
+                p.stage_bufs, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(grid));
     cfg.blockDim = dim3(blr::NUM_THREADS);

@@ -52,7 +52,8 @@ struct FParams {
     uint32_t slot_bytes;
     int stages;
     int c_box_w;
-    uint32_t c_swz, stage_warp_bytes;
+    uint32_t c_swz, stage_warp_bytes;  // stage_warp_bytes = stage_bufs x (32 rows x c_box_w bf16)
+    int stage_bufs;
 };
 
 struct FLayout {
@@ -270,6 +271,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // mode 2: ring steps issued before this item's first Z-load step (the epilogue consumes the
         // Z-load steps; the S3 steps in between belong to the MMA warp)
         long long gstep = 0;
+        uint32_t nstore = 0;  // staged Y chunks (staging buffer rotation)
         ptx::griddep_wait();  // our Y stores must not overtake the previous kernel's reads
         for (int it = 0; it < nitems; ++it) {
             int T, kq, c_lo, c_hi;
@@ -381,16 +383,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (j * 8 < CW) ptx::tmem_ld_x8(tmem_base + lane_addr + b * 256 + c0 + j * 8,
                                                         *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
                     ptx::tmem_wait_ld();
-                    if (lane == 0) ptx::bulk_wait_read<0>();  // staging buffer free
+                    const uint32_t buf = stg + (nstore % p.stage_bufs) * (32u * row_bytes);
+                    ++nstore;
+                    if (lane == 0) {  // the store that last read this staging buffer is done reading it
+                        if (p.stage_bufs == 2) ptx::bulk_wait_read<1>();
+                        else ptx::bulk_wait_read<0>();
+                    }
                     __syncwarp();
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
                         if (j * 8 < CW)
-                            stage_row8(stg, lane, j, row_bytes, p.c_swz, *reinterpret_cast<const float(*)[8]>(&fv[j * 8]), 0);
+                            stage_row8(buf, lane, j, row_bytes, p.c_swz, *reinterpret_cast<const float(*)[8]>(&fv[j * 8]), 0);
                     ptx::fence_async_smem();
                     __syncwarp();
                     if (lane == 0) {
-                        ptx::tma_store_4d(&tmC, stg, n0 + c0, 0, kq, row0);  // Y (c, 0, k, t), rows >= n clipped
+                        ptx::tma_store_4d(&tmC, buf, n0 + c0, 0, kq, row0);  // Y (c, 0, k, t), rows >= n clipped
                         ptx::bulk_commit();
                     }
                 }
