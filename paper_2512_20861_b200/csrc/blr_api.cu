@@ -1210,8 +1210,13 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             const char* oe = getenv("BLR_S2_ORDER");
             const int s2_order = oe ? atoi(oe) : 0;
             const int64_t items = cdiv(n_tok, 128) * (r / 8);
+            // b2 <= 8: the half-register instantiation, two CTAs per SM when both fit in smem
+            const char* se = getenv("BLR_S2_SMALL");
+            const bool small = b2 <= 8 && !(se && se[0] == '0');
+            const int per_sm = (small && 2 * (sl.total + 1024 + 1024) <= 233472) ? 2 : 1;
+            auto s2fn = small ? blr::blast_s2_mma_kernel<8> : blr::blast_s2_mma_kernel<16>;
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(items, d.sm_count)));
+            cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(items, static_cast<int64_t>(per_sm) * d.sm_count)));
             cfg.blockDim = dim3(blr::S2M_THREADS);
             cfg.dynamicSmemBytes = sl.total + 1024;
             cfg.stream = st;
@@ -1223,7 +1228,9 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             {
                 std::lock_guard<std::mutex> lk(g_mu);
                 if (!g_attr_set[8][dev]) {
-                    if (cudaFuncSetAttribute(blr::blast_s2_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    if (cudaFuncSetAttribute(blr::blast_s2_mma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             232448) != cudaSuccess ||
+                        cudaFuncSetAttribute(blr::blast_s2_mma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              232448) != cudaSuccess)
                         return BLR_ERR_CUDA;
                     g_attr_set[8][dev] = true;
@@ -1231,7 +1238,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             }
             const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
             if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
-            if (cudaLaunchKernelEx(&cfg, blr::blast_s2_mma_kernel, static_cast<const __half*>(zl),
+            if (cudaLaunchKernelEx(&cfg, s2fn, static_cast<const __half*>(zl),
                                    static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
                                    static_cast<int>(n_tok), static_cast<int>(b1), static_cast<int>(b2),
                                    static_cast<int>(r), s2_order) != cudaSuccess)

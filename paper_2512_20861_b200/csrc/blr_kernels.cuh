@@ -969,7 +969,10 @@ __host__ __device__ inline S2MLayout s2m_layout(int b1, int b2) {
     return L;
 }
 
-__global__ void __launch_bounds__(S2M_THREADS, 1)
+// MAXB2: largest b2 of the instantiation (8: few output blocks -> half the epilogue registers and
+// two CTAs per SM, which is what the short, latency-bound S2 of small layers needs; 16: b = 16)
+template <int MAXB2>
+__global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
     blast_s2_mma_kernel(const __half* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
                         const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order) {
     extern __shared__ __align__(1024) uint8_t s2m_smem[];
@@ -1104,10 +1107,10 @@ __global__ void __launch_bounds__(S2M_THREADS, 1)
             const int acc = j & 1, cb = j & 1;
             ptx::mbar_wait(d_full + 8 * acc, (j >> 1) & 1);
             ptx::tc_fence_after();
-            uint32_t v[128];
+            uint32_t v[8 * MAXB2];
             const uint32_t taddr = tmem + (static_cast<uint32_t>(q * 32) << 16) + acc * 128;
 #pragma unroll
-            for (int g = 0; g < 4; ++g)
+            for (int g = 0; g < MAXB2 / 4; ++g)
                 if (g * 4 < b2) ptx::tmem_ld_x32(taddr + g * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[g * 32]));
             ptx::tmem_wait_ld();
             ptx::tc_fence_before();
@@ -1118,7 +1121,7 @@ __global__ void __launch_bounds__(S2M_THREADS, 1)
             ptx::named_bar_sync(1, 128);
             const uint32_t c0 = base + L.c + cb * L.c_bytes + row * 16;
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
+            for (int k = 0; k < MAXB2; ++k) {
                 if (k < b2) {
                     uint4 o;
                     o.x = ptx::pack_bf16x2(__uint_as_float(v[8 * k + 0]), __uint_as_float(v[8 * k + 1]));
