@@ -1215,6 +1215,8 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             const bool small = b2 <= 8 && !(se && se[0] == '0');
             const int per_sm = (small && 2 * (sl.total + 1024 + 1024) <= 233472) ? 2 : 1;
             auto s2fn = small ? blr::blast_s2_mma_kernel<8> : blr::blast_s2_mma_kernel<16>;
+            const char* pe2 = getenv("BLR_S2_PDL");
+            const bool s2_pdl = pdl_enabled() && !(pe2 && pe2[0] == '0');
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(items, static_cast<int64_t>(per_sm) * d.sm_count)));
             cfg.blockDim = dim3(blr::S2M_THREADS);
@@ -1222,7 +1224,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             cfg.stream = st;
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[0].val.programmaticStreamSerializationAllowed = 0;
+            attr[0].val.programmaticStreamSerializationAllowed = s2_pdl ? 1 : 0;
             cfg.attrs = attr;
             cfg.numAttrs = 1;
             {

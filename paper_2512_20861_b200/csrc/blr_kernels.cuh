@@ -1028,6 +1028,7 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(s2m_smem + L.tslot);
+    ptx::griddep_launch_dependents();  // the S3 launch may start its prologue as SMs free up
 
     if (warp == 0) {  // ---------------------------------------------------------- TMA producer
         ptx::griddep_wait();  // Z is the previous kernel's output
