@@ -388,10 +388,7 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     KParams p;
     int pair = 1;
     const char* pe = getenv("BLR_PAIR");
-    // bulk-copied (tile-blocked) A completes on the issuing CTA's barrier: single-CTA MMAs only
-    // (a pair variant that relayed the peer's A arrival to the leader measured no faster on the
-    //  Llama-7B S3 expands: 2.58 / 1.24 ms vs 2.54 / 0.91 ms)
-    const int force = a_blocked ? 1 : (pe ? atoi(pe) : 0);
+    const int force = pe ? atoi(pe) : 0;
     if (force == 2 && n_tok >= 256) {
         pair = 2;
     } else if (force != 1) {
@@ -400,6 +397,10 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
         // tile's B (K x BN) is about twice its A (BM x K), i.e. full-width BN = 256 tiles
         // (measured: GPT2-S BLAST c_proj S1 with BN = 192 is faster unpaired)
         if (!p.b_resident && n_tok >= 1024 && p.BN >= 2 * blr::BM) pair = 2;
+        // split BLAST S3 (tile-blocked Z'' as A, long K, streamed U): a pair halves each CTA's U
+        // bytes per stage, so the ring holds more K blocks in flight (BLR_S3_PAIR=0 disables)
+        const char* s3p = getenv("BLR_S3_PAIR");
+        if (a_blocked && !(s3p && s3p[0] == '0') && !p.b_resident && n_tok >= 1024 && p.BN >= 192 && K >= 512) pair = 2;
     }
     if (!plan_gemm(p, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp)) {
         if (pair == 1 || !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp))
@@ -412,9 +413,18 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     p.a_nchunks = static_cast<int>(K / 8);
 
     CUtensorMap ta, tb, tc;
-    // (a tile-blocked A / output moves by 1-D bulk copies in the kernel; the maps below are then
-    // encoded over the same buffer but unused)
-    {
+    if (a_blocked) {
+        // tile-blocked A [g][T][K/8][128][8] viewed as rows of 64 elements (128 B): a K block of a
+        // 128-row tile is 128 consecutive rows, one unswizzled tensor box (it lands in smem byte
+        // for byte as the no-swizzle K-major core-matrix layout); a tensor copy (unlike a 1-D bulk
+        // copy) can complete on the leader's barrier of a CTA pair
+        p.a_tiles = static_cast<int>(cdiv(n_tok, blr::BM));
+        const uint64_t rows = static_cast<uint64_t>(groups) * p.a_tiles * (K / 8) * 16;
+        const uint64_t dims[3] = {64, rows, 1};
+        const uint64_t str[2] = {128, rows * 128};
+        const uint32_t box[3] = {64, static_cast<uint32_t>(blr::BM), 1};
+        if (!encode(&ta, A, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return BLR_ERR_CUDA;
+    } else {
         const int64_t Ka = K * comp;  // A row length actually stored
         uint64_t dims[3], str[2];
         dims[0] = static_cast<uint64_t>(Ka);

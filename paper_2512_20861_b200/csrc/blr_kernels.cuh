@@ -55,6 +55,7 @@ struct KParams {
                       //    tile is 8 adjacent 2-KB panels, one bulk copy into 8 no-swizzle K core-matrix columns
     const __nv_bfloat16* a_ptr;  // a_blocked: A base
     int a_nchunks;               // a_blocked: K / 8
+    int a_tiles;                 // a_blocked: 128-row tiles per group in the layout
     int kbox;         // 64-wide K blocks per pipeline stage (1 or 2; 2 halves the handshakes)
     int n_sub;        // sub-GEMMs accumulated into separate TMEM slots (BLAST proj: b1)
     int stages;       // smem ring depth
@@ -398,19 +399,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 const int k0 = (kb - part * p.kb_half) * BK;  // padded block: k0 >= K, zero-filled
                                 if constexpr (KIND == KIND_GEMM) {
                                     if (p.a_blocked) {
-                                        // tile-blocked A [g][T][K/8][128][8]: the k-block's 8 panels
-                                        // of tile T are one contiguous 16 KB (panels past K -- also
-                                        // whole padded k-blocks of a kbox pair -- repeat the last
-                                        // panel: finite values against B's zero-filled rows)
-                                        const int nch = a_nch, c0b = k0 >> 3, nv = max(0, min(8, nch - c0b));
-                                        const __nv_bfloat16* tile_a =
-                                            p.a_ptr + (static_cast<long long>(tc.g) * p.tiles_m + tc.m_blk) * nch * (BM * 8);
-                                        if (nv > 0)
-                                            ptx::bulk_load(a_dst, tile_a + static_cast<long long>(c0b) * (BM * 8),
-                                                           static_cast<uint32_t>(nv) * 2048u, fb);
-                                        for (int ch = nv; ch < 8; ++ch)
-                                            ptx::bulk_load(a_dst + ch * 2048u, tile_a + static_cast<long long>(nch - 1) * (BM * 8),
-                                                           2048u, fb);
+                                        // tile-blocked A [g][T][K/8][128][8]: the K block's 8 panels of
+                                        // this CTA's 128-row tile are 128 consecutive 128-B rows of
+                                        // the map (panels past K read the following panels or TMA's
+                                        // zero fill: finite values against B's zero-filled rows)
+                                        const int t128 = tc.m_blk * PAIR + static_cast<int>(crank);
+                                        const int row = ((tc.g * p.a_tiles + t128) * a_nch + (k0 >> 3)) * 16;
+                                        load3(a_dst, &tmA, fb, 0, row, 0);
                                     } else if (p.a_gmid)
                                         load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, tc.g, m0);
                                     else
