@@ -463,6 +463,16 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
         const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32};
         if (!encode(&tc, out.ptr, 4, dims, strb, box, cs.mode, out.f32)) return BLR_ERR_CUDA;
     }
+    if (out.blocked) {
+        // tile-blocked fp16 output [g][T][N/8][128][8] viewed (64 elem, 16 rows, N/8 panels, g*T):
+        // a chunk's panels of one tile are one tensor store box (64, 16, CW/8, 1); panels past N
+        // fall outside dim 2 and are clipped (a 1-D bulk copy per chunk measured slower)
+        p.o_tiles = static_cast<int>(cdiv(n_tok, blr::BM));
+        const uint64_t dims[4] = {64, 16, static_cast<uint64_t>(N / 8), static_cast<uint64_t>(groups) * p.o_tiles};
+        const uint64_t strb[3] = {128, 2048, static_cast<uint64_t>(N / 8) * 2048};
+        const uint32_t box[4] = {64, 16, static_cast<uint32_t>(p.c_box_w / 8), 1};
+        if (!encode(&tc, out.ptr, 4, dims, strb, box, CU_TENSOR_MAP_SWIZZLE_NONE, out.f32)) return BLR_ERR_CUDA;
+    }
     // fp16 output (BLAST split-path Z) is a separate instantiation: the bf16 epilogue stays as is
     if (out.f32 == 2 && out.blocked)
         return pair == 2 ? launch<blr::KIND_GEMM, 2, 2>(ta, tb, tc, p, d, dev, st)
@@ -1250,7 +1260,18 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             }
             const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
             if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
-            if (cudaLaunchKernelEx(&cfg, s2fn, static_cast<const __half*>(zl),
+            CUtensorMap tmz, tmzpp;
+            {   // Z / Z'' tile-blocked [g][T][r/8][128][8] viewed (64 elem, 16 rows, T*r/8 panels, g)
+                const int64_t np = cdiv(n_tok, blr::BM) * (r / 8);
+                const uint64_t dz[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b1)};
+                const uint64_t sz[3] = {128, 2048, static_cast<uint64_t>(np) * 2048};
+                const uint32_t bz[4] = {64, 16, 1, static_cast<uint32_t>(b1)};
+                if (!encode(&tmz, zl, 4, dz, sz, bz, CU_TENSOR_MAP_SWIZZLE_NONE, 2)) return BLR_ERR_CUDA;
+                const uint64_t dp[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b2)};
+                const uint32_t bp[4] = {64, 16, 1, static_cast<uint32_t>(b2)};
+                if (!encode(&tmzpp, zpp, 4, dp, sz, bp, CU_TENSOR_MAP_SWIZZLE_NONE)) return BLR_ERR_CUDA;
+            }
+            if (cudaLaunchKernelEx(&cfg, s2fn, tmz, tmzpp, static_cast<const __half*>(zl),
                                    static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
                                    static_cast<int>(n_tok), static_cast<int>(b1), static_cast<int>(b2),
                                    static_cast<int>(r), s2_order) != cudaSuccess)

@@ -56,6 +56,7 @@ struct KParams {
     const __nv_bfloat16* a_ptr;  // a_blocked: A base
     int a_nchunks;               // a_blocked: K / 8
     int a_tiles;                 // a_blocked: 128-row tiles per group in the layout
+    int o_tiles;                 // OUTF 2: 128-row tiles per group of the tile-blocked output
     int kbox;         // 64-wide K blocks per pipeline stage (1 or 2; 2 halves the handshakes)
     int n_sub;        // sub-GEMMs accumulated into separate TMEM slots (BLAST proj: b1)
     int stages;       // smem ring depth
@@ -690,12 +691,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (iss && !(p.dbg & 1)) {
                             // tile-blocked [g][T][N/8][128][8]: this chunk's panels of tile T are
                             // contiguous -> one bulk copy (rows >= n_tok are zeros: A was OOB-filled)
-                            const int nch = p.N >> 3, cc = (n0 + c0) >> 3, npan = min(CW / 8, nch - cc);
-                            auto* ob = static_cast<uint16_t*>(p.out_ptr) + tc.g * p.out_gstride;
-                            const int T = m0 / BM;
-                            if (npan > 0)
-                                ptx::bulk_store(ob + (static_cast<long long>(T) * nch + cc) * (BM * 8), hbuf,
-                                                static_cast<uint32_t>(npan) * 2048u);
+                            const int cc = (n0 + c0) >> 3;
+                            ptx::tma_store_4d(&tmC, hbuf, 0, 0, cc, tc.g * p.o_tiles + m0 / BM);
                             ptx::bulk_commit();
                         }
                         continue;
@@ -968,7 +965,8 @@ __host__ __device__ inline S2MLayout s2m_layout(int b1, int b2) {
 // two CTAs per SM, which is what the short, latency-bound S2 of small layers needs; 16: b = 16)
 template <int MAXB2>
 __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
-    blast_s2_mma_kernel(const __half* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
+    blast_s2_mma_kernel(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmZpp,
+                        const __half* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
                         const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order) {
     extern __shared__ __align__(1024) uint8_t s2m_smem[];
     const S2MLayout L = s2m_layout(b1, b2);
@@ -1034,10 +1032,9 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
                 const int s = j % S2M_ASTAGES;
                 if (j >= S2M_ASTAGES) ptx::mbar_wait(a_empty + 8 * s, ((j / S2M_ASTAGES) - 1) & 1);
                 ptx::mbar_arrive_expect_tx(a_full + 8 * s, static_cast<uint32_t>(b1 * 2048));
-                for (int l = 0; l < b1; ++l)  // panel (l, T, c): 128 rows x 16 B contiguous
-                    ptx::bulk_load(base + L.a + s * L.a_bytes + l * 2048,
-                                   Z + ((static_cast<long long>(l) * tiles + T) * nchunks + c) * 1024, 2048,
-                                   a_full + 8 * s);
+                // the b1 panels (l, T, c) in ONE tensor copy: Z viewed (64, 16, tiles*r/8, b1),
+                // box (64, 16, 1, b1) -> smem [l][2 KB] (1-D bulk copies per panel measured slower)
+                ptx::tma_load_4d(base + L.a + s * L.a_bytes, &tmZ, a_full + 8 * s, 0, 0, T * nchunks + c, 0);
             }
         }
         __syncwarp();
@@ -1130,9 +1127,8 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
             ptx::fence_async_smem();
             ptx::named_bar_sync(1, 128);
             if (issuer) {
-                for (int k = 0; k < b2; ++k)  // panel (k, T, c)
-                    ptx::bulk_store(Zpp + ((static_cast<long long>(k) * tiles + T) * nchunks + c) * 1024,
-                                    base + L.c + cb * L.c_bytes + k * 2048, 2048);
+                // panels (k, T, c) for all k in ONE tensor store (Z'' viewed like Z)
+                ptx::tma_store_4d(&tmZpp, base + L.c + cb * L.c_bytes, 0, 0, T * nchunks + c, 0);
                 ptx::bulk_commit();
             }
         }
