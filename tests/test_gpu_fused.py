@@ -123,3 +123,23 @@ def test_blast_s2_s3_fused_asymmetric_S(cuda_lib, monkeypatch):
     torch.cuda.synchronize()
     ref = orc.blast_forward(to64(X), to64(V), to64(S), to64(U))
     assert_parity(Y, ref, "BLAST S2+S3 asymmetric S")
+
+
+@pytest.mark.parametrize("n", [17, 127, 128, 129])
+def test_single_partial_tile_token_counts(cuda_lib, monkeypatch, n):
+    """Token counts inside or at the edge of one 128-row tile through the tile-blocked BLAST split
+    path (S1 epilogue tensor store, S2 tensor copies, S3 tensor-box A) and the forced fused layer."""
+    monkeypatch.setenv("BLR_DECODE", "0")
+    b1, b2, r, p, q = 16, 16, 128, 32, 48
+    X = synth.make_x(n, b1 * p, seed=27)
+    V, S, U = synth.blast_factors(b1 * p, b2 * q, b1, b2, r, seed=27)
+    Y = cuda_lib.blast_matmul(X.to(DEV), V.to(DEV), S.to(DEV), U.to(DEV))
+    torch.cuda.synchronize()
+    assert_parity(Y, orc.blast_forward(to64(X), to64(V), to64(S), to64(U)), f"BLAST split n={n}")
+    monkeypatch.setenv("BLR_FUSED", "1")
+    i, o, rl = 640, 896, 192
+    Xl = synth.make_x(n, i, seed=28)
+    Vl, Ul = synth.lowrank_factors(i, o, rl, seed=28)
+    Yl = cuda_lib.lowrank_matmul(Xl.to(DEV), Vl.to(DEV), Ul.to(DEV))
+    torch.cuda.synchronize()
+    assert_parity(Yl, orc.lowrank_forward(to64(Xl), to64(Vl), to64(Ul)), f"fused LR n={n}")
