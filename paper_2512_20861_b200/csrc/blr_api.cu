@@ -401,6 +401,10 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
         // bytes per stage, so the ring holds more K blocks in flight (BLR_S3_PAIR=0 disables)
         const char* s3p = getenv("BLR_S3_PAIR");
         if (a_blocked && !(s3p && s3p[0] == '0') && !p.b_resident && n_tok >= 1024 && p.BN >= 192 && K >= 512) pair = 2;
+        // any long-K streamed GEMM (e.g. Monarch S3, K = b1 r' = 1536): same ingress argument
+        // (Llama-7B Monarch gate S3 2.08 -> 2.02 ms; BLR_LONGK_PAIR=0 disables)
+        const char* lkp = getenv("BLR_LONGK_PAIR");
+        if (!(lkp && lkp[0] == '0') && !p.b_resident && n_tok >= 1024 && p.BN >= 192 && K >= 1024) pair = 2;
     }
     if (!plan_gemm(p, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp)) {
         if (pair == 1 || !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp))
