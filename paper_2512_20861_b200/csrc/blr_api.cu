@@ -1050,9 +1050,10 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         int pair = 1;
         const char* pe = getenv("BLR_PAIR");
         const int force = pe ? atoi(pe) : 0;
-        // measured (Llama-7B, GPT2-S): the Monarch S1 runs best as one CTA per tile; pairs only
-        // when forced (BLR_PAIR=2)
+        // measured (Llama-7B): pairs win for a long block contraction (down S1, p = 688: 3.05 ->
+        // 2.57 ms) and lose for a short one (gate S1, p = 256: 1.33 -> 1.89 ms); BLR_PAIR forces
         if (force == 2 && n_tok >= 256) pair = 2;
+        if (force == 0 && n_tok >= 1024 && pdim >= 512) pair = 2;
         if (!plan_mon(p, pair)) {
             if (pair == 1 || !plan_mon(p, pair = 1)) return BLR_ERR_UNSUPPORTED;
         }
