@@ -623,7 +623,8 @@ def dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev, use_graph=Tr
 
 def e2e_run(w, chains, facs, xs, flush, stream, K, dev):
     """Same step through the public API with pinned HOST buffers: H2D of each chain's X and
-    D2H of each chain's final Y are inside the timed region every step."""
+    D2H of each chain's final Y are inside the timed region every step (copy streams overlap
+    them with the kernels of the other chains)."""
     xh = {ci: xs[ci].cpu().pin_memory() for ci in xs}
     last = {ci: chain[-1][1] for ci, chain in enumerate(chains)}
     yh = {ci: torch.empty((w.n, last[ci].o), dtype=torch.bfloat16).pin_memory() for ci in xs}
@@ -631,14 +632,34 @@ def e2e_run(w, chains, facs, xs, flush, stream, K, dev):
     h2d = sum(t.numel() * 2 for t in xh.values())
     d2h = sum(t.numel() * 2 for t in yh.values())
 
+    # copies on their own streams so PCIe traffic overlaps the kernels (full duplex): chain c's X
+    # lands while chain c-1 computes, chain c's Y drains while chain c+1 computes; the step's end
+    # event waits for the last D2H, so every step still carries all of its own copies
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev_start = torch.cuda.Event()
+    ev_in = {ci: torch.cuda.Event() for ci in xs}
+    ev_done = {ci: torch.cuda.Event() for ci in xs}
+    ev_out = torch.cuda.Event()
+
     def one():
-        for ci in xd:
-            xd[ci].copy_(xh[ci], non_blocking=True)
+        ev_start.record(stream)
+        with torch.cuda.stream(s_in):
+            s_in.wait_event(ev_start)
+            for ci in xd:
+                xd[ci].copy_(xh[ci], non_blocking=True)
+                ev_in[ci].record(s_in)
         for ci, chain in enumerate(chains):
+            stream.wait_event(ev_in[ci])
             h = xd[ci]
             for j, L in chain:
                 h = step_call(L, j, h)
-            yh[ci].copy_(h, non_blocking=True)
+            ev_done[ci].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_done[ci])
+                h.record_stream(s_out)  # the allocator must not recycle h before the D2H read it
+                yh[ci].copy_(h, non_blocking=True)
+        ev_out.record(s_out)
+        stream.wait_event(ev_out)
 
     import paper_2512_20861_b200 as blr
 
