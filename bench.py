@@ -1,24 +1,29 @@
 #!/usr/bin/env python
 """bench.py -- BLR prefill forward on B200: tokens/s, speedup vs cuBLAS dense bf16, roofline.
 
-Default workload = BASELINE.json configs[1] (C2): the GPT2-S MLP (c_fc 768->3072, then
-c_proj 3072->768) over batch 8 x seq 1024 = 8192 tokens, run in each BLR format of PAPER.md
-Table 3 (low-rank r=192; Monarch r=192 b=4; BLAST r=192 b=6).  One *step* = one pass of the
-whole hot path over the batch: the three MLPs back to back (6 BLR layer calls, 12 kernels).
-value = tokens/s counting one token through one BLR MLP as one token (3 * 8192 per step).
+Default workload = BASELINE.json configs[3] (C4), the Llama-7B MLP that north_star's target
+names: gate/up 4096 -> 11008 then down 11008 -> 4096, BLAST (r = 1488, b = 16, Table 3
+L335-342), over batch 8 x seq 8192 = 65,536 tokens.  One *step* = one pass of the whole hot path
+(S1, S2, S3 of both layers) over the batch; value = tokens/s through the BLR MLP.  The same line
+carries `variants`: the Monarch MLP of Table 3 (C4M, r' = 96) and the >= 2x-compression ranks
+(C4X: BLAST r = 1456, Monarch r' = 88), each timed the same way next to cuBLAS.
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2|C1|C3|C4|C4M]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C4|C4M|C4X|C2|...]
 
-Multi-GPU (torchrun, one process per GPU): every rank runs the full batch on its own GPU
-(token-sharded weak scaling, factors replicated, no collective on the data path); the step
-time is the max over ranks; value = tokens of all ranks / that time.
+Multi-GPU (one process per GPU; `--gpus N` re-launches itself through torch.distributed.run
+when it is not already under torchrun): the workload's tokens are sharded contiguously across
+the ranks (strong scaling: 65,536 tokens in total, 8,192 per GPU at N = 8), factors replicated,
+no collective on the data path; the step time is the max over ranks and
+value = all tokens / that time.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -39,6 +44,22 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(nproc: int) -> int:
+    """`--gpus N` outside torchrun: start N ranks of this script (one per GPU) and exit with
+    their status.  Rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def factors_for(L, layer_id, device):
@@ -68,13 +89,14 @@ def build_chains(w):
 
 
 class Sampler:
-    """nvml clock / throttle-reason sampler running during the timed region."""
+    """nvml clock / throttle-reason sampler running during a timed region."""
 
     REASONS = {
         0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
         0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
         0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
     }
+    BAD = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
 
     def __init__(self, index: int):
         self.ok = False
@@ -122,25 +144,38 @@ class Sampler:
         return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": self.max_mhz, "reasons": reasons,
                 "samples": len(mhz)}
 
+    def bad(self):
+        return bool(self.BAD & set(self.summary().get("reasons", [])))
+
+
+def _any_rank(flag: bool, ws: int, dev) -> bool:
+    t = torch.tensor([1.0 if flag else 0.0], device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return bool(t.item() > 0)
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
 
 # ------------------------------------------------------------------------------- reference ----
-def run_reference(args, w):
-    """--impl reference: the fp64 oracle as it stands, on this host's cores, on a bounded sample
-    of the same workload (each step = `rows` token rows through every layer of the workload)."""
-    ws, rank, _ = dist_env()
-    if rank != 0:
-        return 0
+def oracle_step_fn(w, rows, seed=0):
+    """One step of the workload through the fp64 oracle on `rows` token rows."""
     import numpy as np
 
     from oracle import oracle as orc
-    rows = args.ref_rows
     chains = build_chains(w)
     facs = {j: [t.float().numpy().astype(np.float64) for t in factors_for(L, j, "cpu")] for j, L in enumerate(w.layers)}
-    X = synth.make_x(rows, w.layers[0].i, seed=0).float().numpy().astype(np.float64)
+    xs = {ci: synth.make_x(rows, chain[0][1].i, seed=seed, layer_id=ci).double().numpy()
+          for ci, chain in enumerate(chains)}
 
     def step():
-        for chain in chains:
-            h = X if chain[0][1].i == X.shape[1] else synth.make_x(rows, chain[0][1].i, seed=1).double().numpy()
+        for ci, chain in enumerate(chains):
+            h = xs[ci]
             for j, L in chain:
                 f = facs[j]
                 if L.method == "lowrank":
@@ -149,19 +184,34 @@ def run_reference(args, w):
                     h = orc.monarch_forward(h, *f, L.b1, L.b2)
                 else:
                     h = orc.blast_forward(h, *f)
+        return h
 
+    return step, len(chains)
+
+
+def run_reference(args, w):
+    """--impl reference: the fp64 oracle as it stands, on this host's cores, on a bounded sample
+    of the same workload (each step = `rows` token rows through every layer of the workload).
+    Under torchrun only rank 0 runs; the other ranks exit without work."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+    orc.set_num_threads(host_cores())  # torchrun sets OMP_NUM_THREADS=1 for every rank
+    rows = args.ref_rows
+    step, nchains = oracle_step_fn(w, rows)
     for _ in range(args.warmup):
         step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         step()
     dt = (time.perf_counter() - t0) / args.steps
-    value = rows * len(chains) / dt
+    value = rows * nchains / dt
     cores = orc.num_threads()
     sample = f"{rows} token rows of {w.key} through all {len(w.layers)} layers per step (fp64 oracle)"
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{w.key}: {w.desc}", "rows_per_step": rows},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -171,36 +221,25 @@ def run_reference(args, w):
 
 def cpu_baseline(w, target_s=10.0):
     """Time the oracle (as it stands) on a bounded token sample of the same workload."""
-    import numpy as np
-
     from oracle import oracle as orc
-    chains = build_chains(w)
-    facs = {j: [t.float().numpy().astype(np.float64) for t in factors_for(L, j, "cpu")] for j, L in enumerate(w.layers)}
+    orc.set_num_threads(host_cores())
 
     def run(rows):
+        step, nch = oracle_step_fn(w, rows)
         t0 = time.perf_counter()
-        for chain in chains:
-            h = synth.make_x(rows, chain[0][1].i, seed=0).double().numpy()
-            for j, L in chain:
-                f = facs[j]
-                if L.method == "lowrank":
-                    h = orc.lowrank_forward(h, *f)
-                elif L.method == "monarch":
-                    h = orc.monarch_forward(h, *f, L.b1, L.b2)
-                else:
-                    h = orc.blast_forward(h, *f)
-        return time.perf_counter() - t0
+        step()
+        return time.perf_counter() - t0, nch
 
     rows = 16
-    dt = run(rows)
+    dt, nch = run(rows)
     rows = int(max(16, min(w.n, rows * target_s / max(dt, 1e-3))))
-    dt = run(rows)
+    dt, nch = run(rows)
     # single-thread figure on a smaller sample (SURVEY §8(d): report the 1-thread run too)
     cores = orc.num_threads()
     orc.set_num_threads(1)
     rows1 = max(4, rows // max(1, cores) // 4)
-    dt1 = run(rows1)
-    orc.set_num_threads(0)
+    dt1, _ = run(rows1)
+    orc.set_num_threads(host_cores())
     model = ""
     try:
         for line in open("/proc/cpuinfo"):
@@ -209,228 +248,278 @@ def cpu_baseline(w, target_s=10.0):
                 break
     except OSError:
         pass
-    return {"value": rows * len(chains) / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
+    return {"value": rows * nch / dt, "unit": "tokens/s", "cores": cores, "kind": "oracle",
             "sample": f"{rows} token rows of {w.key} through every layer ({dt:.1f} s fp64 on host)",
-            "single_thread_value": rows1 * len(chains) / dt1, "cpu_model": model}
+            "single_thread_value": rows1 * nch / dt1, "cpu_model": model}
 
 
-# ------------------------------------------------------------------------------- main bench ---
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
-    ap.add_argument("--ref-rows", type=int, default=64)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-dense", action="store_true")
-    ap.add_argument("--eager", action="store_true", help="launch every step from the host (no CUDA graph)")
-    ap.add_argument("--flush", default="write+read", choices=["write+read", "write"],
-                    help="L2 flush between timed steps (see L2Flush)")
-    args = ap.parse_args()
-    w = configs.WORKLOADS[args.config]
-    if args.impl == "reference":
-        return run_reference(args, w)
+# ------------------------------------------------------------------------------- the arm ------
+class Arm:
+    """One workload on this rank's token shard: inputs, outputs, workspaces and the step."""
 
-    import paper_2512_20861_b200 as blr
+    def __init__(self, w, n, dev, seed):
+        import paper_2512_20861_b200 as blr
+        self.blr = blr
+        self.lib = blr.load()
+        self.w, self.n, self.dev = w, n, dev
+        self.chains = build_chains(w)
+        self.facs = {j: [t.to(dev) for t in factors_for(L, j, "cpu")] for j, L in enumerate(w.layers)}
+        self.xs = {ci: synth.make_x(n, chain[0][1].i, seed=seed, layer_id=ci, device=dev)
+                   for ci, chain in enumerate(self.chains)}
+        self.outs, self.wss = {}, {}
+        for j, L in enumerate(w.layers):
+            self.outs[j] = torch.empty((n, L.o), dtype=torch.bfloat16, device=dev)
+            if L.method == "lowrank":
+                nb = self.lib.blr_lowrank_workspace_size(n, L.i, L.o, L.r)
+            elif L.method == "monarch":
+                nb = self.lib.blr_monarch_workspace_size(n, L.i, L.o, L.b1, L.b2, L.r_blk)
+            else:
+                nb = self.lib.blr_blast_workspace_size(n, L.i, L.o, L.b1, L.b2, L.r)
+            self.wss[j] = torch.empty(max(nb, 16), dtype=torch.uint8, device=dev)
 
-    ws, rank, local = dist_env()
-    if ws > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    dev = torch.device("cuda", local if ws > 1 else 0)
-    torch.cuda.set_device(dev)
-    lib = blr.load()
-    stream = torch.cuda.current_stream(dev)
-
-    # ---- inputs (seeded, synthetic; rank offset in the seed so shards differ)
-    chains = build_chains(w)
-    n = w.n
-    facs = {j: [t.to(dev) for t in factors_for(L, j, "cpu")] for j, L in enumerate(w.layers)}
-    xs = {}
-    for ci, chain in enumerate(chains):
-        xs[ci] = synth.make_x(n, chain[0][1].i, seed=rank, layer_id=ci, device=dev)
-
-    def call(L, j, h):
-        f = facs[j]
+    def call(self, L, j, h, out=None, ws=None):
+        f = self.facs[j]
+        blr = self.blr
         if L.method == "lowrank":
-            return blr.lowrank_matmul(h, *f, out=outs[j], workspace=wss[j])
+            return blr.lowrank_matmul(h, *f, out=out, workspace=ws)
         if L.method == "monarch":
-            return blr.monarch_matmul(h, *f, L.b1, L.b2, out=outs[j], workspace=wss[j])
-        return blr.blast_matmul(h, *f, out=outs[j], workspace=wss[j])
+            return blr.monarch_matmul(h, *f, L.b1, L.b2, out=out, workspace=ws)
+        return blr.blast_matmul(h, *f, out=out, workspace=ws)
 
-    outs, wss = {}, {}
-    for j, L in enumerate(w.layers):
-        outs[j] = torch.empty((n, L.o), dtype=torch.bfloat16, device=dev)
-        if L.method == "lowrank":
-            nb = lib.blr_lowrank_workspace_size(n, L.i, L.o, L.r)
-        elif L.method == "monarch":
-            nb = lib.blr_monarch_workspace_size(n, L.i, L.o, L.b1, L.b2, L.r_blk)
-        else:
-            nb = lib.blr_blast_workspace_size(n, L.i, L.o, L.b1, L.b2, L.r)
-        wss[j] = torch.empty(nb, dtype=torch.uint8, device=dev)
-
-    def step(x_by_chain):
-        for ci, chain in enumerate(chains):
-            h = x_by_chain[ci]
+    def step(self):
+        for ci, chain in enumerate(self.chains):
+            h = self.xs[ci]
             for j, L in chain:
-                h = call(L, j, h)
+                h = self.call(L, j, h, self.outs[j], self.wss[j])
         return h
 
-    # ---- launch map: which layer / phase each kernel launch of a step belongs to
-    phases = []  # (layer index, phase name) per launch, in launch order
-    for ci, chain in enumerate(chains):
-        h = xs[ci]
-        for j, L in chain:
-            h = call(L, j, h)
-            nl = lib.blr_last_launch_count()
-            names = (["layer"] if nl == 1 else ["proj", "expand"] if nl == 2 else ["s1", "s2", "expand"] if nl == 3
-                     else [f"k{i}" for i in range(nl)])
-            phases += [(j, nm) for nm in names]
-    torch.cuda.synchronize()
-    n_launch = len(phases)
-    if os.environ.get("BLR_DUMP_PHASES"):
-        json.dump([f"{w.layers[j].model}.{w.layers[j].name}.{w.layers[j].method}.{nm}" for j, nm in phases],
-                  open(os.environ["BLR_DUMP_PHASES"], "w"))
-
-    # ---- per-launch events (C-ABI profiling hook) and L2 flush buffer
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = L2Flush(max(2 * l2, 256 << 20), dev, args.flush)
-    K, W = args.steps, args.warmup
-    gev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_launch)]
-    for e in gev:
-        e.record(stream)  # forces creation of the underlying cudaEvent_t
-    step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-
-    import ctypes
-    # ---- the step as a CUDA graph (host launch overhead removed, as under the paper's
-    #      torch.compile + CUDA-graph protocol); the per-launch events of the
-    #      C-ABI profiling hook are captured as event-record nodes inside the graph.
-    # Two graphs of the same step: `graph` (timed; nothing but the kernels, so programmatic
-    # dependent launch overlaps each kernel's prologue with its predecessor) and `graph_prof`
-    # (per-launch event-record nodes between the kernels, replayed separately after the timed
-    # region for the per-phase breakdown -- the events serialise the launches, so its per-launch
-    # sum is an upper bound of the step).
-    graph = graph_prof = None
-    if not args.eager:
-        for _ in range(2):
-            step(xs)
+    def phases(self):
+        """(layer index, phase name) of every kernel launch of one step, in launch order."""
+        ph = []
+        for ci, chain in enumerate(self.chains):
+            h = self.xs[ci]
+            for j, L in chain:
+                h = self.call(L, j, h, self.outs[j], self.wss[j])
+                nl = self.lib.blr_last_launch_count()
+                names = (["layer"] if nl == 1 else ["proj", "expand"] if nl == 2 else ["s1", "s2", "expand"]
+                         if nl == 3 else [f"k{i}" for i in range(nl)])
+                ph += [(j, nm) for nm in names]
         torch.cuda.synchronize()
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step(xs)
-        graph_prof = torch.cuda.CUDAGraph()
-        arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in gev])
-        with torch.cuda.graph(graph_prof):
-            lib.blr_profile_begin(arr, 2 * n_launch)
-            step(xs)
-            per_replay_prof = lib.blr_profile_end()
-        assert per_replay_prof == n_launch
-        torch.cuda.synchronize()
+        return ph
 
-    def run_step():
-        if graph is not None:
-            graph.replay()
-            return n_launch
-        step(xs)
-        return n_launch
 
-    def run_step_profiled():
-        if graph_prof is not None:
-            graph_prof.replay()
-            return
-        arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in gev])
-        lib.blr_profile_begin(arr, 2 * n_launch)
-        step(xs)
-        lib.blr_profile_end()
-
-    for _ in range(W):
-        flush()
-        run_step()
+def graph_of(fn):
+    for _ in range(2):
+        fn()
     torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    torch.cuda.synchronize()
+    return g
 
-    def timed_region():
-        nl = 0
+
+def timed(run, flush, stream, K, dev, ws):
+    """K steps, L2 flushed between them (outside the events), bracketed by barrier + sync;
+    clocks sampled during the region; re-measured once if any rank saw hw/thermal slowdown."""
+    def region():
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
         smp = Sampler(dev.index)
         if ws > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
         with smp:
             for s in range(K):
-                flush()  # L2 flush between timed steps (outside the step events)
-                step_ev[s][0].record(stream)
-                nl += run_step()
-                step_ev[s][1].record(stream)
+                flush()
+                evs[s][0].record(stream)
+                run()
+                evs[s][1].record(stream)
             torch.cuda.synchronize()
         if ws > 1:
             torch.distributed.barrier()
-        return nl, smp
+        return [a.elapsed_time(b) for a, b in evs], smp
 
-    launches, sampler = timed_region()
-    # a run that saw hardware / thermal slowdown is re-measured once (all ranks decide together)
-    bad = {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"}
-    slow = torch.tensor([1.0 if bad & set(sampler.summary().get("reasons", [])) else 0.0], device=dev)
-    if ws > 1:
-        torch.distributed.all_reduce(slow, op=torch.distributed.ReduceOp.MAX)
-    remeasured = bool(slow.item() > 0)
+    ms, smp = region()
+    remeasured = _any_rank(smp.bad(), ws, dev)
     if remeasured:
-        launches, sampler = timed_region()
+        ms, smp = region()
+    return ms, dict(smp.summary(), remeasured=remeasured)
 
-    # per-launch breakdown (profiled graph, outside the timed region)
-    launch_tot = [0.0] * n_launch
-    kp = max(3, min(K, 20))
-    prof_step_ms = 0.0
-    pe = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-    for s in range(kp):
+
+def stats(ms):
+    srt = sorted(ms)
+    return {"mean": sum(ms) / len(ms), "median": srt[len(srt) // 2], "min": srt[0],
+            "p90": srt[min(len(srt) - 1, int(0.9 * len(srt)))]}
+
+
+def dense_comparator(arm, flush, stream, K, W, dev, ws, use_graph=True):
+    """cuBLAS dense bf16 on the same shapes: X @ W with W reconstructed once (torch.matmul)."""
+    w = arm.w
+    Ws = {j: dense_weight(L, arm.facs[j]) for j, L in enumerate(w.layers)}
+    outs = {j: torch.empty((arm.n, L.o), dtype=torch.bfloat16, device=dev) for j, L in enumerate(w.layers)}
+
+    def step():
+        for ci, chain in enumerate(arm.chains):
+            h = arm.xs[ci]
+            for j, L in chain:
+                h = torch.matmul(h, Ws[j], out=outs[j])
+
+    for _ in range(max(W, 2)):
         flush()
-        pe[0].record(stream)
-        run_step_profiled()
-        pe[1].record(stream)
-        torch.cuda.synchronize()
-        prof_step_ms += pe[0].elapsed_time(pe[1]) / kp
-        for j in range(n_launch):
-            launch_tot[j] += gev[2 * j].elapsed_time(gev[2 * j + 1])
-    launch_tot = [v * K / kp for v in launch_tot]
+        step()
+    torch.cuda.synchronize()
+    run = graph_of(step).replay if use_graph else step
+    ms, clocks = timed(run, flush, stream, K, dev, ws)
+    t = sum(ms) / K
+    if ws > 1:
+        from paper_2512_20861_b200 import dist as bdist
+        t = bdist.max_over_ranks(t, device=dev)
+    del Ws, outs
+    return {"ms_per_step": t, "tokens_per_s": ws * arm.n * len(arm.chains) / (t * 1e-3),
+            "impl": "torch.matmul (cuBLAS/cuBLASLt) bf16" + (", CUDA graph" if use_graph else ", eager"),
+            "clocks": clocks}
 
-    step_ms = [a.elapsed_time(b) for a, b in step_ev]
+
+def e2e_run(arm, flush, stream, K, dev, ws):
+    """The step end to end through the public API with pinned HOST buffers: H2D of the step's X
+    and D2H of its Y are inside the timed region every step.  The tokens are processed in chunks
+    so PCIe (full duplex) overlaps the kernels: chunk c's X lands while chunk c-1 computes and
+    chunk c's Y drains while chunk c+1 computes; the step's end event waits for the last D2H."""
+    blr = arm.blr
+    nch = 8 if arm.n >= 8 * 2048 else 1
+    bounds = [(c * arm.n // nch, (c + 1) * arm.n // nch) for c in range(nch)]
+    xh = {ci: arm.xs[ci].cpu().pin_memory() for ci in arm.xs}
+    last = {ci: chain[-1][1] for ci, chain in enumerate(arm.chains)}
+    yh = {ci: torch.empty((arm.n, last[ci].o), dtype=torch.bfloat16).pin_memory() for ci in arm.xs}
+    xd = {ci: torch.empty_like(arm.xs[ci]) for ci in arm.xs}
+    yd = {ci: torch.empty((arm.n, last[ci].o), dtype=torch.bfloat16, device=dev) for ci in arm.xs}
+    h2d = sum(t.numel() * 2 for t in xh.values())
+    d2h = sum(t.numel() * 2 for t in yh.values())
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev_start, ev_out = torch.cuda.Event(), torch.cuda.Event()
+    ev_in = {(ci, c): torch.cuda.Event() for ci in arm.xs for c in range(nch)}
+    ev_done = {(ci, c): torch.cuda.Event() for ci in arm.xs for c in range(nch)}
+
+    def fwd(L, j, h, out=None):
+        f = arm.facs[j]
+        if L.method == "lowrank":
+            return blr.lowrank_matmul(h, *f, out=out)
+        if L.method == "monarch":
+            return blr.monarch_matmul(h, *f, L.b1, L.b2, out=out)
+        return blr.blast_matmul(h, *f, out=out)
+
+    def one():
+        ev_start.record(stream)
+        with torch.cuda.stream(s_in):
+            s_in.wait_event(ev_start)
+            for ci in xd:
+                for c, (lo, hi) in enumerate(bounds):
+                    xd[ci][lo:hi].copy_(xh[ci][lo:hi], non_blocking=True)
+                    ev_in[(ci, c)].record(s_in)
+        for ci, chain in enumerate(arm.chains):
+            for c, (lo, hi) in enumerate(bounds):
+                stream.wait_event(ev_in[(ci, c)])
+                h = xd[ci][lo:hi]
+                for jj, (j, L) in enumerate(chain):
+                    h = fwd(L, j, h, out=yd[ci][lo:hi] if jj == len(chain) - 1 else None)
+                ev_done[(ci, c)].record(stream)
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_done[(ci, c)])
+                    yh[ci][lo:hi].copy_(yd[ci][lo:hi], non_blocking=True)
+        ev_out.record(s_out)
+        stream.wait_event(ev_out)
+
+    one()
+    torch.cuda.synchronize()
+    ms, _ = timed(one, flush, stream, K, dev, ws)
+    t = sum(ms) / K
+    if ws > 1:
+        from paper_2512_20861_b200 import dist as bdist
+        t = bdist.max_over_ranks(t, device=dev)
+    return {"value": ws * arm.n * len(arm.chains) / (t * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": t, "chunks": nch,
+            "how": "public API (blr.*_matmul) on pinned host X/Y, H2D + kernels + D2H per step, "
+                   f"{nch} token chunks pipelined over copy streams"}
+
+
+def measure(w, n, dev, stream, args, ws, rank, flush, full=True):
+    """Time workload `w` on this rank's n tokens: graph-replayed step (the headline), per-launch
+    breakdown, dominant-kernel roofline, cuBLAS comparator and (full) the e2e run."""
+    arm = Arm(w, n, dev, seed=rank)
+    lib = arm.lib
+    ph = arm.phases()
+    n_launch = len(ph)
+    K, W = args.steps, args.warmup
+    graph = None if args.eager else graph_of(arm.step)
+    run = graph.replay if graph is not None else arm.step
+    for _ in range(W):
+        flush()
+        run()
+    torch.cuda.synchronize()
+    step_ms, clocks = timed(run, flush, stream, K, dev, ws)
     t_ms = sum(step_ms) / K
-    srt = sorted(step_ms)
-    step_stats = {"mean": t_ms, "median": srt[len(srt) // 2], "min": srt[0],
-                  "p90": srt[min(len(srt) - 1, int(0.9 * len(srt)))]}
+    st = stats(step_ms)
     # warm-L2 figure (no flush between steps), reported separately (SURVEY §8(d))
     wev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(min(K, 10))]
     for a, b in wev:
         a.record(stream)
-        run_step()
+        run()
         b.record(stream)
     torch.cuda.synchronize()
-    step_stats["warm_l2_mean"] = sum(a.elapsed_time(b) for a, b in wev) / len(wev)
-    launch_ms = [v / K for v in launch_tot]
+    st["warm_l2_mean"] = sum(a.elapsed_time(b) for a, b in wev) / len(wev)
+
+    # per-launch breakdown: a second graph of the step with the C-ABI hook's event-record nodes
+    # (the events serialise the launches: upper bounds), replayed after the timed region
+    import ctypes
+    gev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_launch)]
+    for e in gev:
+        e.record(stream)
+    arr = (ctypes.c_void_p * (2 * n_launch))(*[e.cuda_event for e in gev])
+
+    def prof_step():
+        lib.blr_profile_begin(arr, 2 * n_launch)
+        arm.step()
+        got = lib.blr_profile_end()
+        assert got == n_launch, (got, n_launch)
+
+    prun = graph_of(prof_step).replay if not args.eager else prof_step
+    kp = max(3, min(K, 10))
+    launch_ms = [0.0] * n_launch
+    prof_step_ms = 0.0
+    pe = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    for _ in range(kp):
+        flush()
+        pe[0].record(stream)
+        prun()
+        pe[1].record(stream)
+        torch.cuda.synchronize()
+        prof_step_ms += pe[0].elapsed_time(pe[1]) / kp
+        for j in range(n_launch):
+            launch_ms[j] += gev[2 * j].elapsed_time(gev[2 * j + 1]) / kp
     if ws > 1:
         from paper_2512_20861_b200 import dist as bdist
         t_ms = bdist.max_over_ranks(t_ms, device=dev)
 
-    tokens_per_step = n * len(chains)
-    value = ws * tokens_per_step / (t_ms * 1e-3)
-
-    # ---- per-layer accounting (sum of that layer's launches; phases named per launch)
     peaks = roofline.load_peaks(ROOT)
     per_layer = []
     for j, L in enumerate(w.layers):
         c = roofline.layer_counts(L, n)
-        mine = [(nm, launch_ms[x]) for x, (jj, nm) in enumerate(phases) if jj == j]
+        mine = [(nm, launch_ms[x]) for x, (jj, nm) in enumerate(ph) if jj == j]
         ms = sum(v for _, v in mine)
         t_roof = roofline.roofline_time_s(c["flops"], c["bytes"], peaks) * 1e3
-        per_layer.append({"layer": f"{L.model}.{L.name}.{L.method}", "ms": ms,
+        per_layer.append({"layer": f"{L.model}.{L.name}.{L.method}(r={L.r},b={L.b})", "ms": ms,
                           "launch_ms": {nm: v for nm, v in mine}, "tflops": c["flops"] / ms * 1e-9,
-                          "gbs_alg": c["bytes"] / ms * 1e-6, "roofline_frac": t_roof / ms})
+                          "gbs_alg": c["bytes"] / ms * 1e-6, "roofline_frac": t_roof / ms,
+                          "roofline_ms": t_roof})
+    # step roofline: all layers' FLOPs / bytes against the peaks
+    fl = sum(roofline.layer_counts(L, n)["flops"] for L in w.layers)
+    by = sum(roofline.layer_counts(L, n)["bytes"] for L in w.layers)
+    step_roof_ms = roofline.roofline_time_s(fl, by, peaks) * 1e3
 
-    # ---- dominant kernel roofline (algorithmic bytes/flops per launch)
+    # dominant kernel (algorithmic bytes / FLOPs per launch, DESIGN.md §5.5)
     jmax = max(range(n_launch), key=lambda x: launch_ms[x])
-    Ld = w.layers[phases[jmax][0]]
-    phase = phases[jmax][1]
+    Ld = w.layers[ph[jmax][0]]
+    phase = ph[jmax][1]
     alg = phase_counts(Ld, n, phase)
     dt_s = launch_ms[jmax] * 1e-3
     bw_t = alg["bytes"] / peaks["hbm_gbs"] / 1e9
@@ -440,38 +529,119 @@ def main():
         achieved, peak, unit = alg["bytes"] / dt_s / 1e9, peaks["hbm_gbs"], "GB/s"
     else:
         achieved, peak, unit = alg["flops"] / dt_s / 1e12, peaks["bf16_tflops"], "TFLOP/s"
-    traffic = profiled_traffic(Ld, phase, w.key)
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
-            "traffic": traffic, "kernel": f"{phase_kind(Ld, phase)} ({Ld.model}.{Ld.name}.{Ld.method} {phase})",
+            "traffic": profiled_traffic(Ld, phase, w.key),
+            "kernel": f"{phase_kind(Ld, phase)} ({Ld.model}.{Ld.name}.{Ld.method} {phase})",
             "algorithmic_bytes": alg["bytes"], "algorithmic_flops": alg["flops"], "launch_ms": launch_ms[jmax],
-            "share_of_step": launch_ms[jmax] / t_ms, "peak_source": peaks.get("source", "measured")}
-    io = phase_io_bytes(Ld, n, phase)
-    roof["kernel_io_bytes"] = io  # incl. the intermediate this design moves
-    roof["kernel_io_gbs"] = io / dt_s / 1e9
+            "share_of_step": launch_ms[jmax] / t_ms, "peak_source": peaks.get("source", "measured"),
+            "peak_note": "burst bf16 / copy HBM from MEASURED_PEAKS.json",
+            "kernel_io_bytes": phase_io_bytes(Ld, n, phase)}
+    roof["kernel_io_gbs"] = roof["kernel_io_bytes"] / dt_s / 1e9
+    if peaks.get("bf16_tflops_sustained") and bound == "tensor":
+        roof["frac_of_sustained"] = achieved / peaks["bf16_tflops_sustained"]
 
-    # ---- cuBLAS dense bf16 comparator on the same shapes (X @ W, W reconstructed once)
-    dense = None
-    if not args.no_dense:
-        dense = dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev, not args.eager)
+    dense = None if args.no_dense else dense_comparator(arm, flush, stream, K, W, dev, ws, not args.eager)
+    e2e = e2e_run(arm, flush, stream, min(K, 10), dev, ws) if full else None
+    tokens = ws * n * len(arm.chains)
+    res = {"t_ms": t_ms, "value": tokens / (t_ms * 1e-3), "stats": st, "clocks": clocks, "per_layer": per_layer,
+           "roofline": roof, "dense": dense, "e2e": e2e, "launches_per_step": n_launch,
+           "prof_step_ms": prof_step_ms, "step_roofline_ms": step_roof_ms, "n_chains": len(arm.chains)}
+    del arm, graph
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
 
-    # ---- end to end through the public API with host buffers (H2D X, D2H Y inside the region)
-    e2e = e2e_run(w, chains, facs, xs, flush, stream, min(K, 20), dev)
 
-    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": K, "warmup": W,
-            "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{w.key}: {w.desc}", "n_tokens_per_gpu": n,
-                       "value_def": f"tokens/s; one step = {len(chains)} BLR MLPs/layer chains x {n} tokens",
+# ------------------------------------------------------------------------------- main bench ---
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--ref-rows", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--variants", default="C4M,C4X", help="comma-separated extra workloads (N = 1 only)")
+    ap.add_argument("--eager", action="store_true", help="launch every step from the host (no CUDA graph)")
+    ap.add_argument("--flush", default="write+read", choices=["write+read", "write"],
+                    help="L2 flush between timed steps (see L2Flush)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="rank/shard plumbing only (gloo, no GPU work): prints n_gpus and the shards")
+    args = ap.parse_args()
+    ws, rank, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
+    w = configs.WORKLOADS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    from paper_2512_20861_b200 import dist as bdist
+    lo, hi = bdist.shard_rows(w.n, rank, ws)
+    if args.dry_run:
+        if ws > 1:
+            torch.distributed.init_process_group("gloo")
+        shards = [bdist.shard_rows(w.n, r, ws) for r in range(ws)]
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unit": "tokens/s", "n_gpus": ws, "dry_run": True,
+                              "scaling": "strong" if ws > 1 else "weak",
+                              "config": {"workload": f"{w.key}: {w.desc}", "n_tokens_total": w.n,
+                                         "shards": shards}}), flush=True)
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    if ws > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if ws > 1 else 0)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    n = hi - lo
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = L2Flush(max(2 * l2, 256 << 20), dev, args.flush)
+
+    r = measure(w, n, dev, stream, args, ws, rank, flush, full=True)
+    variants = []
+    if ws == 1 and not args.no_variants:
+        for key in [k for k in args.variants.split(",") if k and k != w.key]:
+            wv = configs.WORKLOADS[key]
+            v = measure(wv, wv.n, dev, stream, args, ws, rank, flush, full=False)
+            ent = {"workload": f"{wv.key}: {wv.desc}", "value": v["value"], "unit": "tokens/s",
+                   "ms_per_step": v["t_ms"], "clocks": v["clocks"],
+                   "per_layer": [{k2: pl[k2] for k2 in ("layer", "ms", "launch_ms", "tflops", "roofline_frac")}
+                                 for pl in v["per_layer"]],
+                   "roofline": {k2: v["roofline"][k2] for k2 in ("bound", "achieved", "peak", "unit", "frac", "kernel")},
+                   "step_roofline_ms": v["step_roofline_ms"]}
+            if v["dense"] is not None:
+                ent["cublas_dense_bf16_ms"] = v["dense"]["ms_per_step"]
+                ent["speedup_vs_cublas"] = v["dense"]["ms_per_step"] / v["t_ms"]
+            variants.append(ent)
+
+    t_ms = r["t_ms"]
+    line = {"metric": METRIC, "value": r["value"], "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": f"{w.key}: {w.desc}", "n_tokens_total": w.n, "n_tokens_per_gpu": n,
+                       "value_def": f"tokens/s through the BLR MLP; one step = {r['n_chains']} chain(s) x {w.n} tokens"
+                                    + (f", token rows sharded contiguously over {ws} GPUs" if ws > 1 else ""),
                        "layers": [f"{L.model}.{L.name}.{L.method}(r={L.r},b={L.b})" for L in w.layers],
                        "l2": flush.describe(),
                        "launch": "eager" if args.eager else "CUDA graph replay of the step (both arms)",
-                       "parallelism": f"token-sharded dp{ws}, no data-path collective"},
-            "roofline": roof, "per_layer": per_layer, "ms_per_step_stats": step_stats,
-            "ms_per_step_with_launch_events": prof_step_ms, "gpu_launches": launches,
-            "clocks": dict(sampler.summary(), remeasured=remeasured), "e2e": e2e}
-    if dense is not None:
-        line["cublas_dense_bf16"] = dense
-        line["speedup_vs_cublas"] = dense["ms_per_step"] / t_ms
+                       "parallelism": f"token-sharded dp{ws}, factors replicated, no data-path collective"},
+            "roofline": r["roofline"], "step_roofline_ms": r["step_roofline_ms"],
+            "step_roofline_frac": r["step_roofline_ms"] / t_ms,
+            "per_layer": r["per_layer"], "ms_per_step_stats": r["stats"],
+            "ms_per_step_with_launch_events": r["prof_step_ms"],
+            "gpu_launches": r["launches_per_step"] * args.steps, "launches_per_step": r["launches_per_step"],
+            "clocks": r["clocks"], "e2e": r["e2e"]}
+    if r["dense"] is not None:
+        line["cublas_dense_bf16"] = r["dense"]
+        line["speedup_vs_cublas"] = r["dense"]["ms_per_step"] / t_ms
+    if variants:
+        line["variants"] = variants
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w)
     if rank == 0:
@@ -493,7 +663,7 @@ def phase_kind(L, phase):
 
 
 def phase_counts(L, n, phase):
-    """Algorithmic bytes / FLOPs of one phase (DESIGN.md §6): proj reads X and the first-stage
+    """Algorithmic bytes / FLOPs of one phase (DESIGN.md §5.5): proj reads X and the first-stage
     factors (V, and S for BLAST); expand reads U and writes Y.  The intermediate is excluded."""
     B = roofline.BF16
     if phase == "layer":  # fused layer: X, every factor, Y
@@ -539,7 +709,7 @@ def phase_io_bytes(L, n, phase):
 
 def profiled_traffic(L, phase, cfg_key):
     """dram__bytes_read.sum + dram__bytes_write.sum of that launch from the committed
-    `ncu --set full` capture (profiles/ncu_traffic_<config>.json, scripts/profile_round.sh)."""
+    `ncu --set full` capture of the same build (profiles/ncu_traffic_<config>.json)."""
     path = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg_key}.json")
     try:
         d = json.load(open(path))
@@ -586,104 +756,6 @@ class L2Flush:
         if self.mode == "write+read":
             return "flushed between timed steps (write of 2x L2, then read of another 2x L2), outside the step events"
         return "flushed between timed steps (write of 2x L2), outside the step events"
-
-
-def dense_comparator(w, chains, facs, xs, flush, stream, K, W, dev, use_graph=True):
-    Ws = {j: dense_weight(L, facs[j]) for j, L in enumerate(w.layers)}
-    outs = {j: torch.empty((w.n, L.o), dtype=torch.bfloat16, device=dev) for j, L in enumerate(w.layers)}
-
-    def step():
-        for ci, chain in enumerate(chains):
-            h = xs[ci]
-            for j, L in chain:
-                h = torch.matmul(h, Ws[j], out=outs[j])
-
-    for _ in range(max(W, 2)):
-        flush()
-        step()
-    torch.cuda.synchronize()
-    run = step
-    if use_graph:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            step()
-        run = g.replay
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    torch.cuda.synchronize()
-    for s in range(K):
-        flush()
-        evs[s][0].record(stream)
-        run()
-        evs[s][1].record(stream)
-    torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in evs) / K
-    return {"ms_per_step": ms, "tokens_per_s": w.n * len(chains) / (ms * 1e-3),
-            "impl": "torch.matmul (cuBLAS/cuBLASLt) bf16" + (", CUDA graph" if use_graph else ", eager")}
-
-
-def e2e_run(w, chains, facs, xs, flush, stream, K, dev):
-    """Same step through the public API with pinned HOST buffers: H2D of each chain's X and
-    D2H of each chain's final Y are inside the timed region every step (copy streams overlap
-    them with the kernels of the other chains)."""
-    xh = {ci: xs[ci].cpu().pin_memory() for ci in xs}
-    last = {ci: chain[-1][1] for ci, chain in enumerate(chains)}
-    yh = {ci: torch.empty((w.n, last[ci].o), dtype=torch.bfloat16).pin_memory() for ci in xs}
-    xd = {ci: torch.empty_like(xs[ci]) for ci in xs}
-    h2d = sum(t.numel() * 2 for t in xh.values())
-    d2h = sum(t.numel() * 2 for t in yh.values())
-
-    # copies on their own streams so PCIe traffic overlaps the kernels (full duplex): chain c's X
-    # lands while chain c-1 computes, chain c's Y drains while chain c+1 computes; the step's end
-    # event waits for the last D2H, so every step still carries all of its own copies
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    ev_start = torch.cuda.Event()
-    ev_in = {ci: torch.cuda.Event() for ci in xs}
-    ev_done = {ci: torch.cuda.Event() for ci in xs}
-    ev_out = torch.cuda.Event()
-
-    def one():
-        ev_start.record(stream)
-        with torch.cuda.stream(s_in):
-            s_in.wait_event(ev_start)
-            for ci in xd:
-                xd[ci].copy_(xh[ci], non_blocking=True)
-                ev_in[ci].record(s_in)
-        for ci, chain in enumerate(chains):
-            stream.wait_event(ev_in[ci])
-            h = xd[ci]
-            for j, L in chain:
-                h = step_call(L, j, h)
-            ev_done[ci].record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_done[ci])
-                h.record_stream(s_out)  # the allocator must not recycle h before the D2H read it
-                yh[ci].copy_(h, non_blocking=True)
-        ev_out.record(s_out)
-        stream.wait_event(ev_out)
-
-    import paper_2512_20861_b200 as blr
-
-    def step_call(L, j, h):
-        f = facs[j]
-        if L.method == "lowrank":
-            return blr.lowrank_matmul(h, *f)
-        if L.method == "monarch":
-            return blr.monarch_matmul(h, *f, L.b1, L.b2)
-        return blr.blast_matmul(h, *f)
-
-    one()
-    torch.cuda.synchronize()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    for s in range(K):
-        flush()
-        evs[s][0].record(stream)
-        one()
-        evs[s][1].record(stream)
-    torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in evs) / K
-    return {"value": w.n * len(chains) / (ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
-
 
 
 if __name__ == "__main__":

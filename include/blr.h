@@ -13,26 +13,39 @@
  * ---------------------------------------
  *  - Every tensor argument is a CUDA DEVICE pointer to a dense, row-major, contiguous array of
  *    bf16 values (the 16-bit pattern of __nv_bfloat16), base address 16-byte aligned.
- *    Arithmetic: bf16 operands, fp32 accumulation; the rank-r intermediate is rounded once to
- *    bf16 (round-to-nearest-even) and Y is rounded RNE to bf16 (reading R11).
+ *    Arithmetic: bf16 operands, fp32 accumulation, Y rounded RNE to bf16.  Intermediates
+ *    (readings R11-R13):
+ *      low rank, Monarch   Z (Z') rounded once to bf16 RNE; when the second-stage contraction
+ *                          is shorter than 128 it is kept as a compensated bf16 pair hi|lo (R12)
+ *      BLAST, b1*r <= 512  Z'' = sum_l S (.) Z_l formed in fp32 on chip, rounded once to bf16
+ *      BLAST, b1*r >  512  Z_l = X_l V_l stored as IEEE fp16 (RNE, SATURATING: a value beyond
+ *                          +-65504 is clamped, so results are within tolerance only while every
+ *                          |(X_l V_l)[t, rho]| <= 65504; NaN stays NaN), then Z'' rounded to bf16
+ *  - Row independence: Y[t, :] depends only on X[t, :] and the factors, bit for bit, whatever
+ *    the other rows hold (NaN and Inf included).
  *  - Y must not alias X, a factor or the workspace.
- *  - Calls are asynchronous on `stream` (0 = legacy default stream).  The library never
- *    synchronizes, never allocates or frees caller memory and keeps no pointer after return.
- *    The caller owns all memory; `workspace` must stay valid until the work on `stream` ends.
- *  - `workspace` holds the bf16 intermediate between the two tcgen05 phases; query its size
- *    with the matching *_workspace_size() function.  ws_bytes smaller than that returns
- *    BLR_ERR_WORKSPACE.
- *  - Validation happens on the host before any launch; on error nothing is enqueued.
+ *  - Calls are asynchronous on `stream` (0 = legacy default stream) and stream-ordered: every
+ *    kernel of a call starts reading X or a factor only after all work enqueued on `stream`
+ *    before the call has completed.  The library never synchronizes, never allocates or frees
+ *    caller memory and keeps no pointer after return.  The caller owns all memory;
+ *    `workspace` must stay valid until the work on `stream` ends.
+ *  - `workspace` holds the intermediates between the library's kernels; query its size with the
+ *    matching *_workspace_size() function (its layout is private to the library).  ws_bytes
+ *    smaller than that returns BLR_ERR_WORKSPACE.
+ *  - Validation, planning and tensor-map encoding of every phase happen on the host before the
+ *    first launch; on any of the errors below except a launch failure nothing is enqueued.
  *      BLR_ERR_NULL        a required pointer is NULL (with n_tok > 0)
  *      BLR_ERR_SHAPE       a non-positive dimension, n_tok < 0, b1 !| d_in, b2 !| d_out,
  *                          or (Monarch) r_blk inconsistent with the factor shapes
  *      BLR_ERR_ALIGN       a row pitch that is not a multiple of 16 bytes, i.e. d_in, d_out,
  *                          r, r', p or q not a multiple of 8, or a pointer not 16-B aligned
  *      BLR_ERR_UNSUPPORTED a shape outside the kernel envelope (b1 or b2 > 16, r' > 256,
- *                          Monarch transposed output order) -- there is NO CPU fallback
+ *                          n_tok >= 2^31) -- there is NO CPU fallback
  *      BLR_ERR_WORKSPACE   ws_bytes too small
  *      BLR_ERR_ARCH        the current device is not a compute-capability 10.0 (sm_100a) GPU
- *      BLR_ERR_CUDA        a CUDA runtime/driver error while encoding tensor maps or launching
+ *      BLR_ERR_CUDA        a CUDA runtime/driver error while encoding tensor maps (nothing
+ *                          enqueued) or launching a kernel (earlier kernels of the same call
+ *                          may already be enqueued; the stream then holds partial work)
  *  - n_tok == 0 is a successful no-op.
  *  - The library holds one process-wide, thread-safe cache (device properties and the
  *    tensor-map encoder); blr_clear_cache() drops it.
@@ -75,7 +88,7 @@ typedef void* blr_stream_t; /* a cudaStream_t */
 /*
  * Low-rank layer, Y = (X V) U.
  *   X [n_tok, d_in], V [d_in, r], U [r, d_out], Y [n_tok, d_out].
- *   Workspace: the bf16 intermediate Z [n_tok, r].
+ *   Workspace: the intermediate Z [n_tok, r] (bf16; hi|lo pair when r < 128).
  */
 blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t r,
                               const void* V, const void* U, void* Y, void* workspace,
@@ -92,7 +105,7 @@ size_t blr_lowrank_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, in
  *   Y [n_tok, d_out]      out_order must be BLR_OUT_CANONICAL.
  *   The r'<->b2 and b2<->b1 permutations are folded into the kernel's TMA
  *   addressing; V is read in place in either layout (no re-layout pass).
- *   Workspace: the bf16 intermediate Z' [b2][n_tok][b1*r_blk].
+ *   Workspace: the intermediate Z' [b2][n_tok][b1*r_blk] (bf16; hi|lo pair when b1*r' < 128).
  */
 blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1,
                               int64_t b2, int64_t r_blk, const void* V, const void* U,
@@ -106,7 +119,8 @@ size_t blr_monarch_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, in
  * storage:
  *   V [b1, p, r], S [b1, b2, r] (the diagonals of S_{l,k}), U [b2, r, q], Y [n_tok, d_out].
  *   (north_star's s_ij is S[j, i, :]: index order (input block, output block); R5.)
- *   Workspace: the bf16 intermediate Z'' [b2][n_tok][r]  (the S-weighted block sums).
+ *   Workspace: the S-weighted block sums Z'' (bf16, b2 * n_tok * r values) and, when b1*r > 512,
+ *   the fp16 first-stage outputs Z_l (b1 * n_tok * r values), token count padded to 128.
  */
 blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1,
                             int64_t b2, int64_t r, const void* V, const void* S, const void* U,

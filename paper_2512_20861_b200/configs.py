@@ -111,14 +111,34 @@ C4_MONARCH = Workload("C4M", "Llama-7B MLP (4096<->11008) Monarch prefill seq 81
                        table3("Llama-7B", "down_proj", "monarch")))
 
 
+# >= 2x parameter compression at the Llama-7B MLP (north_star target; SURVEY §8(d) compression
+# note): BLAST r = 1456 (CF 2.016) and Monarch r' = 88 (r = 1408, CF 2.12).  Table 3's own ranks
+# (C4 / C4M) give CF 1.97 / 1.94.
+C4_2X = Workload("C4X", "Llama-7B MLP (4096<->11008) at >=2x compression: BLAST r=1456, Monarch r'=88, seq 8192 x batch 8",
+                 8 * 8192,
+                 (Layer("Llama-7B", "gate_up_proj", 4096, 11008, "blast", 1456, 16),
+                  Layer("Llama-7B", "down_proj", 11008, 4096, "blast", 1456, 16),
+                  Layer("Llama-7B", "gate_up_proj", 4096, 11008, "monarch", 1408, 16),
+                  Layer("Llama-7B", "down_proj", 11008, 4096, "monarch", 1408, 16)))
+
+
 def c5(images: int) -> Workload:
+    """ViT-B layers (197 tokens per image, Table 3): qkv, fc1, fc2 in Monarch
+    (r = 128, b = 4) and BLAST (r = 128, b = 3)."""
     vit = tuple(table3("ViT-B", nm, m) for m in ("monarch", "blast") for nm in ("attn_qkv", "fc1", "fc2"))
-    return Workload(f"C5-ViT-{images}", f"ViT-B layers, {images} images x 197 tokens", 197 * images, vit)
+    return Workload(f"C5V-{images}", f"ViT-B layers, {images} images x 197 tokens", 197 * images, vit)
 
 
 def c5_dit(images: int) -> Workload:
+    """DiT-XL/2 layers (256 tokens per image at 256x256 / patch 2, reading
+    R15): QKV (r = 384, b = 9) and fc1 (r = 256, b = 9), BLAST (the paper has no DiT Monarch)."""
     dit = (table3("DiT-XL/2", "qkv_proj", "blast"), table3("DiT-XL/2", "fc1", "blast"))
-    return Workload(f"C5-DiT-{images}", f"DiT-XL/2 layers, {images} images x 256 tokens", 256 * images, dit)
+    return Workload(f"C5D-{images}", f"DiT-XL/2 layers, {images} images x 256 tokens", 256 * images, dit)
 
 
-WORKLOADS = {w.key: w for w in (C1, C2, C3, C4, C4_MONARCH)}
+C5_IMAGES = (1, 8, 64, 256)   # BASELINE.json configs[4]: batch sweep 1-256 images
+
+WORKLOADS = {w.key: w for w in (C1, C2, C3, C4, C4_MONARCH, C4_2X)}
+for _im in C5_IMAGES:
+    WORKLOADS[f"C5V-{_im}"] = c5(_im)
+    WORKLOADS[f"C5D-{_im}"] = c5_dit(_im)

@@ -225,8 +225,11 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
                   const DevInfo& d, int dev, cudaStream_t stream) {
     KParams p = p_in;
     p.trace = t_trace;
+    p.first = t_last_launches == 0 ? 1 : 0;  // first launch of this API call (PDL ordering, kernel)
+#ifdef BLR_DEBUG_KNOBS
     if (const char* e = getenv("BLR_DBG")) p.dbg = atoi(e);  // debug experiments only
     if (const char* e = getenv("BLR_DBG_LAUNCH"); e && atoi(e) != t_last_launches) p.dbg = 0;  // only launch k
+#endif
     if (t_trace) t_trace += 128 * 256;  // next launch traces into the next slot
     auto kfn = blr::blr_gemm_kernel<KIND, PAIR, OUTF>;
     const blr::SmemLayout L = blr::smem_layout(p);
@@ -377,15 +380,35 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     return finish_plan(p, true, 32 * p.c_box_w * esz, d.sm_count / pair);
 }
 
+// A planned GEMM phase: parameters and tensor maps, encoded before anything is launched (so a
+// planning or encoding error leaves the stream untouched, include/blr.h).
+struct GemmPrep {
+    KParams p;
+    CUtensorMap ta, tb, tc;
+    int pair = 1;
+    int outf = 0;  // 0 bf16, 1 fp16, 2 fp16 tile-blocked
+};
+
+blr_status gemm_run(const GemmPrep& g, const DevInfo& d, int dev, cudaStream_t st) {
+    if (g.outf == 2)
+        return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st)
+                           : launch<blr::KIND_GEMM, 1, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st);
+    if (g.outf == 1)
+        return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 1>(g.ta, g.tb, g.tc, g.p, d, dev, st)
+                           : launch<blr::KIND_GEMM, 1, 1>(g.ta, g.tb, g.tc, g.p, d, dev, st);
+    if (g.pair == 2) return launch<blr::KIND_GEMM, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st);
+    return launch<blr::KIND_GEMM, 1>(g.ta, g.tb, g.tc, g.p, d, dev, st);
+}
+
 // One plain GEMM phase: out[g](t, c) = sum_k A[g](t, k) B[g](k, c), K-major A.
 //   A map: a_gmid ? (K*comp, groups, rows) : (K*comp, rows, groups) with the given strides.
 //   comp == 2: A rows hold [hi | lo] (lo at column offset K) multiplying the same B rows.
 // CTA pairs (cta_group::2) are used when the weight slice would otherwise stream and outweighs
 // the activation tile (BLR_PAIR=1/2 forces a mode).
-blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A, int a_gmid, int64_t a_row_stride,
-                      int64_t a_group_stride, int64_t n_tok, int64_t K, int64_t groups, int64_t N, const void* B,
-                      bool b_mn_major, const OutMap& out, int comp, int a_blocked = 0) {
-    KParams p;
+blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid, int64_t a_row_stride,
+                        int64_t a_group_stride, int64_t n_tok, int64_t K, int64_t groups, int64_t N, const void* B,
+                        bool b_mn_major, const OutMap& out, int comp, int a_blocked = 0) {
+    KParams& p = g.p;
     int pair = 1;
     const char* pe = getenv("BLR_PAIR");
     const int force = pe ? atoi(pe) : 0;
@@ -416,7 +439,9 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
     p.a_ptr = static_cast<const __nv_bfloat16*>(A);
     p.a_nchunks = static_cast<int>(K / 8);
 
-    CUtensorMap ta, tb, tc;
+    CUtensorMap& ta = g.ta;
+    CUtensorMap& tb = g.tb;
+    CUtensorMap& tc = g.tc;
     if (a_blocked) {
         // tile-blocked A [g][T][K/8][128][8] viewed as rows of 64 elements (128 B): a K block of a
         // 128-row tile is 128 consecutive rows, one unswizzled tensor box (it lands in smem byte
@@ -478,14 +503,9 @@ blr_status gemm_phase(const DevInfo& d, int dev, cudaStream_t st, const void* A,
         if (!encode(&tc, out.ptr, 4, dims, strb, box, CU_TENSOR_MAP_SWIZZLE_NONE, out.f32)) return BLR_ERR_CUDA;
     }
     // fp16 output (BLAST split-path Z) is a separate instantiation: the bf16 epilogue stays as is
-    if (out.f32 == 2 && out.blocked)
-        return pair == 2 ? launch<blr::KIND_GEMM, 2, 2>(ta, tb, tc, p, d, dev, st)
-                         : launch<blr::KIND_GEMM, 1, 2>(ta, tb, tc, p, d, dev, st);
-    if (out.f32 == 2)
-        return pair == 2 ? launch<blr::KIND_GEMM, 2, 1>(ta, tb, tc, p, d, dev, st)
-                         : launch<blr::KIND_GEMM, 1, 1>(ta, tb, tc, p, d, dev, st);
-    if (pair == 2) return launch<blr::KIND_GEMM, 2>(ta, tb, tc, p, d, dev, st);
-    return launch<blr::KIND_GEMM, 1>(ta, tb, tc, p, d, dev, st);
+    g.pair = pair;
+    g.outf = out.f32 == 2 ? (out.blocked ? 2 : 1) : 0;
+    return BLR_OK;
 }
 
 // ------------------------------------------------------- one-launch LR / Monarch layer ----
@@ -503,17 +523,6 @@ bool fused_wanted(int64_t n_tok, int64_t k2, int64_t n1, bool contracting_lr) {
     if (e && e[0] == '0') return false;
     if (e && e[0] == '1') return true;
     return n_tok >= 256 && !contracting_lr;
-}
-
-// BLAST S2 + S3 in one launch (blr_fused.cuh mode 2): few blocks (each item reads b1 Z_l tiles
-// per output block k), 128 <= r <= 256 (Z'' of a tile fits the smem A operand).  Opt-in only
-// (BLR_FUSED=1): measured slower than the tensor-core S2 + S3 kernels on GPT2-S BLAST (c_fc 44.4 vs
-// 17.9 + 23.9 us; the CUDA-core block sum serialises ahead of each item's S3).
-bool blast_s23_wanted(int64_t n_tok, int64_t b1, int64_t r) {
-    if (r % 64 || r < 128 || r > 256 || b1 * r * 4 > (32 << 10)) return false;
-    const char* e = getenv("BLR_FUSED");
-    (void)n_tok;
-    return e && e[0] == '1';
 }
 
 void fused_b_staging(bool mn, int n, int& boxes, uint32_t& bytes, uint32_t& lbo, uint32_t& sbo, uint32_t& kstep) {
@@ -561,7 +570,7 @@ blr_status fused_launch(const DevInfo& d, int dev, cudaStream_t st, blr::FParams
     p.items = static_cast<int>(base * p.n_parts);
     p.c_box_w = chunk_width(p.bn2);
     p.c_swz = pick_swz(p.c_box_w * 2).mask;
-    if (p.mon != 2) p.s1_bytes = static_cast<uint32_t>(blr::BM * blr::BK * 2) + p.b1_bytes;
+    p.s1_bytes = static_cast<uint32_t>(blr::BM * blr::BK * 2) + p.b1_bytes;
     p.slot_bytes = static_cast<uint32_t>(rup(std::max<int64_t>(p.s1_bytes, p.b2_bytes), 1024));
     // two staging buffers per epilogue warp (Y stores overlap the next chunk's staging) when the
     // ring still gets >= 3 slots, else one (BLR_FUSED_BUFS=1/2 forces)
@@ -933,13 +942,17 @@ blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         if (s != BLR_ERR_UNSUPPORTED) return s;
     }
     const int comp = comp_factor(r);
+    // both phases are planned (tensor maps encoded) before the first launch
+    GemmPrep g1, g3;
     // S1: Z = X V  (V is [d_in][r]: MN-major B); Z rows [hi | lo] when compensated
-    s = gemm_phase(d, dev, st, X, 0, d_in, 0, n_tok, d_in, 1, r, V, true,
-                   OutMap{workspace, 0, comp, r, r, r * comp}, 1);
+    s = gemm_prepare(g1, d, X, 0, d_in, 0, n_tok, d_in, 1, r, V, true, OutMap{workspace, 0, comp, r, r, r * comp}, 1);
     if (s != BLR_OK) return s;
     // S3: Y = Z U  (U is [r][d_out]: MN-major B)
-    return gemm_phase(d, dev, st, workspace, 0, r * comp, 0, n_tok, r, 1, d_out, U, true,
-                      OutMap{Y, 0, 1, d_out, d_out, d_out}, comp);
+    s = gemm_prepare(g3, d, workspace, 0, r * comp, 0, n_tok, r, 1, d_out, U, true,
+                     OutMap{Y, 0, 1, d_out, d_out, d_out}, comp);
+    if (s != BLR_OK) return s;
+    s = gemm_run(g1, d, dev, st);
+    return s != BLR_OK ? s : gemm_run(g3, d, dev, st);
 }
 
 blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
@@ -1038,7 +1051,11 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
             p.BN *= pair;
             p.r_blk = static_cast<int>(r_blk);
             p.out_lo_off = comp == 2 ? K2 : 0;
+            // staged chunk inside one output block k (CW divides r'); an r' without a wide
+            // multiple-of-8 divisor (e.g. 88 = 8 * 11) stores whole unswizzled r'-wide rows instead
+            // of 8-column boxes (16-B rows made the C4X Monarch S1 TMA-op bound: 4.4 ms vs 1.1 ms)
             p.c_box_w = chunk_width(static_cast<int>(r_blk));
+            if (p.c_box_w < 32 && r_blk <= 128) p.c_box_w = static_cast<int>(r_blk);
             p.c_swz = pick_swz(p.c_box_w * 2).mask;
             // weight-stationary only when every slice gets >= 2 CTAs: with short K (p) a tile's MMA is
             // brief and slice ownership idles SMs (measured on Llama-7B: streaming 1.22 ms vs 1.44 ms)
@@ -1083,13 +1100,17 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
                                   static_cast<uint64_t>(K2 * comp) * 2, static_cast<uint64_t>(K2 * comp * n_tok) * 2};
         const uint32_t cbox[5] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32, 1};
         if (!encode(&tc, workspace, 5, cd, cstr, cbox, cs.mode)) return BLR_ERR_CUDA;
+        // ---- phase 2: Y[t, k q + c] = sum_kk Z'[k][t][kk] U[k][c][kk]  (U is [N][K]: K-major B),
+        //      planned before phase 1 is launched
+        GemmPrep g2;
+        s = gemm_prepare(g2, d, workspace, 0, K2 * comp, n_tok * K2 * comp, n_tok, K2, b2, qdim, U, false,
+                         OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
+        if (s != BLR_OK) return s;
         s = pair == 2 ? launch<blr::KIND_MONARCH_PROJ, 2>(ta, tb, tc, p, d, dev, st)
                       : launch<blr::KIND_MONARCH_PROJ, 1>(ta, tb, tc, p, d, dev, st);
         if (s != BLR_OK) return s;
+        return gemm_run(g2, d, dev, st);
     }
-    // ---- phase 2: Y[t, k q + c] = sum_kk Z'[k][t][kk] U[k][c][kk]  (U is [N][K]: K-major B)
-    return gemm_phase(d, dev, st, workspace, 0, K2 * comp, n_tok * K2 * comp, n_tok, K2, b2, qdim, U, false,
-                      OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
 }
 
 blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
@@ -1142,7 +1163,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         return decode_mn(st, zp2, 1, r, n_tok * r, U, qdim, r * qdim, Y, 1, d_out, qdim, n_tok, r, qdim, b2, part);
     }
     const int comp = comp_factor(r);
-    void* zpp = workspace;  // Z'' [b2][n][r*comp]
+    void* zpp = workspace;  // Z'' [b2][n][r*comp] (split path: tile-blocked, then fp16 Z after it)
 
     if (blast_fused(b1, r)) {
         // ---- phase 1: Z''[k][t][rho] = sum_l S[l,k,rho] (X_l V_l)[t, rho]  (S1 on tcgen05, S2 fused)
@@ -1184,199 +1205,176 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
                                   static_cast<uint64_t>(r * comp * n_tok) * 2};
         const uint32_t cbox[4] = {static_cast<uint32_t>(R / 2), 1, 32, 1};
         if (!encode(&tc, zpp, 4, cd, cstr, cbox, pick_swz(R).mode)) return BLR_ERR_CUDA;
+        // ---- S3: Y_k = Z''_k U_k  (U is [b2][r][q]: MN-major B), planned before phase 1 launches
+        GemmPrep g3;
+        s = gemm_prepare(g3, d, zpp, 0, r * comp, n_tok * r * comp, n_tok, r, b2, qdim, U, true,
+                         OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
+        if (s != BLR_OK) return s;
         s = launch<blr::KIND_BLAST_PROJ, 1>(ta, tb, tc, p, d, dev, st);
-        if (s != BLR_OK) return s;
-    } else {
-        // ---- S1: Z[l][t][rho] = (X_l V_l)[t, rho]  -- grouped GEMM over l (A = X viewed (p, b1, n))
-        const char* s2e = getenv("BLR_S2");
-        // tensor-core S2 (single-rounded Z''): Z and Z'' tile-blocked [g][T][r/8][128][8]
-        const bool s2_mma = comp == 1 && !(s2e && !strcmp(s2e, "cuda"));
-        const int64_t n_pad = rup(n_tok, blr::BM);
-        void* zl = static_cast<char*>(workspace) + static_cast<size_t>(b2) * n_pad * r * 2 * comp;
-        // tile-blocked Z for the tensor-core S2: [l][T][r/8][128][8], group stride n_pad * r
-        OutMap zmap{zl, 2, 1, r, s2_mma ? n_pad * r : n_tok * r, r};
-        zmap.blocked = s2_mma ? 1 : 0;
-        s = gemm_phase(d, dev, st, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true, zmap, 1);
-        if (s != BLR_OK) return s;
-        // ---- S2 + S3 in one launch for few blocks (blr_fused.cuh mode 2): Z'' stays on chip
-        if (s2_mma && blast_s23_wanted(n_tok, b1, r)) {
-            blr::FParams p = {};
-            p.n_tok = static_cast<int>(n_tok);
-            p.mon = 2;
-            p.z = static_cast<const __half*>(zl);
-            p.S = static_cast<const __nv_bfloat16*>(S);
-            p.b1 = static_cast<int>(b1);
-            p.r = static_cast<int>(r);
-            p.s1_bytes = static_cast<uint32_t>(b1) * 8192u;
-            p.stab_bytes = static_cast<uint32_t>(b1 * r * 4);
-            p.g1 = 1;
-            p.k1_blocks = static_cast<int>(r / 32);
-            p.n1 = static_cast<int>(r);
-            p.b1_mn = 1;
-            p.g2 = static_cast<int>(b2);
-            p.n2 = static_cast<int>(qdim);
-            p.b2_mn = 1;
-            CUtensorMap tb2;
-            {   // U [b2][r][q]: MN-major, box (64 cols, 64 K rows, 1)
-                const uint64_t dims[3] = {static_cast<uint64_t>(qdim), static_cast<uint64_t>(r), static_cast<uint64_t>(b2)};
-                const uint64_t str[2] = {static_cast<uint64_t>(qdim) * 2, static_cast<uint64_t>(qdim * r) * 2};
-                const uint32_t box[3] = {64, blr::BK, 1};
-                if (!encode(&tb2, U, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
-            }
-            // (the A / B1 maps are unused in mode 2: pass U's map in their place)
-            s = fused_launch(d, dev, st, p, tb2, tb2, tb2, Y, d_out);
-            if (s != BLR_ERR_UNSUPPORTED) return s;
+        return s != BLR_OK ? s : gemm_run(g3, d, dev, st);
+    }
+
+    // ---- split path (b1 r > TMEM): S1 grouped GEMM -> fp16 Z, S2, S3.  Every phase is planned and
+    //      every tensor map encoded before S1 is launched.
+    const char* s2e = getenv("BLR_S2");
+    // tensor-core S2 (single-rounded Z''): Z and Z'' tile-blocked [g][T][r/8][128][8]
+    const bool s2_mma = comp == 1 && !(s2e && !strcmp(s2e, "cuda"));
+    const int64_t n_pad = rup(n_tok, blr::BM);
+    void* zl = static_cast<char*>(workspace) + static_cast<size_t>(b2) * n_pad * r * 2 * comp;
+    // S1: Z[l][t][rho] = (X_l V_l)[t, rho]  -- grouped GEMM over l (A = X viewed (p, b1, n));
+    // tile-blocked Z for the tensor-core S2: [l][T][r/8][128][8], group stride n_pad * r
+    OutMap zmap{zl, 2, 1, r, s2_mma ? n_pad * r : n_tok * r, r};
+    zmap.blocked = s2_mma ? 1 : 0;
+    GemmPrep g1, g3;
+    s = gemm_prepare(g1, d, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true, zmap, 1);
+    if (s != BLR_OK) return s;
+    // S3: Y_k = Z''_k U_k (U is [b2][r][q]: MN-major B); A tile-blocked after the tensor-core S2
+    s = s2_mma ? gemm_prepare(g3, d, zpp, 0, r, n_tok * r, n_tok, r, b2, qdim, U, true,
+                              OutMap{Y, 0, 1, d_out, qdim, d_out}, 1, /*a_blocked=*/1)
+               : gemm_prepare(g3, d, zpp, 0, r * comp, n_tok * r * comp, n_tok, r, b2, qdim, U, true,
+                              OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
+    if (s != BLR_OK) return s;
+
+    if (s2_mma) {
+        // ---- S2 on the tensor cores (blast_s2_mma_kernel): tile-blocked fp16 Z [l][T][r/8][128][8]
+        //      in, tile-blocked bf16 Z'' [k][T][r/8][128][8] out
+        const blr::S2MLayout sl = blr::s2m_layout(static_cast<int>(b1), static_cast<int>(b2));
+        const char* oe = getenv("BLR_S2_ORDER");
+        const int s2_order = oe ? atoi(oe) : 0;
+        const int64_t items = cdiv(n_tok, 128) * (r / 8);
+        // b2 <= 8: the half-register instantiation, two CTAs per SM when both fit in smem
+        const char* se = getenv("BLR_S2_SMALL");
+        const bool small = b2 <= 8 && !(se && se[0] == '0');
+        const int per_sm = (small && 2 * (sl.total + 1024 + 1024) <= 233472) ? 2 : 1;
+        auto s2fn = small ? blr::blast_s2_mma_kernel<8> : blr::blast_s2_mma_kernel<16>;
+        const char* pe2 = getenv("BLR_S2_PDL");
+        const bool s2_pdl = pdl_enabled() && !(pe2 && pe2[0] == '0');
+        CUtensorMap tmz, tmzpp;
+        {   // Z / Z'' tile-blocked [g][T][r/8][128][8] viewed (64 elem, 16 rows, T*r/8 panels, g)
+            const int64_t np = cdiv(n_tok, blr::BM) * (r / 8);
+            const uint64_t dz[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b1)};
+            const uint64_t sz[3] = {128, 2048, static_cast<uint64_t>(np) * 2048};
+            const uint32_t bz[4] = {64, 16, 1, static_cast<uint32_t>(b1)};
+            if (!encode(&tmz, zl, 4, dz, sz, bz, CU_TENSOR_MAP_SWIZZLE_NONE, 2)) return BLR_ERR_CUDA;
+            const uint64_t dp[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b2)};
+            const uint32_t bp[4] = {64, 16, 1, static_cast<uint32_t>(b2)};
+            if (!encode(&tmzpp, zpp, 4, dp, sz, bp, CU_TENSOR_MAP_SWIZZLE_NONE)) return BLR_ERR_CUDA;
         }
-        // ---- S2: Z''[k][t][rho] = sum_l S[l,k,rho] Z[l][t][rho]
-        if (s2_mma) {
-            // tensor-core S2 (blast_s2_mma_kernel): tile-blocked fp16 Z [l][T][r/8][128][8] in,
-            // tile-blocked bf16 Z'' [k][T][r/8][128][8] out (2-KB panels, 1-D bulk copies)
-            const blr::S2MLayout sl = blr::s2m_layout(static_cast<int>(b1), static_cast<int>(b2));
-            const char* oe = getenv("BLR_S2_ORDER");
-            const int s2_order = oe ? atoi(oe) : 0;
-            const int64_t items = cdiv(n_tok, 128) * (r / 8);
-            // b2 <= 8: the half-register instantiation, two CTAs per SM when both fit in smem
-            const char* se = getenv("BLR_S2_SMALL");
-            const bool small = b2 <= 8 && !(se && se[0] == '0');
-            const int per_sm = (small && 2 * (sl.total + 1024 + 1024) <= 233472) ? 2 : 1;
-            auto s2fn = small ? blr::blast_s2_mma_kernel<8> : blr::blast_s2_mma_kernel<16>;
-            const char* pe2 = getenv("BLR_S2_PDL");
-            const bool s2_pdl = pdl_enabled() && !(pe2 && pe2[0] == '0');
-            cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(items, static_cast<int64_t>(per_sm) * d.sm_count)));
-            cfg.blockDim = dim3(blr::S2M_THREADS);
-            cfg.dynamicSmemBytes = sl.total + 1024;
-            cfg.stream = st;
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[0].val.programmaticStreamSerializationAllowed = s2_pdl ? 1 : 0;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            {
-                std::lock_guard<std::mutex> lk(g_mu);
-                if (!g_attr_set[8][dev]) {
-                    if (cudaFuncSetAttribute(blr::blast_s2_mma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             232448) != cudaSuccess ||
-                        cudaFuncSetAttribute(blr::blast_s2_mma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             232448) != cudaSuccess)
-                        return BLR_ERR_CUDA;
-                    g_attr_set[8][dev] = true;
-                }
-            }
-            const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
-            if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
-            CUtensorMap tmz, tmzpp;
-            {   // Z / Z'' tile-blocked [g][T][r/8][128][8] viewed (64 elem, 16 rows, T*r/8 panels, g)
-                const int64_t np = cdiv(n_tok, blr::BM) * (r / 8);
-                const uint64_t dz[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b1)};
-                const uint64_t sz[3] = {128, 2048, static_cast<uint64_t>(np) * 2048};
-                const uint32_t bz[4] = {64, 16, 1, static_cast<uint32_t>(b1)};
-                if (!encode(&tmz, zl, 4, dz, sz, bz, CU_TENSOR_MAP_SWIZZLE_NONE, 2)) return BLR_ERR_CUDA;
-                const uint64_t dp[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b2)};
-                const uint32_t bp[4] = {64, 16, 1, static_cast<uint32_t>(b2)};
-                if (!encode(&tmzpp, zpp, 4, dp, sz, bp, CU_TENSOR_MAP_SWIZZLE_NONE)) return BLR_ERR_CUDA;
-            }
-            if (cudaLaunchKernelEx(&cfg, s2fn, tmz, tmzpp, static_cast<const __half*>(zl),
-                                   static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
-                                   static_cast<int>(n_tok), static_cast<int>(b1), static_cast<int>(b2),
-                                   static_cast<int>(r), s2_order) != cudaSuccess)
-                return BLR_ERR_CUDA;
-            if (cudaGetLastError() != cudaSuccess) return BLR_ERR_CUDA;
-            if (prof) {
-                if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
-                ++t_prof_n;
-            }
-            ++t_last_launches;
-            return gemm_phase(d, dev, st, zpp, 0, r, n_tok * r, n_tok, r, b2, qdim, U, true,
-                              OutMap{Y, 0, 1, d_out, qdim, d_out}, 1, /*a_blocked=*/1);
-        }
-        // CUDA-core S2 (blast_s2_kernel; used for compensated Z'' (r < 128) or with BLR_S2=cuda):
-        // fp16 Z viewed (rho, t, l), box (64, S2_ROWS, b1): one item's b1 row segments per request
-        CUtensorMap tz;
         {
-            const uint64_t dims[3] = {static_cast<uint64_t>(r), static_cast<uint64_t>(n_tok), static_cast<uint64_t>(b1)};
-            const uint64_t str[2] = {static_cast<uint64_t>(r) * 2, static_cast<uint64_t>(r * n_tok) * 2};
-            const uint32_t box[3] = {64, static_cast<uint32_t>(blr::S2_ROWS), static_cast<uint32_t>(b1)};
-            if (!encode(&tz, zl, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, 2)) return BLR_ERR_CUDA;
+            std::lock_guard<std::mutex> lk(g_mu);
+            if (!g_attr_set[8][dev]) {
+                if (cudaFuncSetAttribute(blr::blast_s2_mma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         232448) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_mma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         232448) != cudaSuccess)
+                    return BLR_ERR_CUDA;
+                g_attr_set[8][dev] = true;
+            }
         }
-        // KG output blocks per consumer warp (S held in registers: NL x KG packed pairs per lane;
-        // NL = b1 rounded up to 4/8/16, the extra planes are zero)
-        const int kg = b2 == 1 ? 1 : 2;
-        const int nw = static_cast<int>(cdiv(b2, kg)) * blr::S2_RSPLIT;
-        const int nl = b1 <= 4 ? 4 : b1 <= 8 ? 8 : 16;
-        const int slabs = static_cast<int>(cdiv(n_tok, blr::S2_ROWS));
-        const int nchunks = static_cast<int>(cdiv(r, 64));
-        const int total = nchunks * slabs;
-        const int map_mode = 1;
-        // blocks per SM: up to 16 consumer warps per SM (<= 128 registers per thread)
-        const int bps = std::max(1, std::min(4, 16 / nw));
-        int grid = std::min<int>(total, bps * d.sm_count);
-        int ipb = static_cast<int>(cdiv(total, grid));
-        if (map_mode == 1) {  // a multiple of nchunks, at most bps block-slots per SM, >= 1 per chunk
-            const int gpc = std::max(1, std::min(slabs, bps * d.sm_count / nchunks));
-            grid = gpc * nchunks;
-        } else {
-            grid = static_cast<int>(cdiv(total, ipb));
-        }
-        const size_t stage_bytes = static_cast<size_t>(nl) * blr::S2_ROWS * 64 * 2;
-        const size_t ring_bytes = (192u << 10) / bps;  // ~192 KB of ring per SM
-        const int nst = static_cast<int>(std::max<size_t>(2, std::min<size_t>(blr::S2_MAX_STAGES, ring_bytes / stage_bytes)));
-        const size_t smem = nst * stage_bytes + 16 * nst;
+        s = gemm_run(g1, d, dev, st);
+        if (s != BLR_OK) return s;
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>(grid));
-        cfg.blockDim = dim3(static_cast<unsigned>(32 * nw));
-        cfg.dynamicSmemBytes = smem;
+        cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(items, static_cast<int64_t>(per_sm) * d.sm_count)));
+        cfg.blockDim = dim3(blr::S2M_THREADS);
+        cfg.dynamicSmemBytes = sl.total + 1024;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        // S2 is launched without programmatic dependent launch: its blocks, started early on the
-        // few SMs the S1 grid leaves idle, measured ~4 us slower per GPT2-S layer
-        attr[0].val.programmaticStreamSerializationAllowed = 0;
+        attr[0].val.programmaticStreamSerializationAllowed = s2_pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
-        if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess)
+        if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+        if (cudaLaunchKernelEx(&cfg, s2fn, tmz, tmzpp, static_cast<const __half*>(zl),
+                               static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
+                               static_cast<int>(n_tok), static_cast<int>(b1), static_cast<int>(b2),
+                               static_cast<int>(r), s2_order) != cudaSuccess)
             return BLR_ERR_CUDA;
-        {
-            std::lock_guard<std::mutex> lk(g_mu);
-            if (!g_attr_set[7][dev]) {
-                const int mx = 220 << 10;
+        if (prof) {
+            if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+            ++t_prof_n;
+        }
+        ++t_last_launches;
+        return gemm_run(g3, d, dev, st);
+    }
+    // ---- CUDA-core S2 (blast_s2_kernel; used for compensated Z'' (r < 128) or with BLR_S2=cuda):
+    // fp16 Z viewed (rho, t, l), box (64, S2_ROWS, b1): one item's b1 row segments per request
+    CUtensorMap tz;
+    {
+        const uint64_t dims[3] = {static_cast<uint64_t>(r), static_cast<uint64_t>(n_tok), static_cast<uint64_t>(b1)};
+        const uint64_t str[2] = {static_cast<uint64_t>(r) * 2, static_cast<uint64_t>(r * n_tok) * 2};
+        const uint32_t box[3] = {64, static_cast<uint32_t>(blr::S2_ROWS), static_cast<uint32_t>(b1)};
+        if (!encode(&tz, zl, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_NONE, 2)) return BLR_ERR_CUDA;
+    }
+    // KG output blocks per consumer warp (S held in registers: NL x KG packed pairs per lane;
+    // NL = b1 rounded up to 4/8/16, the extra planes are zero)
+    const int kg = b2 == 1 ? 1 : 2;
+    const int nw = static_cast<int>(cdiv(b2, kg)) * blr::S2_RSPLIT;
+    const int nl = b1 <= 4 ? 4 : b1 <= 8 ? 8 : 16;
+    const int slabs = static_cast<int>(cdiv(n_tok, blr::S2_ROWS));
+    const int nchunks = static_cast<int>(cdiv(r, 64));
+    const int total = nchunks * slabs;
+    const int map_mode = 1;
+    // blocks per SM: up to 16 consumer warps per SM (<= 128 registers per thread); a multiple of
+    // nchunks, at most bps block-slots per SM, >= 1 per chunk
+    const int bps = std::max(1, std::min(4, 16 / nw));
+    const int gpc = std::max(1, std::min(slabs, bps * d.sm_count / nchunks));
+    const int grid = gpc * nchunks;
+    const int ipb = static_cast<int>(cdiv(total, grid));
+    const size_t stage_bytes = static_cast<size_t>(nl) * blr::S2_ROWS * 64 * 2;
+    const size_t ring_bytes = (192u << 10) / bps;  // ~192 KB of ring per SM
+    const int nst = static_cast<int>(std::max<size_t>(2, std::min<size_t>(blr::S2_MAX_STAGES, ring_bytes / stage_bytes)));
+    const size_t smem = nst * stage_bytes + 16 * nst;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_attr_set[7][dev]) {
+            const int mx = 220 << 10;
 #define BLR_S2_ATTR(KG, NL) \
     cudaFuncSetAttribute(blr::blast_s2_kernel<KG, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
-                if (BLR_S2_ATTR(1, 4) || BLR_S2_ATTR(1, 8) || BLR_S2_ATTR(1, 16) || BLR_S2_ATTR(2, 4) ||
-                    BLR_S2_ATTR(2, 8) || BLR_S2_ATTR(2, 16))
-                    return BLR_ERR_CUDA;
+            if (BLR_S2_ATTR(1, 4) || BLR_S2_ATTR(1, 8) || BLR_S2_ATTR(1, 16) || BLR_S2_ATTR(2, 4) ||
+                BLR_S2_ATTR(2, 8) || BLR_S2_ATTR(2, 16))
+                return BLR_ERR_CUDA;
 #undef BLR_S2_ATTR
-                g_attr_set[7][dev] = true;
-            }
+            g_attr_set[7][dev] = true;
         }
-        const auto* sb = static_cast<const __nv_bfloat16*>(S);
-        auto* ob = static_cast<__nv_bfloat16*>(zpp);
-        const int in = static_cast<int>(n_tok), ib1 = static_cast<int>(b1), ib2 = static_cast<int>(b2),
-                  ir = static_cast<int>(r);
-        cudaError_t le;
-        switch (kg * 32 + nl) {
+    }
+    s = gemm_run(g1, d, dev, st);
+    if (s != BLR_OK) return s;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(static_cast<unsigned>(32 * nw));
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    // S2 is launched without programmatic dependent launch: its blocks, started early on the
+    // few SMs the S1 grid leaves idle, measured ~4 us slower per GPT2-S layer
+    attr[0].val.programmaticStreamSerializationAllowed = 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+    if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+    const auto* sb = static_cast<const __nv_bfloat16*>(S);
+    auto* ob = static_cast<__nv_bfloat16*>(zpp);
+    const int in = static_cast<int>(n_tok), ib1 = static_cast<int>(b1), ib2 = static_cast<int>(b2),
+              ir = static_cast<int>(r);
+    cudaError_t le = cudaErrorInvalidValue;
+    switch (kg * 32 + nl) {
 #define BLR_S2_CASE(KG, NL) \
     case KG * 32 + NL: \
         le = cudaLaunchKernelEx(&cfg, blr::blast_s2_kernel<KG, NL>, tz, sb, ob, in, ib1, ib2, ir, comp, slabs, total, \
                                 ipb, nchunks, map_mode, nst); \
         break;
-            BLR_S2_CASE(1, 4) BLR_S2_CASE(1, 8) BLR_S2_CASE(1, 16) BLR_S2_CASE(2, 4) BLR_S2_CASE(2, 8) BLR_S2_CASE(2, 16)
+        BLR_S2_CASE(1, 4) BLR_S2_CASE(1, 8) BLR_S2_CASE(1, 16) BLR_S2_CASE(2, 4) BLR_S2_CASE(2, 8) BLR_S2_CASE(2, 16)
 #undef BLR_S2_CASE
-            default: return BLR_ERR_UNSUPPORTED;
-        }
-        if (le != cudaSuccess) return BLR_ERR_CUDA;
-        if (cudaGetLastError() != cudaSuccess) return BLR_ERR_CUDA;
-        if (prof) {
-            if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess)
-                return BLR_ERR_CUDA;
-            ++t_prof_n;
-        }
-        ++t_last_launches;
     }
-    // ---- S3: Y_k = Z''_k U_k  (U is [b2][r][q]: MN-major B)
-    return gemm_phase(d, dev, st, zpp, 0, r * comp, n_tok * r * comp, n_tok, r, b2, qdim, U, true,
-                      OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
+    if (le != cudaSuccess) return BLR_ERR_CUDA;
+    if (prof) {
+        if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+        ++t_prof_n;
+    }
+    ++t_last_launches;
+    return gemm_run(g3, d, dev, st);
 }
 
 }  // extern "C"

@@ -10,11 +10,6 @@
 // it from there as its A operand.  Z never reaches HBM and the layer is one launch instead of two
 // (the intermediate round trip is what makes the unfused layer memory-bound).
 //
-// Mode 2 (BLAST split path with few blocks): the S1 output Z_l (fp16) is read back per tile and
-// the S-weighted block sum Z''_k = sum_l S[l,k,:] (.) Z_l is formed by the epilogue
-// warps in fp32 on CUDA cores (ascending l, one RNE rounding to bf16) straight into the smem A
-// operand of S3: Z'' never reaches HBM and S2 + S3 are one launch.
-//
 // Work item = (128-token tile T, output block k (Monarch; 1 for low rank), part of the S3 N range).
 // S1 is recomputed per part (the N split only exists to fill the SMs at small token counts).
 // Roles as in blr_gemm_kernel: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2..9
@@ -29,15 +24,8 @@ namespace blr {
 struct FParams {
     int n_tok, tiles_m;
     int g2, n_parts, items;  // items = tiles_m * g2 * n_parts, item = (T * g2 + k) * n_parts + part
-    int mon;                 // 1: Monarch operand addressing, 0: low rank, 2: BLAST S2+S3 (below)
-    // mode 2 (BLAST split path, small b1): the "S1 steps" load the S1 output Z (fp16, tile-blocked
-    // [l][T][r/8][128][8]) of tile T in 32-rho blocks, and the epilogue warps form
-    // Z''_k = sum_l S[l,k,:] (.) Z_l on CUDA cores straight into the smem A operand
-    const __half* z;         // mode 2: Z base
-    const __nv_bfloat16* S;  // mode 2: S [b1][b2][r]
-    int b1, r;               // mode 2: block count l, rank
-    uint32_t s1_bytes;       // bytes of one S1 / Z-load step in a ring slot
-    uint32_t stab_bytes;     // mode 2: fp32 S[l, k, :] table of the current item
+    int mon;                 // 1: Monarch operand addressing, 0: low rank
+    uint32_t s1_bytes;       // bytes of one S1 step (X block + V block) in a ring slot
     // S1: g1 sub-GEMMs (Monarch l), each K1 = k1_blocks * 64, N = n1 columns at TMEM col s * n1
     int g1, k1_blocks, n1;
     int b1_mn, b1_boxes;
@@ -57,15 +45,14 @@ struct FParams {
 };
 
 struct FLayout {
-    uint32_t ring, zs, stg, stab, bars, total;
+    uint32_t ring, zs, stg, bars, total;
 };
 __host__ __device__ inline FLayout fused_layout(const FParams& p) {
     FLayout L;
     L.ring = 0;
     L.zs = L.ring + p.slot_bytes * p.stages;
     L.stg = L.zs + (p.k2 / 64) * 16384u;
-    L.stab = L.stg + p.stage_warp_bytes * NUM_EPI_WARPS;
-    L.bars = L.stab + p.stab_bytes;
+    L.bars = L.stg + p.stage_warp_bytes * NUM_EPI_WARPS;
     L.total = L.bars + 8 * (2 * MAX_STAGES + 6) + 16;
     return L;
 }
@@ -114,7 +101,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    ptx::griddep_launch_dependents();
 
     const int k2b = p.k2 / 64;
     // item -> (token tile, output block, part); the S3 column range of the item
@@ -134,27 +120,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         int stage = 0;
         uint32_t phase = 0;
         ptx::griddep_wait();  // X may be the previous kernel's output
+        // the next kernel may start its prologue only once everything before this launch is
+        // complete (it may read weights before its own griddepcontrol.wait)
+        ptx::griddep_launch_dependents();
         for (int it = 0; it < nitems; ++it) {
             int T, kq, c_lo, c_hi;
             item_of(it, T, kq, c_lo, c_hi);
             const int m0 = T * BM;
-            for (int s = 0; s < p.g1; ++s) {  // S1 steps: X block + V block (mode 2: Z blocks)
+            for (int s = 0; s < p.g1; ++s) {  // S1 steps: X block + V block
                 for (int kb = 0; kb < p.k1_blocks; ++kb) {
                     ptx::mbar_wait(empty_bar + 8 * stage, phase ^ 1);
                     const uint32_t slot = ring + stage * p.slot_bytes, fb = full_bar + 8 * stage;
-                    if (p.mon == 2) {  // Z_l panels (l, T, 4 kb .. 4 kb + 3): 8 KB contiguous per l
-                        if (ptx::elect_one()) {
-                            ptx::mbar_arrive_expect_tx(fb, p.s1_bytes);
-                            const int nch = p.r >> 3;
-                            for (int l = 0; l < p.b1; ++l)
-                                ptx::bulk_load(slot + l * 8192u,
-                                               p.z + ((static_cast<long long>(l) * p.tiles_m + T) * nch + kb * 4) * (BM * 8),
-                                               8192u, fb);
-                        }
-                        __syncwarp();
-                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
-                        continue;
-                    }
                     if (ptx::elect_one()) {
                         ptx::mbar_arrive_expect_tx(fb, p.s1_bytes);
                         const int k0 = kb * BK;
@@ -199,10 +175,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         for (int it = 0; it < nitems; ++it) {
             int T, kq, c_lo, c_hi;
             item_of(it, T, kq, c_lo, c_hi);
-            if (p.mon == 2) {  // the item's Z-load ring steps are consumed by the epilogue warps
-                for (int j = 0; j < p.k1_blocks; ++j)
-                    if (++stage == p.stages) { stage = 0; phase ^= 1; }
-            } else {   // ---- S1: Z into buffer use & 1 (mode 2: Z'' comes from the epilogue)
+            {   // ---- S1: Z into buffer use & 1
                 const uint32_t b = use & 1;
                 ptx::mbar_wait(tempty_bar + 8 * b, ((use >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
@@ -268,75 +241,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int CW = p.c_box_w;
         const uint32_t row_bytes = CW * 2;
         uint32_t use = 0;
-        // mode 2: ring steps issued before this item's first Z-load step (the epilogue consumes the
-        // Z-load steps; the S3 steps in between belong to the MMA warp)
-        long long gstep = 0;
         uint32_t nstore = 0;  // staged Y chunks (staging buffer rotation)
         ptx::griddep_wait();  // our Y stores must not overtake the previous kernel's reads
         for (int it = 0; it < nitems; ++it) {
             int T, kq, c_lo, c_hi;
             item_of(it, T, kq, c_lo, c_hi);
             const int row0 = T * BM + quarter * 32;
-            if (p.mon == 2) {   // ---- Z''_k = sum_l S[l,k,:] (.) Z_l  ->  bf16 (RNE) -> swizzled K-major smem
-                const int et = threadIdx.x - 64;   // 0..255
-                const uint32_t stab = sbase + L.stab;
-                ptx::named_bar_sync(2, 32 * NUM_EPI_WARPS);  // previous item's table reads are done
-                for (int e = et; e < p.b1 * p.r; e += 32 * NUM_EPI_WARPS) {
-                    const int l = e / p.r, rho = e - l * p.r;
-                    ptx::st_shared_f32(stab + 4u * e, __bfloat162float(p.S[(static_cast<long long>(l) * p.g2 + kq) * p.r + rho]));
-                }
-                ptx::named_bar_sync(2, 32 * NUM_EPI_WARPS);
-                if (it > 0) ptx::mbar_wait(zsfree_bar, (it - 1) & 1);  // previous item's S3 read Z''
-                const int prow = et & 127, pp = et >> 7;  // row, which 2 of the block's 4 panels
-                for (int kb = 0; kb < p.k1_blocks; ++kb) {
-                    const int sstage = static_cast<int>((gstep + kb) % p.stages);
-                    ptx::mbar_wait(full_bar + 8 * sstage, static_cast<uint32_t>(((gstep + kb) / p.stages) & 1));
-                    const uint32_t slot = ring + sstage * p.slot_bytes;
-#pragma unroll
-                    for (int q2 = 0; q2 < 2; ++q2) {
-                        const int pan = pp * 2 + q2;       // panel within the 32-rho block
-                        const int col = kb * 32 + pan * 8; // first rho of the panel
-                        float acc[8];
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-                        for (int l = 0; l < p.b1; ++l) {   // ascending l, fp32 (as the S2 kernels)
-                            // a warp reads 512 contiguous bytes of Z (conflict-free); S is a broadcast
-                            const uint4 zw = ptx::ld_shared_v4(slot + l * 8192u + pan * 2048u + prow * 16u);
-                            const uint4 sa = ptx::ld_shared_v4(stab + 4u * (l * p.r + col));
-                            const uint4 sb = ptx::ld_shared_v4(stab + 4u * (l * p.r + col + 4));
-                            const float4 s0 = make_float4(__uint_as_float(sa.x), __uint_as_float(sa.y), __uint_as_float(sa.z),
-                                                          __uint_as_float(sa.w));
-                            const float4 s1 = make_float4(__uint_as_float(sb.x), __uint_as_float(sb.y), __uint_as_float(sb.z),
-                                                          __uint_as_float(sb.w));
-                            const float2 z0 = __half22float2(*reinterpret_cast<const __half2*>(&zw.x));
-                            const float2 z1 = __half22float2(*reinterpret_cast<const __half2*>(&zw.y));
-                            const float2 z2 = __half22float2(*reinterpret_cast<const __half2*>(&zw.z));
-                            const float2 z3 = __half22float2(*reinterpret_cast<const __half2*>(&zw.w));
-                            acc[0] = fmaf(s0.x, z0.x, acc[0]);
-                            acc[1] = fmaf(s0.y, z0.y, acc[1]);
-                            acc[2] = fmaf(s0.z, z1.x, acc[2]);
-                            acc[3] = fmaf(s0.w, z1.y, acc[3]);
-                            acc[4] = fmaf(s1.x, z2.x, acc[4]);
-                            acc[5] = fmaf(s1.y, z2.y, acc[5]);
-                            acc[6] = fmaf(s1.z, z3.x, acc[6]);
-                            acc[7] = fmaf(s1.w, z3.y, acc[7]);
-                        }
-                        uint4 w;
-                        w.x = ptx::pack_bf16x2(acc[0], acc[1]);
-                        w.y = ptx::pack_bf16x2(acc[2], acc[3]);
-                        w.z = ptx::pack_bf16x2(acc[4], acc[5]);
-                        w.w = ptx::pack_bf16x2(acc[6], acc[7]);
-                        const uint32_t chunk = (col & 63) >> 3;
-                        ptx::st_shared_v4(zs + (col >> 6) * 16384u + prow * 128u + ((chunk ^ (prow & 7)) << 4), w);
-                    }
-                    ptx::named_bar_sync(2, 32 * NUM_EPI_WARPS);  // every thread is done with the slot
-                    if (et == 0) ptx::mbar_arrive(empty_bar + 8 * sstage);
-                }
-                gstep += p.k1_blocks + static_cast<long long>((c_hi - c_lo + p.bn2 - 1) / p.bn2) * k2b;
-                ptx::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(zready_bar);
-            } else {   // ---- Z: TMEM -> bf16 (RNE) -> swizzled K-major smem, this warp's half of the columns
+            {   // ---- Z: TMEM -> bf16 (RNE) -> swizzled K-major smem, this warp's half of the columns
                 const uint32_t b = use & 1;
                 ptx::mbar_wait(tfull_bar + 8 * b, (use >> 1) & 1);
                 ptx::tc_fence_after();

@@ -38,6 +38,14 @@ constexpr int MAX_BRES = 48;       // max resident B k-blocks (one mbarrier each
 
 enum Kind : int { KIND_GEMM = 0, KIND_MONARCH_PROJ = 1, KIND_BLAST_PROJ = 2 };
 
+// Debug switches that skip kernel stages (timing experiments only; the results are then wrong).
+// Compiled in only with -DBLR_DEBUG_KNOBS; release builds ignore KParams::dbg entirely.
+#ifdef BLR_DEBUG_KNOBS
+#define BLR_DBG_ON(p, bit) (((p).dbg & (bit)) != 0)
+#else
+#define BLR_DBG_ON(p, bit) false
+#endif
+
 struct KParams {
     // ---- tiling
     int n_tok;        // M extent (tokens)
@@ -84,13 +92,14 @@ struct KParams {
     int r;                 // BLAST: rank
     const __nv_bfloat16* S;  // BLAST: S [b1][b2][r]
     unsigned long long* trace;  // debug: per-CTA %globaltimer stamps [grid][64] (nullptr = off)
-    int dbg;                    // debug bits (0 in production): 1 skip bulk stores, 2 skip staging,
+    int first;                  // 1: first launch of an API call (see the PDL note in the kernel)
+    int dbg;                    // debug bits (BLR_DEBUG_KNOBS builds only): 1 skip bulk stores, 2 skip staging,
                                 //   4 skip the whole GEMM epilogue, 8 skip MMAs, 16 plain-arrive slot release (PAIR 1),
                                 //   32 no accumulator hand-off, 64 no resident weight loads
 };
 
 struct SmemLayout {
-    uint32_t a_off, b_off, c_off, s_off, bar_off, tab_off, total;
+    uint32_t a_off, b_off, c_off, s_off, bar_off, tab_off, zero_off, total;
 };
 // Per-CTA tile table: the coordinates of the CTA's first TILE_TAB tiles, computed once by all
 // threads in the prologue, so the single-thread producer / MMA loops and the epilogue do no
@@ -115,7 +124,10 @@ __host__ __device__ inline SmemLayout smem_layout(const KParams& p) {
     if (p.S != nullptr) s_bytes = p.b1 * ((p.b2 + 7) / 8 * 8) * p.BN * 4;  // k rows zero-padded to 8
     L.bar_off = (L.s_off + s_bytes + 15) & ~15u;
     L.tab_off = L.bar_off + 8 * (2 * MAX_STAGES + 6 + MAX_BRES) + 16;
-    L.total = L.tab_off + TILE_TAB * 8;
+    // tile-blocked A whose K is an odd number of 8-wide panels: a 2-KB zero panel above everything
+    // else stands in for the missing half of the last K = 16 step (see the MMA issuer)
+    L.zero_off = (L.tab_off + TILE_TAB * 8 + 127) & ~127u;
+    L.total = L.zero_off + ((p.a_blocked && (p.a_nchunks & 1)) ? 2048u : 0u);
     return L;
 }
 
@@ -305,6 +317,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t tile_tab = sbase + L.tab_off;  // explicit shared-window addressing (see s_tile)
     for (int e = threadIdx.x; e < ntiles && e < TILE_TAB; e += NUM_THREADS)
         ptx::st_shared_v2u32(tile_tab + 8u * e, tile_pack(tile_coord(p, tile_at(p, titer, e))));
+    if (p.a_blocked && (p.a_nchunks & 1)) {  // the zero panel (generic stores -> async proxy)
+        for (uint32_t o = threadIdx.x * 16u; o < 2048u; o += NUM_THREADS * 16u)
+            ptx::st_shared_v4(sbase + L.zero_off + o, make_uint4(0, 0, 0, 0));
+        ptx::fence_async_smem();
+    }
     if (trace && threadIdx.x == 64 && KIND != KIND_BLAST_PROJ) trace[15] = clock64();
     ptx::tc_fence_before();
     __syncthreads();
@@ -315,9 +332,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     if (trace && threadIdx.x == 0) trace[1] = clock64();
     // Programmatic dependent launch: everything above overlapped the previous kernel's tail.
     // Roles that read the previous kernel's output (producer: A) or write outputs it may still
-    // read (epilogue) call griddep_wait() first; the producer prefetches the resident weight
-    // slice -- never written by a previous kernel -- before waiting.
-    ptx::griddep_launch_dependents();
+    // read (epilogue) call griddep_wait() first.  Weights are never written by this library, so
+    // a later launch of the same API call prefetches its resident weight slice before waiting.
+    // The FIRST launch of a call (p.first) may follow a caller kernel that wrote the weights: it
+    // waits before loading anything and lets the next grid start only after that wait, so by the
+    // time any later launch of the call starts, all work enqueued before the call has completed.
+    if (!p.first) ptx::griddep_launch_dependents();
 
     if (warp == 0) {
         // ===================================================== TMA producer =================
@@ -341,12 +361,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 else ptx::tma_load_4d(dst, m, bar, c0, c1, c2, c3);
             };
             const int n_steps = (p.k_blocks + p.kbox - 1) / p.kbox;
-            const int kbr = (p.dbg & 64) ? 0 : kb_resident(p);  // dbg 64: no weight loads
+            const int kbr = BLR_DBG_ON(p, 64) ? 0 : kb_resident(p);  // dbg 64: no weight loads
+            if (p.first) {
+                ptx::griddep_wait();
+                ptx::griddep_launch_dependents();
+            }
             int stage = 0;
             uint32_t phase = 0;
             int cur_slice = -1;
             uint32_t nslices = 0;
-            bool waited = false;
+            bool waited = p.first != 0;
             int nstep_tr = 0;
             for (int it = 0; it < ntiles; ++it) {
                 const TileCoord tc = tile_get(p, titer, tile_tab, it);
@@ -462,7 +486,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const uint32_t a_blk = BM * BK * 2;
             const int n_steps = (p.k_blocks + p.kbox - 1) / p.kbox;
             const int kbr = kb_resident(p);
-            const bool wait_b = p.b_resident && !(p.dbg & 64);
+            const bool wait_b = p.b_resident && !BLR_DBG_ON(p, 64);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -478,7 +502,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     ++nslices;
                     fresh = true;
                 }
-                if (!(p.dbg & 32)) ptx::mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
+                if (!BLR_DBG_ON(p, 32)) ptx::mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
                 ptx::tc_fence_after();
                 for (int sub = 0; sub < p.n_sub; ++sub) {
                     const uint32_t d_tmem = tmem_base + acc * acc_stride + sub * p.BN;
@@ -503,16 +527,33 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 const uint32_t a_off = stage * (a_blk * p.kbox) + j * a_blk;
                                 const uint32_t b_off = p.b_resident ? bkb * p.b_stage_bytes
                                                                     : stage * (p.b_stage_bytes * p.kbox) + j * p.b_stage_bytes;
+                                // tile-blocked A: the box of a K block that runs past K also holds the
+                                // NEXT token tile's panels; only the K = 16 steps over valid panels
+                                // are issued (a half-valid last step takes its second core matrix
+                                // from the zero panel), so no other token's value -- NaN or Inf
+                                // included -- enters this tile's sums (row independence)
+                                int n16 = BK / UMMA_K;
+                                bool half_last = false;
+                                if (p.a_blocked) {
+                                    const int vp = min(8, max(0, p.a_nchunks - kb * 8));  // valid panels
+                                    n16 = (vp + 1) >> 1;
+                                    half_last = (vp & 1) != 0;
+                                }
 #pragma unroll
                                 for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-                                    const uint64_t ad = ptx::desc_make(a_lo0 + ((a_off + kk * a_kstep) >> 4), a_hi);
+                                    if (kk >= n16) break;
+                                    uint64_t ad = ptx::desc_make(a_lo0 + ((a_off + kk * a_kstep) >> 4), a_hi);
+                                    if (half_last && kk == n16 - 1) {
+                                        const uint32_t pa = a_base + a_off + kk * a_kstep;
+                                        ad = ptx::smem_desc(pa, sbase + L.zero_off - pa, 128, 0);
+                                    }
                                     const uint64_t bd = ptx::desc_make(b_lo0 + ((b_off + kk * p.b_kstep) >> 4), b_hi);
-                                    if (p.dbg & 8) continue;  // debug: skip the MMA itself
+                                    if (BLR_DBG_ON(p, 8)) continue;  // debug: skip the MMA itself
                                     if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
                                     else ptx::mma_bf16(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
                                 }
                             }
-                            if (p.dbg & 16) ptx::mbar_arrive(empty_bar + 8 * stage);  // debug: plain release
+                            if (BLR_DBG_ON(p, 16)) ptx::mbar_arrive(empty_bar + 8 * stage);  // debug: plain release
                             else commit(empty_bar + 8 * stage);  // frees the smem slot (both CTAs of a pair)
                         }
                         __syncwarp();
@@ -548,7 +589,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t acc_phase = 0;
         uint32_t nstore = 0;  // staged chunks written by this warp (buffer rotation)
         ptx::griddep_wait();  // our stores must not overtake the previous kernel's reads
-        for (int it = 0; !(p.dbg & 32) && it < ntiles; ++it) {
+        for (int it = 0; !BLR_DBG_ON(p, 32) && it < ntiles; ++it) {
             const TileCoord tc = tile_get(p, titer, tile_tab, it);
             const int m0 = (tc.m_blk * PAIR + static_cast<int>(crank)) * BM;
             const int row0 = m0 + quarter * 32;
@@ -647,19 +688,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     }
                 }
             } else {
-                const int nvalid = (p.dbg & 4) ? 0 : min(p.BN, p.N - n0);  // dbg 4: empty epilogue
+                const int nvalid = BLR_DBG_ON(p, 4) ? 0 : min(p.BN, p.N - n0);  // dbg 4: empty epilogue
                 const int parts = p.out_lo_off > 0 ? 2 : 1;
                 // column chunks of CW elements; chunk j of this warp starts at col = (half + 2 j) * CW
                 const int CW = p.c_box_w;
                 const uint32_t row_bytes = CW * 2;
                 const uint32_t buf_bytes = 32 * row_bytes;
                 for (int c0 = half * CW; c0 < nvalid; c0 += 2 * CW) {
-                    // TMEM -> registers: CW fp32 columns of this warp's 32 rows (CW <= 64, mult. of 8)
+                    // TMEM -> registers: CW fp32 columns of this warp's 32 rows (mult. of 8; CW <= 64
+                    // except for the unswizzled whole-r' Monarch chunks, staged 64 columns at a time)
                     float fv[64];
+                    if (OUTF == 2 || CW <= 64) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (j * 8 < CW) ptx::tmem_ld_x8(tbase + c0 + j * 8, *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
-                    ptx::tmem_wait_ld();
+                        for (int j = 0; j < 8; ++j)
+                            if (j * 8 < CW) ptx::tmem_ld_x8(tbase + c0 + j * 8, *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
+                        ptx::tmem_wait_ld();
+                    }
                     if constexpr (OUTF == 2) {
                         // tile-blocked fp16 output [g][T][N/8][128][8]: the four warps of this column
                         // half (one per TMEM lane quarter) stage the chunk's 128 rows together and one
@@ -688,7 +732,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         }
                         ptx::fence_async_smem();
                         ptx::named_bar_sync(2 + half, 128);
-                        if (iss && !(p.dbg & 1)) {
+                        if (iss && !BLR_DBG_ON(p, 1)) {
                             // tile-blocked [g][T][N/8][128][8]: this chunk's panels of tile T are
                             // contiguous -> one bulk copy (rows >= n_tok are zeros: A was OOB-filled)
                             const int cc = (n0 + c0) >> 3;
@@ -706,16 +750,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             else ptx::bulk_wait_read<0>();
                         }
                         __syncwarp();
+                        for (int h0 = 0; h0 < CW; h0 += 64) {
+                            if (CW > 64) {  // wide chunk: the next <= 64 columns
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            if (j * 8 < CW && !(p.dbg & 2)) {
-                                stage_row8<OUTF>(buf, lane, j, row_bytes, p.c_swz,
+                                for (int j = 0; j < 8; ++j)
+                                    if (h0 + j * 8 < CW)
+                                        ptx::tmem_ld_x8(tbase + c0 + h0 + j * 8, *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
+                                ptx::tmem_wait_ld();
+                            }
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                if (h0 + j * 8 < CW && !BLR_DBG_ON(p, 2)) {
+                                    stage_row8<OUTF>(buf, lane, h0 / 8 + j, row_bytes, p.c_swz,
                                                      *reinterpret_cast<const float(*)[8]>(&fv[j * 8]), part);
+                                }
                             }
                         }
                         ptx::fence_async_smem();
                         __syncwarp();
-                        if (lane == 0 && !(p.dbg & 1)) {
+                        if (lane == 0 && !BLR_DBG_ON(p, 1)) {
                             if constexpr (KIND == KIND_GEMM) {
                                 // out (N, comp, groups, rows): element (c, part, g, t); blocked
                                 // out (8, rows, N/8, groups): element (c % 8, t, c / 8, g)

@@ -307,9 +307,12 @@ __host__ __device__ __forceinline__ uint32_t idesc_bf16(uint32_t M, uint32_t N, 
            ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// fp16 pair, RNE with saturation: |v| > 65504 becomes +-65504 instead of +-Inf, NaN stays NaN
+// (the BLAST split path's fp16 Z, R13: a finite input never turns into Inf there).
 __device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {
-    __half2 h = __floats2half2_rn(a, b);  // cvt.rn.f16x2.f32 (RNE)
-    return *reinterpret_cast<uint32_t*>(&h);
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %2, %1;" : "=r"(r) : "f"(a), "f"(b));
+    return r;
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // cvt.rn.bf16x2.f32 (RNE)

@@ -125,3 +125,20 @@ def test_monarch_local_factors_select_the_block_rows():
             part = orc.monarch_forward(X.numpy(), Vl.numpy(), Ul.numpy(), b1, k1 - k0, layout)
             assert abs(part - full[:, k0 * qd:k1 * qd]).max() < 1e-12, (layout, k0, k1)
 
+
+
+def test_bench_gpus2_self_launch_dry_run():
+    """`python bench.py --gpus 2` starts two ranks itself (torch.distributed.run, 127.0.0.1) and
+    strong-shards C4's 65,536 tokens contiguously (8,192 per GPU at N = 8); the --dry-run
+    plumbing pass runs the rank/shard logic over gloo without touching a GPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["scaling"] == "strong"
+    assert line["config"]["shards"] == [[0, 32768], [32768, 65536]]
+    assert [bdist.shard_rows(65536, r, 8) for r in range(8)] == [(8192 * r, 8192 * (r + 1)) for r in range(8)]
