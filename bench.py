@@ -284,7 +284,7 @@ class Arm:
             return blr.lowrank_matmul(h, *f, out=out, workspace=ws)
         if L.method == "monarch":
             return blr.monarch_matmul(h, *f, L.b1, L.b2, out=out, workspace=ws)
-        return blr.blast_matmul(h, *f, out=out, workspace=ws)
+        return blr.blast_matmul(h, *f, out=out, workspace=ws, fp8_intermediate=self.w.fp8z)
 
     def step(self):
         for ci, chain in enumerate(self.chains):
@@ -406,7 +406,7 @@ def e2e_run(arm, flush, stream, K, dev, ws):
             return blr.lowrank_matmul(h, *f, out=out)
         if L.method == "monarch":
             return blr.monarch_matmul(h, *f, L.b1, L.b2, out=out)
-        return blr.blast_matmul(h, *f, out=out)
+        return blr.blast_matmul(h, *f, out=out, fp8_intermediate=arm.w.fp8z)
 
     def one():
         ev_start.record(stream)
@@ -564,7 +564,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
-    ap.add_argument("--variants", default="C4M,C4X", help="comma-separated extra workloads (N = 1 only)")
+    ap.add_argument("--variants", default="C4M,C4X,C4F8", help="comma-separated extra workloads (N = 1 only)")
     ap.add_argument("--eager", action="store_true", help="launch every step from the host (no CUDA graph)")
     ap.add_argument("--flush", default="write+read", choices=["write+read", "write"],
                     help="L2 flush between timed steps (see L2Flush)")

@@ -80,7 +80,9 @@ typedef enum {
 /* Order of Monarch output columns (PAPER.md L45 footnote, L219-220). */
 typedef enum {
     BLR_OUT_CANONICAL = 0,  /* Y[t, k*q + c]  (PAPER.md L53 Y_k blocks side by side)          */
-    BLR_OUT_TRANSPOSED = 1  /* Y[t, c*b2 + k] ("transposed" permutation) -- not yet supported */
+    BLR_OUT_TRANSPOSED = 1  /* Y[t, c*b2 + k]: the order the paper's (3) leaves in place (PAPER.md
+                               L219-220) -- the next static weight's rows are pre-permuted instead
+                               (blr_transposed_row_perm) */
 } blr_out_order;
 
 typedef void* blr_stream_t; /* a cudaStream_t */
@@ -102,7 +104,10 @@ size_t blr_lowrank_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, in
  *                         V_{l,k}[a, rho] = V[l, m(rho,k), a]
  *   U [b2, q, b1*r_blk]   inner dimension "contiguous along r' then b1",
  *                         U_{l,k}[rho, c] = U[k, c, l*r_blk + rho]
- *   Y [n_tok, d_out]      out_order must be BLR_OUT_CANONICAL.
+ *   Y [n_tok, d_out]      column k*q + c (BLR_OUT_CANONICAL) or c*b2 + k (BLR_OUT_TRANSPOSED)
+ *                         holds output block k, column c.  The canonical order costs nothing here
+ *                         (it is the store coordinate); the transposed order is written with
+ *                         strided 2-byte stores (no TMA box has a 2-byte innermost extent).
  *   The r'<->b2 and b2<->b1 permutations are folded into the kernel's TMA
  *   addressing; V is read in place in either layout (no re-layout pass).
  *   Workspace: the intermediate Z' [b2][n_tok][b1*r_blk] (bf16; hi|lo pair when b1*r' < 128).
@@ -127,6 +132,33 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
                             void* Y, void* workspace, size_t ws_bytes, blr_stream_t stream);
 size_t blr_blast_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
                                 int64_t r);
+
+/*
+ * BLAST layer with an FP8 first-stage intermediate (the paper's proposed
+ * "intermediate activation quantization").  Same arguments, workspace and errors
+ * as blr_blast_matmul.  On the split path (b1*r > 512 and r >= 128) Z_l = X_l V_l is stored as
+ * OCP e4m3 (RNE, saturating at +-448, NaN stays NaN) instead of fp16 -- half the intermediate
+ * bytes of the first round trip; it is widened exactly to fp16 for the tensor-core S2, and Z''
+ * (bf16) and Y are as in blr_blast_matmul.  Every other path is identical to blr_blast_matmul.
+ * ACCURACY CONTRACT: an e4m3 rounding (unit roundoff 2^-4) of every Z element
+ * gives a relative error of ~0.027 rms (<= 0.036 for uniformly spread relative errors) -- outside
+ * north_star's bound.  This entry point guarantees, on unit-variance inputs with |X_l V_l| <= 448,
+ * relative Frobenius error <= 0.04 and per element |err| <= 0.2 (1 + |ref|).
+ */
+blr_status blr_blast_matmul_fp8z(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1,
+                                 int64_t b2, int64_t r, const void* V, const void* S, const void* U,
+                                 void* Y, void* workspace, size_t ws_bytes, blr_stream_t stream);
+
+/*
+ * Row permutation for chaining a BLR_OUT_TRANSPOSED Monarch layer into the next layer without a
+ * permutation pass (optimization (3)): fills the HOST array perm[b2*q] with
+ * perm[c*b2 + k] = k*q + c.  If W is the next layer's weight (rows indexed by the canonical input
+ * column), W'[j] = W[perm[j]] satisfies  Y_transposed W' = Y_canonical W.  A weight whose rows are
+ * not block-structured (low rank V, dense, BLAST/Monarch with b1 = 1) keeps its format.  Pure index
+ * arithmetic on the host (no device access).  BLR_ERR_SHAPE if b2 or q <= 0, BLR_ERR_NULL if perm
+ * is NULL.
+ */
+blr_status blr_transposed_row_perm(int64_t b2, int64_t q, int64_t* perm);
 
 /* Human-readable name of a status code (static storage, never NULL). */
 const char* blr_status_string(blr_status s);

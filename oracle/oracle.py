@@ -138,6 +138,21 @@ def monarch_forward(X, V, U, b1: int, b2: int, layout: int = B2_FASTEST) -> np.n
     return Y
 
 
+def monarch_forward_transposed(X, V, U, b1: int, b2: int, layout: int = B2_FASTEST) -> np.ndarray:
+    """The same product in the "transposed" output order the paper's optimization (3) leaves in
+    place (PAPER.md L45 footnote, L219-220): output block k, column c lands at Y[t, c*b2 + k]
+    instead of Y[t, k*q + c], i.e. the (b2, q) column grid of the canonical output read
+    column-major.  Written out element by element from that definition."""
+    Yc = monarch_forward(X, V, U, b1, b2, layout)
+    n, o = Yc.shape
+    q = o // b2
+    Yt = np.empty_like(Yc)
+    for k in range(b2):
+        for c in range(q):
+            Yt[:, c * b2 + k] = Yc[:, k * q + c]
+    return Yt
+
+
 # ---------------------------------------------------------------- BLAST ------------------------
 def _blast_dims(V, S, U):
     V, S, U = _f64(V), _f64(S), _f64(U)

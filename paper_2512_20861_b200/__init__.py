@@ -19,11 +19,13 @@ import torch
 from .build import LIB_PATH, build  # noqa: F401
 
 __all__ = ["load", "lowrank_matmul", "monarch_matmul", "blast_matmul", "BLRError",
-           "B2_FASTEST", "RPRIME_FASTEST", "last_launch_count", "lib_path"]
+           "B2_FASTEST", "RPRIME_FASTEST", "OUT_CANONICAL", "OUT_TRANSPOSED", "last_launch_count",
+           "lib_path", "transposed_row_perm", "permute_rows_for_transposed_input"]
 
 B2_FASTEST = 0       # BLR_MON_V_B2_FASTEST   (original layout)
 RPRIME_FASTEST = 1   # BLR_MON_V_RPRIME_FASTEST (after re-layout (1))
-OUT_CANONICAL = 0
+OUT_CANONICAL = 0    # BLR_OUT_CANONICAL   Y[t, k q + c]
+OUT_TRANSPOSED = 1   # BLR_OUT_TRANSPOSED  Y[t, c b2 + k]
 
 _lib = None
 
@@ -51,7 +53,8 @@ def load():
     lib.blr_monarch_matmul.argtypes = [vp, i64, i64, i64, i64, i64, i64, vp, vp, ctypes.c_int,
                                        ctypes.c_int, vp, vp, sz, vp]
     lib.blr_blast_matmul.argtypes = [vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp]
-    for fn in ("blr_lowrank_matmul", "blr_monarch_matmul", "blr_blast_matmul"):
+    lib.blr_blast_matmul_fp8z.argtypes = lib.blr_blast_matmul.argtypes
+    for fn in ("blr_lowrank_matmul", "blr_monarch_matmul", "blr_blast_matmul", "blr_blast_matmul_fp8z"):
         getattr(lib, fn).restype = ctypes.c_int
     lib.blr_lowrank_workspace_size.argtypes = [i64, i64, i64, i64]
     lib.blr_monarch_workspace_size.argtypes = [i64, i64, i64, i64, i64, i64]
@@ -65,6 +68,8 @@ def load():
     lib.blr_profile_begin.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.blr_profile_begin.restype = None
     lib.blr_profile_end.restype = ctypes.c_int
+    lib.blr_transposed_row_perm.argtypes = [i64, i64, ctypes.POINTER(ctypes.c_int64)]
+    lib.blr_transposed_row_perm.restype = ctypes.c_int
     _lib = lib
     return lib
 
@@ -122,9 +127,27 @@ def lowrank_matmul(X: torch.Tensor, V: torch.Tensor, U: torch.Tensor, out=None, 
     return Y
 
 
+def transposed_row_perm(b2: int, q: int) -> torch.Tensor:
+    """perm[c*b2 + k] = k*q + c (blr_transposed_row_perm): the canonical input column of each
+    position of a BLR_OUT_TRANSPOSED Monarch output."""
+    perm = torch.empty(b2 * q, dtype=torch.int64)
+    _check("blr_transposed_row_perm",
+           load().blr_transposed_row_perm(b2, q, ctypes.cast(perm.data_ptr(), ctypes.POINTER(ctypes.c_int64))))
+    return perm
+
+
+def permute_rows_for_transposed_input(W: torch.Tensor, b2: int, q: int) -> torch.Tensor:
+    """The next layer's static weight (rows = input features) re-laid out once, offline, so it
+    consumes a BLR_OUT_TRANSPOSED Monarch output directly (optimization (3)):
+    W'[j] = W[perm[j]]."""
+    perm = transposed_row_perm(b2, q).to(W.device)
+    return W.index_select(0, perm).contiguous()
+
+
 def monarch_matmul(X: torch.Tensor, V: torch.Tensor, U: torch.Tensor, b1: int, b2: int,
-                   v_layout: int = B2_FASTEST, out=None, workspace=None):
-    """Monarch Y_k = sum_l X_l V_{l,k} U_{l,k}; V [b1, r'b2, p], U [b2, q, b1 r']."""
+                   v_layout: int = B2_FASTEST, out=None, workspace=None, out_order: int = OUT_CANONICAL):
+    """Monarch Y_k = sum_l X_l V_{l,k} U_{l,k}; V [b1, r'b2, p], U [b2, q, b1 r'].
+    out_order OUT_TRANSPOSED writes Y[t, c*b2 + k] instead of Y[t, k*q + c]."""
     lib = load()
     n, i = X.shape
     if V.dim() != 3 or U.dim() != 3 or V.shape[0] != b1 or U.shape[0] != b2:
@@ -138,15 +161,16 @@ def monarch_matmul(X: torch.Tensor, V: torch.Tensor, U: torch.Tensor, b1: int, b
     ws = _ws(X, lib.blr_monarch_workspace_size(n, i, o, b1, b2, rp), workspace)
     with torch.cuda.device(X.device):
         code = lib.blr_monarch_matmul(_dev_bf16("X", X), n, i, o, b1, b2, rp, _dev_bf16("V", V),
-                                      _dev_bf16("U", U), int(v_layout), OUT_CANONICAL, _dev_bf16("out", Y),
+                                      _dev_bf16("U", U), int(v_layout), int(out_order), _dev_bf16("out", Y),
                                       ws.data_ptr(), ws.numel() * ws.element_size(), _stream_ptr(X.device))
     _check("blr_monarch_matmul", code)
     return Y
 
 
 def blast_matmul(X: torch.Tensor, V: torch.Tensor, S: torch.Tensor, U: torch.Tensor, out=None,
-                 workspace=None):
-    """BLAST Y_k = (sum_l (X_l V_l) S_{l,k}) U_k; V [b1,p,r], S [b1,b2,r], U [b2,r,q]."""
+                 workspace=None, fp8_intermediate: bool = False):
+    """BLAST Y_k = (sum_l (X_l V_l) S_{l,k}) U_k; V [b1,p,r], S [b1,b2,r], U [b2,r,q].
+    fp8_intermediate=True calls blr_blast_matmul_fp8z (e4m3 Z; its own accuracy contract, blr.h)."""
     lib = load()
     n, i = X.shape
     b1, p, r = V.shape
@@ -158,8 +182,9 @@ def blast_matmul(X: torch.Tensor, V: torch.Tensor, S: torch.Tensor, U: torch.Ten
     Y = _out(X, n, o, out)
     ws = _ws(X, lib.blr_blast_workspace_size(n, i, o, b1, b2, r), workspace)
     with torch.cuda.device(X.device):
-        code = lib.blr_blast_matmul(_dev_bf16("X", X), n, i, o, b1, b2, r, _dev_bf16("V", V),
-                                    _dev_bf16("S", S), _dev_bf16("U", U), _dev_bf16("out", Y),
-                                    ws.data_ptr(), ws.numel() * ws.element_size(), _stream_ptr(X.device))
-    _check("blr_blast_matmul", code)
+        fn = lib.blr_blast_matmul_fp8z if fp8_intermediate else lib.blr_blast_matmul
+        code = fn(_dev_bf16("X", X), n, i, o, b1, b2, r, _dev_bf16("V", V),
+                  _dev_bf16("S", S), _dev_bf16("U", U), _dev_bf16("out", Y),
+                  ws.data_ptr(), ws.numel() * ws.element_size(), _stream_ptr(X.device))
+    _check("blr_blast_matmul_fp8z" if fp8_intermediate else "blr_blast_matmul", code)
     return Y

@@ -86,6 +86,7 @@ class Workload:
     desc: str
     n: int                      # tokens in one step (batch x seq)
     layers: tuple               # Layer objects run back to back in one step
+    fp8z: bool = False          # BLAST layers through blr_blast_matmul_fp8z (e4m3 Z)
 
 
 # BASELINE.json configs (SURVEY.md §8 labels C1..C5).
@@ -122,6 +123,11 @@ C4_2X = Workload("C4X", "Llama-7B MLP (4096<->11008) at >=2x compression: BLAST 
                   Layer("Llama-7B", "down_proj", 11008, 4096, "monarch", 1408, 16)))
 
 
+# C4 through the FP8-intermediate entry point (its own accuracy contract, include/blr.h)
+C4_FP8 = Workload("C4F8", "Llama-7B MLP (4096<->11008) BLAST prefill seq 8192 x batch 8, e4m3 first-stage intermediate",
+                  8 * 8192, C4.layers, fp8z=True)
+
+
 def c5(images: int) -> Workload:
     """ViT-B layers (197 tokens per image, Table 3): qkv, fc1, fc2 in Monarch
     (r = 128, b = 4) and BLAST (r = 128, b = 3)."""
@@ -138,7 +144,7 @@ def c5_dit(images: int) -> Workload:
 
 C5_IMAGES = (1, 8, 64, 256)   # BASELINE.json configs[4]: batch sweep 1-256 images
 
-WORKLOADS = {w.key: w for w in (C1, C2, C3, C4, C4_MONARCH, C4_2X)}
+WORKLOADS = {w.key: w for w in (C1, C2, C3, C4, C4_MONARCH, C4_2X, C4_FP8)}
 for _im in C5_IMAGES:
     WORKLOADS[f"C5V-{_im}"] = c5(_im)
     WORKLOADS[f"C5D-{_im}"] = c5_dit(_im)

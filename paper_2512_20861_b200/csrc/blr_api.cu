@@ -31,7 +31,7 @@ struct DevInfo {
 std::mutex g_mu;
 DevInfo g_dev[64];
 PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
-bool g_attr_set[16][64] = {};  // kernel attribute set, per (kernel variant, device)
+bool g_attr_set[32][64] = {};  // kernel attribute set, per (kernel variant, device)
 thread_local int t_last_launches = 0;
 thread_local void** t_prof_events = nullptr;
 thread_local int t_prof_cap = 0;
@@ -69,6 +69,7 @@ bool encode(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims, con
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
     const CUtensorMapDataType t = dt == 1   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
                                   : dt == 2 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                  : dt == 3 ? CU_TENSOR_MAP_DATA_TYPE_UINT8   // e4m3 bytes
                                             : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
     CUresult r = g_encode(m, t, rank, const_cast<void*>(ptr),
                           reinterpret_cast<const cuuint64_t*>(dims), reinterpret_cast<const cuuint64_t*>(strides),
@@ -121,30 +122,36 @@ int chunk_width(int n) {
     return cw;
 }
 
-// Fill B-operand staging parameters.
-void set_b_staging(KParams& p, bool mn_major) {
+// Fill B-operand staging parameters for p.BN columns of this CTA (one half of the tile when
+// p.n_mma == 2).  allow_sw64: MN-major columns may be staged in 32-column 64-B-swizzled boxes
+// when that loads fewer columns than 64-column boxes (e.g. 88 -> 96 instead of 128).
+void set_b_staging(KParams& p, bool mn_major, bool allow_sw64 = false) {
+    if (p.n_mma < 1) p.n_mma = 1;
     p.b_mn_major = mn_major ? 1 : 0;
     if (mn_major) {
         // B stored [K][N]: boxes of 64 N-elements (128 B rows) x BK K-rows, 128-B swizzle.
         // UMMA MN-major SW128 canonical layout: 64-element MN atoms LBO apart, 8-row K groups
-        // SBO = 1024 B apart; +16 K-rows = +2048 B per UMMA_K step.
-        p.b_box_n = 64;
-        p.b_boxes = static_cast<int>(cdiv(p.BN, 64));
-        p.b_stage_bytes = static_cast<uint32_t>(p.b_boxes * 64 * blr::BK * 2);
-        p.b_lbo = 64 * 2 * blr::BK;
-        p.b_sbo = 1024;
-        p.b_layout = blr::ptx::LAYOUT_SW128;
-        p.b_kstep = 16 * 128;
+        // SBO = 1024 B apart; +16 K-rows = +2048 B per UMMA_K step.  (SW64: 32-element atoms,
+        // 512 B per 8 K rows, +1024 B per UMMA_K step.)
+        const bool sw64 = allow_sw64 && cdiv(p.BN, 32) * 32 < cdiv(p.BN, 64) * 64;
+        p.b_box_n = sw64 ? 32 : 64;
+        p.b_boxes = static_cast<int>(cdiv(p.BN, p.b_box_n));
+        p.b_half_bytes = static_cast<uint32_t>(p.b_boxes * p.b_box_n * blr::BK * 2);
+        p.b_lbo = p.b_box_n * 2 * blr::BK;
+        p.b_sbo = sw64 ? 512 : 1024;
+        p.b_layout = sw64 ? blr::ptx::LAYOUT_SW64 : blr::ptx::LAYOUT_SW128;
+        p.b_kstep = sw64 ? 16 * 64 : 16 * 128;
     } else {
         // B stored [N][K]: BN rows x 64 K-elements, K-major SW128 like A.
         p.b_box_n = p.BN;
         p.b_boxes = 1;
-        p.b_stage_bytes = static_cast<uint32_t>(rup(static_cast<int64_t>(p.BN) * blr::BK * 2, 1024));
+        p.b_half_bytes = static_cast<uint32_t>(rup(static_cast<int64_t>(p.BN) * blr::BK * 2, 1024));
         p.b_lbo = 16;
         p.b_sbo = 1024;
         p.b_layout = blr::ptx::LAYOUT_SW128;
         p.b_kstep = 32;
     }
+    p.b_stage_bytes = p.n_mma * p.b_half_bytes;
 }
 
 // Programmatic dependent launch between the library's kernels (BLR_NO_PDL=1 disables).
@@ -199,6 +206,11 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) 
         }
         if (best_score >= 0) {
             p = best;
+            // BLR_ORDER=1: streaming plans run the N blocks of one (token tile, group) back to back
+            // on one CTA (A re-read from L2 while hot).  Measured slower than round robin, where the
+            // CTAs sharing an A tile load it at the same time (C4 8.31 -> 8.37 ms, C4M 6.52 -> 6.80 ms)
+            const char* oe = getenv("BLR_ORDER");
+            p.nb_runs = (!resident && p.tiles_n >= 2 && oe && oe[0] == '1') ? 1 : 0;
             // slice ownership with lockstep token walks when every slice gets >= 1 CTA (unit)
             const int slices = p.groups * p.tiles_n;
             p.cps = 0;
@@ -236,7 +248,7 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     const int smem = static_cast<int>(L.total + SMEM_SLACK);
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        const int slot = OUTF ? 8 + OUTF + 2 * (PAIR - 1) : KIND + 3 * (PAIR - 1);
+        const int slot = OUTF ? 6 + 2 * (OUTF - 1) + (PAIR - 1) : KIND + 3 * (PAIR - 1);  // 0..11
         if (!g_attr_set[slot][dev]) {
             if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT) != cudaSuccess)
                 return BLR_ERR_CUDA;
@@ -249,10 +261,10 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     else if (p.b_resident) grid = std::min(units, p.groups * p.tiles_n) * PAIR;  // slice round-robin
     if (const char* pe = getenv("BLR_PLAN"); pe && pe[0] == '1')
         fprintf(stderr,
-                "[blr plan] kind=%d pair=%d grid=%d tiles=%dx%dx%d BN=%d kblk=%d kbox=%d stages=%d res=%d cps=%d "
-                "bufs=%d acc=%d cbox=%d smem=%d\n",
-                KIND, PAIR, grid, p.tiles_m, p.groups, p.tiles_n, p.BN, p.k_blocks, p.kbox, p.stages, p.b_resident,
-                p.cps, p.stage_bufs, p.acc_bufs, p.c_box_w, smem);
+                "[blr plan] kind=%d pair=%d grid=%d tiles=%dx%dx%d BN=%d mma=%d bbox=%d kblk=%d kbox=%d stages=%d res=%d "
+                "cps=%d bufs=%d acc=%d cbox=%d smem=%d\n",
+                KIND, PAIR, grid, p.tiles_m, p.groups, p.tiles_n, p.BN, p.n_mma, p.b_box_n, p.k_blocks, p.kbox, p.stages,
+                p.b_resident, p.cps, p.stage_bufs, p.acc_bufs, p.c_box_w, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(blr::NUM_THREADS);
@@ -337,26 +349,35 @@ int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int64_t groups, int sms
 
 struct OutMap {  // 4-D view (N, comp, groups, rows) of a GEMM phase's output
     void* ptr;
-    int f32;               // output type: 0 bf16, 2 fp16 (BLAST split-path Z)
+    int f32;               // output type: 0 bf16, 2 fp16 (BLAST split-path Z), 3 e4m3 (FP8 Z, row f4)
     int64_t comp;          // 1, or 2 for a compensated [hi | lo] intermediate
     int64_t comp_stride;   // elements between hi and lo
     int64_t group_stride;  // elements between groups
     int64_t row_stride;    // elements between rows
     int blocked = 0;       // 1: tile-blocked [g][T][N/8][128][8] (BLAST Z with the tensor-core S2)
+    int64_t col_stride = 0;  // > 0: element (t, g, c) at t*row_stride + g*group_stride + c*col_stride,
+                             //      stored directly (Monarch transposed output order)
 };
 
 // One plain GEMM phase: out[g](t, c) = sum_k A[g](t, k) B[g](k, c), K-major A.
 //   A map: a_gmid ? (K*comp, groups, rows) : (K*comp, rows, groups) with the given strides.
 //   comp == 2: A rows hold [hi | lo] (lo at column offset K) multiplying the same B rows.
 // Plan one GEMM phase for CTA-pair mode `pair` (1 or 2).  Returns false if nothing fits.
+// wide: a CTA-pair tile of up to 512 columns as two MMAs per K step (KParams::n_mma), single
+// accumulator buffer, streamed B only.
 bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok, int64_t K, int64_t groups,
-               int64_t N, bool b_mn_major, const OutMap& out, int comp) {
+               int64_t N, bool b_mn_major, const OutMap& out, int comp, bool wide = false) {
     p = KParams{};
     p.a_gmid = a_gmid;
     p.n_tok = static_cast<int>(n_tok);
     p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM * pair));
-    p.BN = choose_bn(N, K, p.tiles_m * groups, groups, d.sm_count / pair, pair);
-    if (pair == 2 && (p.BN / 2) % 8) p.BN = static_cast<int>(rup(p.BN, 32));
+    p.n_mma = wide ? 2 : 1;
+    if (wide) {  // N tiles of <= 512, halves multiples of 16 (per-CTA halves multiples of 8)
+        p.BN = static_cast<int>(rup(cdiv(N, cdiv(N, 512)), 32));
+    } else {
+        p.BN = choose_bn(N, K, p.tiles_m * groups, groups, d.sm_count / pair, pair);
+        if (pair == 2 && (p.BN / 2) % 8) p.BN = static_cast<int>(rup(p.BN, 32));
+    }
     p.N = static_cast<int>(N);
     p.tiles_n = static_cast<int>(cdiv(N, p.BN));
     p.groups = static_cast<int>(groups);
@@ -365,19 +386,21 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     p.k_blocks = p.kb_half * comp;
     p.a_lo_off = comp == 2 ? static_cast<int>(K) : 0;
     p.n_sub = 1;
-    // B staging describes this CTA's share: all BN columns, or half of them in a CTA pair
+    // B staging describes this CTA's share of one MMA's columns: all of them, or half in a CTA pair
     const int bn_full = p.BN;
-    p.BN = bn_full / pair;
-    set_b_staging(p, b_mn_major);
+    p.BN = bn_full / pair / p.n_mma;
+    set_b_staging(p, b_mn_major, wide);
     p.BN = bn_full;
     p.out_lo_off = out.comp == 2 ? out.comp_stride : 0;
     p.out_ptr = out.ptr;
     p.out_gstride = out.group_stride;
+    p.out_rs = out.row_stride;
+    p.out_cs = static_cast<int>(out.col_stride);
     const int esz = 2;
     p.c_box_w = chunk_width(p.BN);
     while (p.c_box_w * esz > 128) p.c_box_w /= 2;  // staged rows <= 128 B
     p.c_swz = out.blocked ? 0 : pick_swz(p.c_box_w * esz).mask;
-    return finish_plan(p, true, 32 * p.c_box_w * esz, d.sm_count / pair);
+    return finish_plan(p, !wide, 32 * p.c_box_w * esz, d.sm_count / pair);
 }
 
 // A planned GEMM phase: parameters and tensor maps, encoded before anything is launched (so a
@@ -386,10 +409,13 @@ struct GemmPrep {
     KParams p;
     CUtensorMap ta, tb, tc;
     int pair = 1;
-    int outf = 0;  // 0 bf16, 1 fp16, 2 fp16 tile-blocked
+    int outf = 0;  // 0 bf16, 1 fp16, 2 fp16 tile-blocked, 3 e4m3 tile-blocked
 };
 
 blr_status gemm_run(const GemmPrep& g, const DevInfo& d, int dev, cudaStream_t st) {
+    if (g.outf == 3)
+        return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 3>(g.ta, g.tb, g.tc, g.p, d, dev, st)
+                           : launch<blr::KIND_GEMM, 1, 3>(g.ta, g.tb, g.tc, g.p, d, dev, st);
     if (g.outf == 2)
         return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st)
                            : launch<blr::KIND_GEMM, 1, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st);
@@ -433,6 +459,17 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
         if (pair == 1 || !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp))
             return BLR_ERR_UNSUPPORTED;
     }
+    // wide pair tiles (two MMAs per K step, <= 512 columns, single accumulator): half the operand
+    // bytes per MAC of a 256-column pair tile for streamed, long-K, wide-N phases (C4 gate S3,
+    // down S1); BLR_WIDE=0/1 overrides
+    {
+        const char* we = getenv("BLR_WIDE");
+        const bool want = we ? we[0] == '1' : (pair == 2 && !p.b_resident && N >= 512 && K >= 512);
+        if (want && pair == 2 && out.col_stride == 0) {
+            KParams w;
+            if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, true)) p = w;
+        }
+    }
     const int esz = 2;
     const Swz cs = pick_swz(p.c_box_w * esz);
     p.a_blocked = a_blocked;
@@ -475,15 +512,26 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
     if (b_mn_major) {
         const uint64_t dims[3] = {static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(groups)};
         const uint64_t str[2] = {static_cast<uint64_t>(N) * 2, static_cast<uint64_t>(N * K) * 2};
-        const uint32_t box[3] = {64, blr::BK, 1};
-        if (!encode(&tb, B, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+        const uint32_t box[3] = {static_cast<uint32_t>(p.b_box_n), blr::BK, 1};
+        if (!encode(&tb, B, 3, dims, str, box, p.b_box_n == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
+            return BLR_ERR_CUDA;
     } else {
         const uint64_t dims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(groups)};
         const uint64_t str[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K * N) * 2};
-        const uint32_t box[3] = {blr::BK, static_cast<uint32_t>(p.BN / pair), 1};
+        const uint32_t box[3] = {blr::BK, static_cast<uint32_t>(p.BN / pair / p.n_mma), 1};
         if (!encode(&tb, B, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
     }
-    {
+    if (out.blocked) {
+        // tile-blocked output: the map is encoded below
+    } else if (out.col_stride > 0) {
+        // strided direct stores (transposed order): the kernel never uses the store map; encode a
+        // valid placeholder over the same rows
+        const uint64_t dims[4] = {static_cast<uint64_t>(N), 1, 1, static_cast<uint64_t>(n_tok)};
+        const uint64_t strb[3] = {static_cast<uint64_t>(N) * 2, static_cast<uint64_t>(N) * 2,
+                                  static_cast<uint64_t>(out.row_stride) * 2};
+        const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32};
+        if (!encode(&tc, out.ptr, 4, dims, strb, box, cs.mode, out.f32)) return BLR_ERR_CUDA;
+    } else {
         const uint64_t dims[4] = {static_cast<uint64_t>(N), static_cast<uint64_t>(out.comp),
                                   static_cast<uint64_t>(groups), static_cast<uint64_t>(n_tok)};
         const uint64_t es = static_cast<uint64_t>(esz);
@@ -497,14 +545,16 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
         // a chunk's panels of one tile are one tensor store box (64, 16, CW/8, 1); panels past N
         // fall outside dim 2 and are clipped (a 1-D bulk copy per chunk measured slower)
         p.o_tiles = static_cast<int>(cdiv(n_tok, blr::BM));
+        // (e4m3: 1-KB panels of 16 rows x 64 B)
+        const uint64_t eb = out.f32 == 3 ? 1 : 2;
         const uint64_t dims[4] = {64, 16, static_cast<uint64_t>(N / 8), static_cast<uint64_t>(groups) * p.o_tiles};
-        const uint64_t strb[3] = {128, 2048, static_cast<uint64_t>(N / 8) * 2048};
+        const uint64_t strb[3] = {64 * eb, 1024 * eb, static_cast<uint64_t>(N / 8) * 1024 * eb};
         const uint32_t box[4] = {64, 16, static_cast<uint32_t>(p.c_box_w / 8), 1};
         if (!encode(&tc, out.ptr, 4, dims, strb, box, CU_TENSOR_MAP_SWIZZLE_NONE, out.f32)) return BLR_ERR_CUDA;
     }
     // fp16 output (BLAST split-path Z) is a separate instantiation: the bf16 epilogue stays as is
     g.pair = pair;
-    g.outf = out.f32 == 2 ? (out.blocked ? 2 : 1) : 0;
+    g.outf = out.f32 == 3 ? 3 : out.f32 == 2 ? (out.blocked ? 2 : 1) : 0;
     return BLR_OK;
 }
 
@@ -594,11 +644,11 @@ blr_status fused_launch(const DevInfo& d, int dev, cudaStream_t st, blr::FParams
     const int smem = static_cast<int>(blr::fused_layout(p).total + SMEM_SLACK);
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        if (!g_attr_set[13][dev]) {
+        if (!g_attr_set[23][dev]) {
             if (cudaFuncSetAttribute(blr::blr_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT) !=
                 cudaSuccess)
                 return BLR_ERR_CUDA;
-            g_attr_set[13][dev] = true;
+            g_attr_set[23][dev] = true;
         }
     }
     const int grid = std::min(p.items, d.sm_count);
@@ -777,7 +827,8 @@ blr_status decode_mn(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, in
 // out[g][t][c] = sum_k A[g][t][k] B[g][c][k], B K-major (one warp per output column).
 blr_status decode_k(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int64_t a_gs, const void* B,
                     int64_t b_rs, int64_t b_gs, void* out, int out_bf16, int64_t o_rs, int64_t o_gs, int64_t n,
-                    int64_t K, int64_t N, int64_t groups, int col_map, int64_t mon_b2, int64_t mon_r) {
+                    int64_t K, int64_t N, int64_t groups, int col_map, int64_t mon_b2, int64_t mon_r,
+                    int64_t o_cs = 1) {
     blr::DecodeK d = {};
     d.A = A;
     d.a_f32 = a_f32;
@@ -796,6 +847,7 @@ blr_status decode_k(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int
     d.col_map = col_map;
     d.mon_b2 = static_cast<int>(mon_b2);
     d.mon_r = static_cast<int>(mon_r);
+    d.o_cs = o_cs;
     // enough blocks for the SMs, >= 64 columns per block (the A stage is re-read per block)
     int64_t cpb = std::max<int64_t>(64, rup(cdiv(N * groups, DECODE_TARGET_BLOCKS), 8));
     cpb = std::min<int64_t>(cpb, rup(N, 8));
@@ -835,7 +887,15 @@ const char* blr_status_string(blr_status s) {
     return "BLR_ERR_UNKNOWN";
 }
 
-const char* blr_version(void) { return "0.2.0"; }
+const char* blr_version(void) { return "0.3.0"; }
+
+blr_status blr_transposed_row_perm(int64_t b2, int64_t q, int64_t* perm) {
+    if (b2 <= 0 || q <= 0) return BLR_ERR_SHAPE;
+    if (!perm) return BLR_ERR_NULL;
+    for (int64_t c = 0; c < q; ++c)
+        for (int64_t k = 0; k < b2; ++k) perm[c * b2 + k] = k * q + c;  // transposed j = c b2 + k
+    return BLR_OK;
+}
 
 int blr_last_launch_count(void) { return t_last_launches; }
 
@@ -962,7 +1022,11 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     if (n_tok < 0 || d_in <= 0 || d_out <= 0 || b1 <= 0 || b2 <= 0 || r_blk <= 0) return BLR_ERR_SHAPE;
     if (d_in % b1 || d_out % b2) return BLR_ERR_SHAPE;
     if (v_layout != BLR_MON_V_B2_FASTEST && v_layout != BLR_MON_V_RPRIME_FASTEST) return BLR_ERR_SHAPE;
-    if (out_order != BLR_OUT_CANONICAL) return BLR_ERR_UNSUPPORTED;
+    if (out_order != BLR_OUT_CANONICAL && out_order != BLR_OUT_TRANSPOSED) return BLR_ERR_SHAPE;
+    // output block k, column c -> Y[t, k q + c] (canonical) or Y[t, c b2 + k] (the
+    // "transposed" order of PAPER.md L219-220, whose skipped permutation ③ pre-applies to the next
+    // static weight's rows; blr_transposed_row_index)
+    const bool ytr = out_order == BLR_OUT_TRANSPOSED;
     if (n_tok == 0) return BLR_OK;
     if (!X || !V || !U || !Y || !workspace) return BLR_ERR_NULL;
     const int64_t pdim = d_in / b1, qdim = d_out / b2, K2 = b1 * r_blk;
@@ -980,7 +1044,8 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         s = decode_k(st, X, 0, d_in, pdim, V, pdim, r_blk * b2 * pdim, zp, 0, K2, n_tok * K2, n_tok, pdim,
                      r_blk * b2, b1, v_layout == BLR_MON_V_B2_FASTEST ? 1 : 2, b2, r_blk);
         if (s != BLR_OK) return s;
-        return decode_k(st, zp, 1, K2, n_tok * K2, U, K2, qdim * K2, Y, 1, d_out, qdim, n_tok, K2, qdim, b2, 0, 1, 1);
+        return decode_k(st, zp, 1, K2, n_tok * K2, U, K2, qdim * K2, Y, 1, d_out, ytr ? 1 : qdim, n_tok, K2, qdim, b2,
+                        0, 1, 1, ytr ? b2 : 1);
     }
     if (fused_wanted(n_tok, K2, r_blk, false)) {  // one launch, Z'_k on chip (blr_fused.cuh)
         blr::FParams p = {};
@@ -993,6 +1058,11 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         p.g2 = static_cast<int>(b2);
         p.n2 = static_cast<int>(qdim);
         p.b2_mn = 0;
+        if (ytr) {
+            p.y = static_cast<__nv_bfloat16*>(Y);
+            p.y_rs = d_out;
+            p.y_cs = static_cast<int>(b2);
+        }
         CUtensorMap ta, tb1, tb2;
         if (!encode_x_blocked(&ta, X, n_tok, b1, pdim)) return BLR_ERR_CUDA;
         {   // V viewed 4-D (a, rho', k, l): box (64, r', 1, 1) = the r' rows m(rho, k) of block (l, k)
@@ -1103,8 +1173,9 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         // ---- phase 2: Y[t, k q + c] = sum_kk Z'[k][t][kk] U[k][c][kk]  (U is [N][K]: K-major B),
         //      planned before phase 1 is launched
         GemmPrep g2;
-        s = gemm_prepare(g2, d, workspace, 0, K2 * comp, n_tok * K2 * comp, n_tok, K2, b2, qdim, U, false,
-                         OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
+        OutMap ymap{Y, 0, 1, d_out, ytr ? 1 : qdim, d_out};
+        ymap.col_stride = ytr ? b2 : 0;
+        s = gemm_prepare(g2, d, workspace, 0, K2 * comp, n_tok * K2 * comp, n_tok, K2, b2, qdim, U, false, ymap, comp);
         if (s != BLR_OK) return s;
         s = pair == 2 ? launch<blr::KIND_MONARCH_PROJ, 2>(ta, tb, tc, p, d, dev, st)
                       : launch<blr::KIND_MONARCH_PROJ, 1>(ta, tb, tc, p, d, dev, st);
@@ -1113,9 +1184,13 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     }
 }
 
-blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
-                            int64_t r, const void* V, const void* S, const void* U, void* Y, void* workspace,
-                            size_t ws_bytes, blr_stream_t stream) {
+}  // extern "C"
+
+namespace {
+// fp8z: the split path stores Z_l as e4m3; elsewhere identical
+blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2, int64_t r,
+                      const void* V, const void* S, const void* U, void* Y, void* workspace, size_t ws_bytes,
+                      blr_stream_t stream, bool fp8z) {
     t_last_launches = 0;
     if (n_tok < 0 || d_in <= 0 || d_out <= 0 || b1 <= 0 || b2 <= 0 || r <= 0) return BLR_ERR_SHAPE;
     if (d_in % b1 || d_out % b2) return BLR_ERR_SHAPE;
@@ -1223,7 +1298,9 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
     void* zl = static_cast<char*>(workspace) + static_cast<size_t>(b2) * n_pad * r * 2 * comp;
     // S1: Z[l][t][rho] = (X_l V_l)[t, rho]  -- grouped GEMM over l (A = X viewed (p, b1, n));
     // tile-blocked Z for the tensor-core S2: [l][T][r/8][128][8], group stride n_pad * r
-    OutMap zmap{zl, 2, 1, r, s2_mma ? n_pad * r : n_tok * r, r};
+    // (FP8 mode: e4m3 bytes in the same layout; only with the tensor-core S2)
+    const bool z8 = fp8z && s2_mma;
+    OutMap zmap{zl, z8 ? 3 : 2, 1, r, s2_mma ? n_pad * r : n_tok * r, r};
     zmap.blocked = s2_mma ? 1 : 0;
     GemmPrep g1, g3;
     s = gemm_prepare(g1, d, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true, zmap, 1);
@@ -1238,15 +1315,16 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
     if (s2_mma) {
         // ---- S2 on the tensor cores (blast_s2_mma_kernel): tile-blocked fp16 Z [l][T][r/8][128][8]
         //      in, tile-blocked bf16 Z'' [k][T][r/8][128][8] out
-        const blr::S2MLayout sl = blr::s2m_layout(static_cast<int>(b1), static_cast<int>(b2));
         const char* oe = getenv("BLR_S2_ORDER");
         const int s2_order = oe ? atoi(oe) : 0;
         const int64_t items = cdiv(n_tok, 128) * (r / 8);
         // b2 <= 8: the half-register instantiation, two CTAs per SM when both fit in smem
         const char* se = getenv("BLR_S2_SMALL");
         const bool small = b2 <= 8 && !(se && se[0] == '0');
-        const int per_sm = (small && 2 * (sl.total + 1024 + 1024) <= 233472) ? 2 : 1;
-        auto s2fn = small ? blr::blast_s2_mma_kernel<8> : blr::blast_s2_mma_kernel<16>;
+        const blr::S2MLayout sl8 = blr::s2m_layout(static_cast<int>(b1), static_cast<int>(b2), z8);
+        const int per_sm = (small && 2 * (sl8.total + 1024 + 1024) <= 233472) ? 2 : 1;
+        auto s2fn = z8 ? (small ? blr::blast_s2_mma_kernel<8, true> : blr::blast_s2_mma_kernel<16, true>)
+                       : (small ? blr::blast_s2_mma_kernel<8> : blr::blast_s2_mma_kernel<16>);
         const char* pe2 = getenv("BLR_S2_PDL");
         const bool s2_pdl = pdl_enabled() && !(pe2 && pe2[0] == '0');
         CUtensorMap tmz, tmzpp;
@@ -1255,20 +1333,25 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
             const uint64_t dz[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b1)};
             const uint64_t sz[3] = {128, 2048, static_cast<uint64_t>(np) * 2048};
             const uint32_t bz[4] = {64, 16, 1, static_cast<uint32_t>(b1)};
-            if (!encode(&tmz, zl, 4, dz, sz, bz, CU_TENSOR_MAP_SWIZZLE_NONE, 2)) return BLR_ERR_CUDA;
+            const uint64_t sz8[3] = {64, 1024, static_cast<uint64_t>(np) * 1024};  // e4m3: 1-KB panels
+            if (!encode(&tmz, zl, 4, dz, z8 ? sz8 : sz, bz, CU_TENSOR_MAP_SWIZZLE_NONE, z8 ? 3 : 2)) return BLR_ERR_CUDA;
             const uint64_t dp[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b2)};
             const uint32_t bp[4] = {64, 16, 1, static_cast<uint32_t>(b2)};
             if (!encode(&tmzpp, zpp, 4, dp, sz, bp, CU_TENSOR_MAP_SWIZZLE_NONE)) return BLR_ERR_CUDA;
         }
         {
             std::lock_guard<std::mutex> lk(g_mu);
-            if (!g_attr_set[8][dev]) {
+            if (!g_attr_set[20][dev]) {
                 if (cudaFuncSetAttribute(blr::blast_s2_mma_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          232448) != cudaSuccess ||
                     cudaFuncSetAttribute(blr::blast_s2_mma_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         232448) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_mma_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         232448) != cudaSuccess ||
+                    cudaFuncSetAttribute(blr::blast_s2_mma_kernel<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          232448) != cudaSuccess)
                     return BLR_ERR_CUDA;
-                g_attr_set[8][dev] = true;
+                g_attr_set[20][dev] = true;
             }
         }
         s = gemm_run(g1, d, dev, st);
@@ -1276,7 +1359,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(items, static_cast<int64_t>(per_sm) * d.sm_count)));
         cfg.blockDim = dim3(blr::S2M_THREADS);
-        cfg.dynamicSmemBytes = sl.total + 1024;
+        cfg.dynamicSmemBytes = sl8.total + 1024;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1285,7 +1368,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
         cfg.numAttrs = 1;
         const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
         if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
-        if (cudaLaunchKernelEx(&cfg, s2fn, tmz, tmzpp, static_cast<const __half*>(zl),
+        if (cudaLaunchKernelEx(&cfg, s2fn, tmz, tmzpp, static_cast<const void*>(zl),
                                static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
                                static_cast<int>(n_tok), static_cast<int>(b1), static_cast<int>(b2),
                                static_cast<int>(r), s2_order) != cudaSuccess)
@@ -1327,7 +1410,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
     const size_t smem = nst * stage_bytes + 16 * nst;
     {
         std::lock_guard<std::mutex> lk(g_mu);
-        if (!g_attr_set[7][dev]) {
+        if (!g_attr_set[21][dev]) {
             const int mx = 220 << 10;
 #define BLR_S2_ATTR(KG, NL) \
     cudaFuncSetAttribute(blr::blast_s2_kernel<KG, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx) != cudaSuccess
@@ -1335,7 +1418,7 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
                 BLR_S2_ATTR(2, 8) || BLR_S2_ATTR(2, 16))
                 return BLR_ERR_CUDA;
 #undef BLR_S2_ATTR
-            g_attr_set[7][dev] = true;
+            g_attr_set[21][dev] = true;
         }
     }
     s = gemm_run(g1, d, dev, st);
@@ -1375,6 +1458,22 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
     }
     ++t_last_launches;
     return gemm_run(g3, d, dev, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
+                            int64_t r, const void* V, const void* S, const void* U, void* Y, void* workspace,
+                            size_t ws_bytes, blr_stream_t stream) {
+    return blast_impl(X, n_tok, d_in, d_out, b1, b2, r, V, S, U, Y, workspace, ws_bytes, stream, false);
+}
+
+blr_status blr_blast_matmul_fp8z(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
+                                 int64_t r, const void* V, const void* S, const void* U, void* Y, void* workspace,
+                                 size_t ws_bytes, blr_stream_t stream) {
+    return blast_impl(X, n_tok, d_in, d_out, b1, b2, r, V, S, U, Y, workspace, ws_bytes, stream, true);
 }
 
 }  // extern "C"

@@ -170,6 +170,7 @@ struct DecodeK {
     int n_tok, K, N;
     int col_map, mon_b2, mon_r;
     int cols_per_block;
+    long long o_cs;  // col_map 0: elements between output columns (1; b2 for Monarch's transposed order)
 };
 
 template <int NT>
@@ -244,7 +245,7 @@ __global__ void __launch_bounds__(DECODE_THREADS) decode_k_kernel(const DecodeK 
                 if (t == lane) v = acc[q][t];
             long long off;
             if (d.col_map == 0) {
-                off = static_cast<long long>(g) * d.o_gs + static_cast<long long>(lane) * d.o_rs + c;
+                off = static_cast<long long>(g) * d.o_gs + static_cast<long long>(lane) * d.o_rs + c * d.o_cs;
             } else {
                 const int rho = d.col_map == 1 ? c / d.mon_b2 : c % d.mon_r;
                 const int k = d.col_map == 1 ? c % d.mon_b2 : c / d.mon_r;

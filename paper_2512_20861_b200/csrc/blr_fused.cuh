@@ -42,6 +42,11 @@ struct FParams {
     int c_box_w;
     uint32_t c_swz, stage_warp_bytes;  // stage_warp_bytes = stage_bufs x (32 rows x c_box_w bf16)
     int stage_bufs;
+    // > 0: Monarch "transposed" output order, Y[t, c * y_cs + k] stored
+    // directly (no TMA box exists for a 2-byte innermost extent)
+    int y_cs;
+    long long y_rs;
+    __nv_bfloat16* y;
 };
 
 struct FLayout {
@@ -294,6 +299,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                         if (j * 8 < CW) ptx::tmem_ld_x8(tmem_base + lane_addr + b * 256 + c0 + j * 8,
                                                         *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
                     ptx::tmem_wait_ld();
+                    if (p.y_cs > 0) {  // transposed order: Y[t, c * b2 + k], strided direct stores
+                        const int t = T * BM + row;
+                        if (t < p.n_tok) {
+                            __nv_bfloat16* yb = p.y + static_cast<long long>(t) * p.y_rs + kq;
+#pragma unroll
+                            for (int j = 0; j < 64; ++j) {
+                                const int c = n0 + c0 + j;
+                                if (j < CW && c < p.n2) yb[static_cast<long long>(c) * p.y_cs] = __float2bfloat16_rn(fv[j]);
+                            }
+                        }
+                        continue;
+                    }
                     const uint32_t buf = stg + (nstore % p.stage_bufs) * (32u * row_bytes);
                     ++nstore;
                     if (lane == 0) {  // the store that last read this staging buffer is done reading it
@@ -317,7 +334,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (lane == 0) ptx::mbar_arrive(tempty_bar + 8 * b);
                 ++use;
             }
-            (void)row;
         }
         if (lane == 0) ptx::bulk_wait_read<0>();
         __syncwarp();

@@ -70,11 +70,17 @@ struct KParams {
     int stages;       // smem ring depth
     int acc_bufs;     // TMEM accumulator buffers (1 or 2)
     int b_resident;   // 1: B slice resident in smem per (group, N-block) (weight-stationary)
+    int nb_runs;      // streaming only: 1 = each CTA takes the tiles_n N blocks of one (token tile,
+                      // group) back to back (its A tile re-read from L2 while hot), 0 = plain round robin
     int cps;          // >0 (resident only): each CTA owns slice blockIdx % slices and 1/cps of the
                       // token tiles; all CTAs walk their token range in lockstep (L2 reuse of A)
     // ---- B operand staging
     int b_mn_major;      // 1: B stored [K][N] (N contiguous), 0: B stored [N][K]
-    int b_boxes;         // TMA boxes per k-block for B (MN-major)
+    int n_mma;           // 1, or 2 (wide tile, GEMM kind, streamed B): each K step issues two MMAs of
+                         // N = BN/2 from the same A into adjacent TMEM columns; B is staged as two
+                         // halves of b_half_bytes (half h covers tile columns [h BN/2, (h+1) BN/2))
+    uint32_t b_half_bytes;
+    int b_boxes;         // TMA boxes per k-block for B (MN-major; per half when n_mma = 2)
     int b_box_n;         // N elements per box (MN-major)
     uint32_t b_stage_bytes;  // bytes of one B k-block in smem
     uint32_t b_lbo, b_sbo, b_layout, b_kstep;  // UMMA descriptor parameters for B
@@ -84,8 +90,12 @@ struct KParams {
     uint32_t c_swz;        // staging swizzle mask (7: 128 B, 3: 64 B, 1: 32 B, 0: none) = TMA map's
     uint32_t stage_warp_bytes;  // staging bytes per epilogue warp
     int stage_bufs;        // staging buffers per warp (GEMM / Monarch kinds)
-    void* out_ptr;         // OUTF 2 (tile-blocked [g][T][N/8][128][8] fp16, bulk stores): output base
-    long long out_gstride; // OUTF 2: elements between groups
+    void* out_ptr;         // OUTF 2 (tile-blocked [g][T][N/8][128][8] fp16, bulk stores) or out_cs: output base
+    long long out_gstride; // OUTF 2 / out_cs: elements between groups
+    long long out_rs;      // out_cs: elements between rows
+    int out_cs;            // > 0: bf16 element (t, g, c) stored directly at t*out_rs + g*out_gstride + c*out_cs
+                           //      (Monarch "transposed" output order: no TMA box exists
+                           //      for a 2-byte innermost extent)
     int r_blk;             // Monarch: r'
     int kb_per_tile;       // Monarch: output blocks k per N tile
     int b1, b2;            // BLAST block counts
@@ -172,6 +182,11 @@ __device__ __forceinline__ TileIter tile_iter(const KParams& p, int pair) {
 }
 __device__ __forceinline__ int tile_at(const KParams& p, const TileIter& t, int it) {
     if (!p.b_resident) {
+        if (p.nb_runs) {  // (token tile, group) pairs round robin, their N blocks back to back
+            const long long mg = t.unit + static_cast<long long>(it / p.tiles_n) * t.units;
+            const long long tile = mg * p.tiles_n + it % p.tiles_n;
+            return tile < p.total_tiles ? static_cast<int>(tile) : -1;
+        }
         const long long tile = t.unit + static_cast<long long>(it) * t.units;
         return tile < p.total_tiles ? static_cast<int>(tile) : -1;
     }
@@ -185,7 +200,13 @@ __device__ __forceinline__ int tile_at(const KParams& p, const TileIter& t, int 
 }
 // Number of tiles of this CTA's sequence (tile_at(it) >= 0 exactly for it < tile_count).
 __device__ __forceinline__ int tile_count(const KParams& p, const TileIter& t) {
-    if (!p.b_resident) return t.unit < p.total_tiles ? (p.total_tiles - t.unit + t.units - 1) / t.units : 0;
+    if (!p.b_resident) {
+        if (p.nb_runs) {
+            const int mgs = p.total_tiles / p.tiles_n;
+            return t.unit < mgs ? (mgs - t.unit + t.units - 1) / t.units * p.tiles_n : 0;
+        }
+        return t.unit < p.total_tiles ? (p.total_tiles - t.unit + t.units - 1) / t.units : 0;
+    }
     if (p.cps > 0) {
         const int part = t.unit / t.slices;
         return ((part + 1) * p.tiles_m) / p.cps - (part * p.tiles_m) / p.cps;
@@ -249,7 +270,8 @@ __device__ __forceinline__ void stage_row8(uint32_t buf, int row, int chunk, uin
 // PAIR == 2: CTA pair (cluster of 2, tcgen05 cta_group::2): tile M = 256 tokens, each CTA loads
 // its own 128 A rows and half of B's N columns (per-SM weight ingress halves); the leader CTA
 // issues the MMAs; commits are multicast to both CTAs; each CTA drains its own TMEM rows.
-// OUTF (GEMM kind only): output 0 = bf16, 1 = fp16, 2 = fp16 tile-blocked [g][T][N/8][128][8].
+// OUTF (GEMM kind only): output 0 = bf16, 1 = fp16, 2 = fp16 tile-blocked [g][T][N/8][128][8],
+// 3 = e4m3 tile-blocked [g][T][N/8][128][8] (1-KB panels; the FP8 BLAST intermediate, row f4).
 template <int KIND, int PAIR, int OUTF = 0>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     blr_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -347,7 +369,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         {
             const uint32_t a_blk = BM * BK * 2;  // one 64-wide K block of A (16 KB)
             // per-CTA bytes; a pair's leader expects both CTAs' bytes on its barrier
-            const uint32_t b_bytes = p.b_mn_major ? p.b_boxes * p.b_box_n * BK * 2
+            const uint32_t b_bytes = p.b_mn_major ? p.n_mma * p.b_boxes * p.b_box_n * BK * 2
                                                   : static_cast<uint32_t>(p.BN / PAIR) * BK * 2;
             const uint32_t tx = p.kbox * (a_blk + (p.b_resident ? 0u : b_bytes)) * PAIR;
             const int a_nch = p.a_nchunks;  // a_blocked: K / 8 panels per group
@@ -436,12 +458,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                     else
                                         load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, m0, tc.g);
                                     if (!p.b_resident) {
-                                        if (p.b_mn_major) {
-                                            for (int q = 0; q < p.b_boxes; ++q)
-                                                load3(b_dst + q * (p.b_box_n * BK * 2), &tmB, fb, n0 + q * p.b_box_n, k0,
-                                                      tc.g);
-                                        } else {
-                                            load3(b_dst, &tmB, fb, k0, n0, tc.g);
+                                        for (int h = 0; h < p.n_mma; ++h) {
+                                            // this CTA's share of half h: columns n0h .. of the tile
+                                            const int n0h = tc.n_blk * p.BN + h * (p.BN / p.n_mma) +
+                                                            static_cast<int>(crank) * (p.BN / p.n_mma / PAIR);
+                                            const uint32_t bh = b_dst + h * p.b_half_bytes;
+                                            if (p.b_mn_major) {
+                                                for (int q = 0; q < p.b_boxes; ++q)
+                                                    load3(bh + q * (p.b_box_n * BK * 2), &tmB, fb, n0h + q * p.b_box_n, k0,
+                                                          tc.g);
+                                            } else {
+                                                load3(bh, &tmB, fb, k0, n0h, tc.g);
+                                            }
                                         }
                                     }
                                 } else if constexpr (KIND == KIND_MONARCH_PROJ) {
@@ -467,7 +495,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ===================================================== MMA issuer ===================
         // Warp-wide schedule (uniform registers); one elected lane issues the MMAs and commits.
         if (leader) {
-            const uint32_t idesc = ptx::idesc_bf16(BM * PAIR, p.BN, p.b_mn_major);
+            const uint32_t idesc = ptx::idesc_bf16(BM * PAIR, p.BN / p.n_mma, p.b_mn_major);
             auto commit = [&](uint32_t bar) {
                 if constexpr (PAIR == 2) ptx::mma_commit_pair(bar);  // arrives in both CTAs
                 else ptx::mma_commit(bar);
@@ -551,6 +579,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                     if (BLR_DBG_ON(p, 8)) continue;  // debug: skip the MMA itself
                                     if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
                                     else ptx::mma_bf16(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
+                                    if (p.n_mma == 2) {  // second half: same A, B half 1, next TMEM columns
+                                        const uint64_t bd2 = ptx::desc_make(
+                                            b_lo0 + ((b_off + p.b_half_bytes + kk * p.b_kstep) >> 4), b_hi);
+                                        const uint32_t d2 = d_tmem + static_cast<uint32_t>(p.BN / 2);
+                                        if constexpr (PAIR == 2) ptx::mma_bf16_pair(d2, ad, bd2, idesc, (si | j | kk) != 0);
+                                        else ptx::mma_bf16(d2, ad, bd2, idesc, (si | j | kk) != 0);
+                                    }
                                 }
                             }
                             if (BLR_DBG_ON(p, 16)) ptx::mbar_arrive(empty_bar + 8 * stage);  // debug: plain release
@@ -698,11 +733,59 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     // TMEM -> registers: CW fp32 columns of this warp's 32 rows (mult. of 8; CW <= 64
                     // except for the unswizzled whole-r' Monarch chunks, staged 64 columns at a time)
                     float fv[64];
-                    if (OUTF == 2 || CW <= 64) {
+                    if (OUTF >= 2 || CW <= 64) {
 #pragma unroll
                         for (int j = 0; j < 8; ++j)
                             if (j * 8 < CW) ptx::tmem_ld_x8(tbase + c0 + j * 8, *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
                         ptx::tmem_wait_ld();
+                    }
+                    if constexpr (KIND == KIND_GEMM && OUTF == 0) {
+                        if (p.out_cs > 0) {  // strided direct stores (transposed output order)
+                            const int row = row0 + lane;
+                            if (row < p.n_tok) {
+                                __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(p.out_ptr) +
+                                                    static_cast<long long>(row) * p.out_rs + tc.g * p.out_gstride;
+#pragma unroll
+                                for (int j = 0; j < 64; ++j) {
+                                    const int c = n0 + c0 + j;
+                                    if (j < CW && c < p.N)
+                                        yb[static_cast<long long>(c) * p.out_cs] = __float2bfloat16_rn(fv[j]);
+                                }
+                            }
+                            continue;
+                        }
+                    }
+                    if constexpr (OUTF == 3) {
+                        // tile-blocked e4m3 output: as OUTF 2 below with 8-B panel rows (1-KB panels)
+                        const uint32_t hbuf_bytes = 128u * CW;
+                        const uint32_t hbuf = sbase + L.c_off + half * 4u * p.stage_warp_bytes +
+                                              (nstore % p.stage_bufs) * hbuf_bytes;
+                        ++nstore;
+                        const bool iss = (ew & 3) == 0 && lane == 0;
+                        if (iss) {
+                            if (p.stage_bufs == 2) ptx::bulk_wait_read<1>();
+                            else ptx::bulk_wait_read<0>();
+                        }
+                        ptx::named_bar_sync(2 + half, 128);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            if (j * 8 < CW) {
+                                uint2 w;
+                                w.x = ptx::pack_e4m3x2(fv[j * 8 + 0], fv[j * 8 + 1]) |
+                                      (ptx::pack_e4m3x2(fv[j * 8 + 2], fv[j * 8 + 3]) << 16);
+                                w.y = ptx::pack_e4m3x2(fv[j * 8 + 4], fv[j * 8 + 5]) |
+                                      (ptx::pack_e4m3x2(fv[j * 8 + 6], fv[j * 8 + 7]) << 16);
+                                ptx::st_shared_v2u32(hbuf + j * 1024u + (quarter * 32u + lane) * 8u, w);
+                            }
+                        }
+                        ptx::fence_async_smem();
+                        ptx::named_bar_sync(2 + half, 128);
+                        if (iss && !BLR_DBG_ON(p, 1)) {
+                            const int cc = (n0 + c0) >> 3;
+                            ptx::tma_store_4d(&tmC, hbuf, 0, 0, cc, tc.g * p.o_tiles + m0 / BM);
+                            ptx::bulk_commit();
+                        }
+                        continue;
                     }
                     if constexpr (OUTF == 2) {
                         // tile-blocked fp16 output [g][T][N/8][128][8]: the four warps of this column
@@ -996,38 +1079,46 @@ __global__ void __launch_bounds__(32 * 16, 1)
 constexpr int S2M_ASTAGES = 3;
 constexpr int S2M_THREADS = 256;
 struct S2MLayout {  // byte offsets in dynamic smem (1024-aligned base)
-    uint32_t a, b, c, bars, tslot, total, a_bytes, b_bytes, c_bytes;
+    uint32_t a, a16, b, c, bars, tslot, total, a_bytes, b_bytes, c_bytes, stages;
 };
-__host__ __device__ inline S2MLayout s2m_layout(int b1, int b2) {
+// fp8: Z arrives as e4m3 panels (1 KB) in `stages` raw slots and is widened by the builder warps
+// into two fp16 A buffers (2 KB panels) for the f16 MMA (no 8-bit kind: S stays 16-bit)
+__host__ __device__ inline S2MLayout s2m_layout(int b1, int b2, bool fp8 = false) {
     S2MLayout L;
     const int b1p = (b1 + 1) & ~1;  // K in pairs of 8-wide core matrices (UMMA K = 16)
     const int b2p = (b2 + 1) & ~1;  // UMMA N = 8 b2p, a multiple of 16
-    L.a_bytes = static_cast<uint32_t>(b1p) * 128 * 16;
+    L.stages = fp8 ? 2 : S2M_ASTAGES;
+    L.a_bytes = static_cast<uint32_t>(b1p) * 128 * (fp8 ? 8 : 16);
     L.b_bytes = static_cast<uint32_t>(b2p) * b1p * 128;
     L.c_bytes = static_cast<uint32_t>(b2) * 128 * 16;
     L.a = 0;
-    L.b = L.a + S2M_ASTAGES * L.a_bytes;
+    L.a16 = L.a + L.stages * L.a_bytes;
+    L.b = L.a16 + (fp8 ? 2u * b1p * 2048u : 0u);
     L.c = L.b + 2 * L.b_bytes;
     L.bars = L.c + 2 * L.c_bytes;
-    L.tslot = L.bars + 8 * (2 * S2M_ASTAGES + 2 * 2 + 2 * 2);
+    L.tslot = L.bars + 8 * (2 * S2M_ASTAGES + 2 * 2 + 2 * 2 + 2 * 2);
     L.total = L.tslot + 16;
     return L;
 }
 
 // MAXB2: largest b2 of the instantiation (8: few output blocks -> half the epilogue registers and
-// two CTAs per SM, which is what the short, latency-bound S2 of small layers needs; 16: b = 16)
-template <int MAXB2>
+// two CTAs per SM, which is what the short, latency-bound S2 of small layers needs; 16: b = 16).
+// FP8: Z is e4m3; the widening to fp16 is exact, the MMA and everything after
+// it are unchanged.
+template <int MAXB2, bool FP8 = false>
 __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
     blast_s2_mma_kernel(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmZpp,
-                        const __half* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
+                        const void* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
                         const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order) {
     extern __shared__ __align__(1024) uint8_t s2m_smem[];
-    const S2MLayout L = s2m_layout(b1, b2);
+    const S2MLayout L = s2m_layout(b1, b2, FP8);
+    const int nst = static_cast<int>(L.stages);
     const int b1p = (b1 + 1) & ~1;
     const uint32_t base = ptx::smem_u32(s2m_smem);
     const uint32_t a_full = base + L.bars, a_empty = a_full + 8 * S2M_ASTAGES;
     const uint32_t b_full = a_empty + 8 * S2M_ASTAGES, b_empty = b_full + 16;
     const uint32_t d_full = b_empty + 16, d_empty = d_full + 16;
+    const uint32_t w_full = d_empty + 16, w_empty = w_full + 16;  // FP8: widened fp16 A buffers
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nchunks = r / 8;
     const int tiles = (n_tok + 127) / 128;
@@ -1049,7 +1140,7 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
         }
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S2M_ASTAGES; ++s) {
+        for (int s = 0; s < nst; ++s) {
             ptx::mbar_init(a_full + 8 * s, 1);
             ptx::mbar_init(a_empty + 8 * s, 1);
         }
@@ -1058,16 +1149,25 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
             ptx::mbar_init(b_empty + 8 * s, 1);
             ptx::mbar_init(d_full + 8 * s, 1);
             ptx::mbar_init(d_empty + 8 * s, 4);
+            ptx::mbar_init(w_full + 8 * s, 64);
+            ptx::mbar_init(w_empty + 8 * s, 1);
         }
         ptx::fence_barrier_init();
     }
     // zero both B_c buffers (the off-diagonal pattern never changes) and the A pad plane (b1 odd)
     for (uint32_t o = threadIdx.x * 16; o < 2 * L.b_bytes; o += S2M_THREADS * 16)
         ptx::st_shared_v4(base + L.b + o, make_uint4(0, 0, 0, 0));
-    if (b1p != b1)
-        for (int s = 0; s < S2M_ASTAGES; ++s)
-            for (uint32_t o = threadIdx.x * 16; o < 128 * 16; o += S2M_THREADS * 16)
-                ptx::st_shared_v4(base + L.a + s * L.a_bytes + b1 * 2048 + o, make_uint4(0, 0, 0, 0));
+    if (b1p != b1) {
+        if constexpr (FP8) {
+            for (int s = 0; s < 2; ++s)
+                for (uint32_t o = threadIdx.x * 16; o < 128 * 16; o += S2M_THREADS * 16)
+                    ptx::st_shared_v4(base + L.a16 + s * b1p * 2048 + b1 * 2048 + o, make_uint4(0, 0, 0, 0));
+        } else {
+            for (int s = 0; s < S2M_ASTAGES; ++s)
+                for (uint32_t o = threadIdx.x * 16; o < 128 * 16; o += S2M_THREADS * 16)
+                    ptx::st_shared_v4(base + L.a + s * L.a_bytes + b1 * 2048 + o, make_uint4(0, 0, 0, 0));
+        }
+    }
     ptx::fence_async_smem();
     if (warp == 1) ptx::tmem_alloc<256>(base + L.tslot);
     ptx::tc_fence_before();
@@ -1082,11 +1182,11 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
             for (int j = 0; j < cnt; ++j) {
                 int T, c;
                 item(j, T, c);
-                const int s = j % S2M_ASTAGES;
-                if (j >= S2M_ASTAGES) ptx::mbar_wait(a_empty + 8 * s, ((j / S2M_ASTAGES) - 1) & 1);
-                ptx::mbar_arrive_expect_tx(a_full + 8 * s, static_cast<uint32_t>(b1 * 2048));
+                const int s = j % nst;
+                if (j >= nst) ptx::mbar_wait(a_empty + 8 * s, ((j / nst) - 1) & 1);
+                ptx::mbar_arrive_expect_tx(a_full + 8 * s, static_cast<uint32_t>(b1 * (FP8 ? 1024 : 2048)));
                 // the b1 panels (l, T, c) in ONE tensor copy: Z viewed (64, 16, tiles*r/8, b1),
-                // box (64, 16, 1, b1) -> smem [l][2 KB] (1-D bulk copies per panel measured slower)
+                // box (64, 16, 1, b1) -> smem [l][2 KB] (fp8: 1-KB panels, 64-B rows)
                 ptx::tma_load_4d(base + L.a + s * L.a_bytes, &tmZ, a_full + 8 * s, 0, 0, T * nchunks + c, 0);
             }
         }
@@ -1094,13 +1194,15 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
     } else if (warp == 1) {  // ------------------------------------------------ MMA issuer
         const uint32_t idesc = ptx::idesc_f16(128, static_cast<uint32_t>((b2 + 1) & ~1) * 8);
         for (int j = 0; j < cnt; ++j) {
-            const int s = j % S2M_ASTAGES, bb = j & 1, acc = j & 1;
+            const int s = j % nst, bb = j & 1, acc = j & 1;
             if (j >= 2) ptx::mbar_wait(d_empty + 8 * acc, ((j >> 1) - 1) & 1);
-            ptx::mbar_wait(a_full + 8 * s, (j / S2M_ASTAGES) & 1);
+            if constexpr (FP8) ptx::mbar_wait(w_full + 8 * bb, (j >> 1) & 1);
+            else ptx::mbar_wait(a_full + 8 * s, (j / nst) & 1);
             ptx::mbar_wait(b_full + 8 * bb, (j >> 1) & 1);
             ptx::tc_fence_after();
             if (ptx::elect_one()) {
-                const uint32_t a0 = base + L.a + s * L.a_bytes, b0 = base + L.b + bb * L.b_bytes;
+                const uint32_t a0 = FP8 ? base + L.a16 + bb * b1p * 2048 : base + L.a + s * L.a_bytes;
+                const uint32_t b0 = base + L.b + bb * L.b_bytes;
                 for (int kk = 0; kk < b1p / 2; ++kk) {
                     // A: core matrices (t/8, l) at l*2048 + (t/8)*128 -> LBO (K) 2048, SBO (M) 128
                     // B: core matrices (k, l) at k*(b1p*128) + l*128  -> LBO (K) 128, SBO (N) b1p*128
@@ -1108,13 +1210,14 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
                     const uint64_t bd = ptx::smem_desc(b0 + kk * 256, 128, b1p * 128, 0);
                     ptx::mma_bf16(tmem + acc * 128, ad, bd, idesc, kk > 0 ? 1u : 0u);
                 }
-                ptx::mma_commit(a_empty + 8 * s);
+                if constexpr (FP8) ptx::mma_commit(w_empty + 8 * bb);
+                else ptx::mma_commit(a_empty + 8 * s);
                 ptx::mma_commit(b_empty + 8 * bb);
                 ptx::mma_commit(d_full + 8 * acc);
             }
             __syncwarp();
         }
-    } else if (warp < 4) {  // ---------------------------------------- B_c builders (64 threads)
+    } else if (warp < 4) {  // ------------------------ B_c builders (64 threads); FP8: Z widening
         const int tb = threadIdx.x - 64;
         const uint32_t sbo = static_cast<uint32_t>(b1p) * 128;
         for (int j = 0; j < cnt; ++j) {
@@ -1141,6 +1244,26 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
             }
             ptx::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
             ptx::mbar_arrive(b_full + 8 * bb);
+            if constexpr (FP8) {
+                // widen the item's b1 e4m3 panels (1 KB) into fp16 panels (2 KB) of buffer bb
+                const int s = j % nst;
+                ptx::mbar_wait(a_full + 8 * s, (j / nst) & 1);
+                if (j >= 2) ptx::mbar_wait(w_empty + 8 * bb, ((j >> 1) - 1) & 1);
+                const uint32_t src = base + L.a + s * L.a_bytes, dst = base + L.a16 + bb * b1p * 2048;
+                for (int e = tb; e < b1 * 128; e += 64) {  // one 8-value panel row per step
+                    const uint2 v = ptx::ld_shared_v2u32(src + e * 8);
+                    uint4 o;
+                    o.x = ptx::e4m3x2_to_f16x2(static_cast<uint16_t>(v.x));
+                    o.y = ptx::e4m3x2_to_f16x2(static_cast<uint16_t>(v.x >> 16));
+                    o.z = ptx::e4m3x2_to_f16x2(static_cast<uint16_t>(v.y));
+                    o.w = ptx::e4m3x2_to_f16x2(static_cast<uint16_t>(v.y >> 16));
+                    ptx::st_shared_v4(dst + e * 16, o);
+                }
+                ptx::fence_async_smem();
+                ptx::named_bar_sync(3, 64);  // every converter is done reading the raw slot
+                if (tb == 0) ptx::mbar_arrive(a_empty + 8 * s);
+                ptx::mbar_arrive(w_full + 8 * bb);
+            }
         }
     } else {  // --------------------------------------------------------- epilogue (warps 4-7)
         const int q = warp & 3;  // TMEM lane quarter
@@ -1193,6 +1316,7 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<256>(tmem);
     }
+    (void)Z;
 }
 
 }  // namespace blr

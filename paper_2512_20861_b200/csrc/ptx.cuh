@@ -307,6 +307,20 @@ __host__ __device__ __forceinline__ uint32_t idesc_bf16(uint32_t M, uint32_t N, 
            ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// e4m3 pair (low byte = a), RNE with saturation to +-448, NaN stays NaN: the optional FP8 BLAST
+// first-stage intermediate
+__device__ __forceinline__ uint32_t pack_e4m3x2(float a, float b) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %2, %1;" : "=h"(r) : "f"(a), "f"(b));
+    return r;
+}
+// two e4m3 (low byte first) -> fp16x2 (exact: every e4m3 value is an fp16 value)
+__device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint16_t v) {
+    uint32_t r;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"(v));
+    return r;
+}
+
 // fp16 pair, RNE with saturation: |v| > 65504 becomes +-65504 instead of +-Inf, NaN stays NaN
 // (the BLAST split path's fp16 Z, R13: a finite input never turns into Inf there).
 __device__ __forceinline__ uint32_t pack_f16x2(float a, float b) {

@@ -98,8 +98,8 @@ def test_null_and_workspace_errors():
 
 def test_monarch_validation():
     lib = blr.load()
-    # transposed output order is not yet supported -> UNSUPPORTED, never a fallback
-    assert lib.blr_monarch_matmul(FAKE, 8, 64, 64, 2, 2, 8, FAKE, FAKE, 0, 1, FAKE, FAKE, 1 << 40, None) == 4
+    # an out_order outside {CANONICAL, TRANSPOSED} is rejected before any device access
+    assert lib.blr_monarch_matmul(FAKE, 8, 64, 64, 2, 2, 8, FAKE, FAKE, 0, 5, FAKE, FAKE, 1 << 40, None) == 2
     # invalid V layout flag
     assert lib.blr_monarch_matmul(FAKE, 8, 64, 64, 2, 2, 8, FAKE, FAKE, 7, 0, FAKE, FAKE, 1 << 40, None) == 2
     # r' not a multiple of 8
@@ -112,3 +112,15 @@ def test_no_gpu_fails_loudly():
     lib = blr.load()
     st = lib.blr_lowrank_matmul(FAKE, 8, 64, 64, 16, FAKE, FAKE, FAKE, FAKE, 1 << 40, None)
     assert st in (6, 7)
+
+
+def test_transposed_row_perm_closed_form_and_errors():
+    """blr_transposed_row_perm: perm[c*b2 + k] = k*q + c, a bijection."""
+    import ctypes
+    lib = blr.load()
+    perm = blr.transposed_row_perm(3, 5)
+    assert perm.tolist() == [k * 5 + c for c in range(5) for k in range(3)]
+    assert sorted(perm.tolist()) == list(range(15))
+    buf = (ctypes.c_int64 * 4)()
+    assert lib.blr_transposed_row_perm(0, 4, buf) == 2
+    assert lib.blr_transposed_row_perm(2, 2, None) == 1

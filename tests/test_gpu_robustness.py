@@ -63,15 +63,19 @@ def test_nonfinite_token_does_not_touch_other_rows(cuda_lib, method, n, i, o, r,
 
 @pytest.mark.parametrize("scale", [1e3])
 @pytest.mark.parametrize("method,n,i,o,r,b", [("blast", 300, 16 * 256, 16 * 64, 744, 16),
-                                              ("blast", 256, 6 * 128, 6 * 512, 192, 6),
-                                              ("monarch", 256, 4 * 192, 4 * 768, 192, 4),
-                                              ("lowrank", 256, 768, 3072, 192, 1)])
+                                              ("blast", 256, 6 * 512, 6 * 128, 192, 6),
+                                              ("monarch", 256, 16 * 256, 16 * 64, 1536, 16),
+                                              ("lowrank", 256, 4096, 1024, 256, 1)])
 def test_large_magnitude_and_raw_outliers(cuda_lib, method, n, i, o, r, b, scale):
     """|X| ~ 1e3 with 8 channels x20 on top and NO renormalisation (|X| up to ~1e5 in those
     channels), at Llama-7B-like block sizes (p = 256): the split path's fp16 Z stays inside its
     range (|X_l V_l| <= 65504, include/blr.h) and the result meets the north_star bound, applied
     at the output's scale, against the fp64 oracle.  (With p = 16 the same X drives |Z| to
-    ~7.5e4: outside the documented fp16 range -- test_fp16_range_saturates_and_stays_row_local.)"""
+    ~7.5e4: outside the documented fp16 range -- test_fp16_range_saturates_and_stays_row_local.
+    At GPT2-S c_fc shapes this raw-outlier input exceeds the per-element bound even with exact
+    fp32 intermediates before the final two bf16 roundings (emulated: BLAST 1.05x, Monarch 1.08x
+    the bound) -- a property of the bound, not of the kernels, reading R17; the cases
+    below are Llama-7B-like blocks (emulated worst element 0.7-0.8x the bound).)"""
     g = torch.Generator().manual_seed(33)
     x = torch.randn(n, i, generator=g) * scale
     idx = torch.linspace(0, i - 1, 8).round().long()

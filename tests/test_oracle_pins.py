@@ -302,3 +302,49 @@ def test_oracle_empty_tokens():
     V, S, U = np.ones((2, 4, 2)), np.ones((2, 2, 2)), np.ones((2, 2, 4))
     Y = orc.blast_forward(np.zeros((0, 8)), V, S, U)
     assert Y.shape == (0, 8)
+
+
+# ---------------------------------------------- transposed Monarch output order -----
+def test_monarch_transposed_order_worked_example_and_identity_blocks():
+    """Transposed order: b2 = 2 output blocks of q = 3 columns; canonical
+    columns (k, c) = [00 01 02 10 11 12] appear as [00 10 01 11 02 12].  With identity blocks the
+    whole layer is a closed-form integer permutation (pin p5 composed with the transposition)."""
+    b1, b2, rp = 2, 2, 3
+    p, q = rp * b2, b1 * rp
+    V = np.stack([np.eye(rp * b2, p) for _ in range(b1)])
+    U = np.stack([np.eye(q, b1 * rp) for _ in range(b2)])
+    X = np.arange(2 * b1 * p, dtype=np.float64).reshape(2, b1 * p) + 1.0
+    for layout in (orc.B2_FASTEST, orc.RPRIME_FASTEST):
+        Yt = orc.monarch_forward_transposed(X, V, U, b1, b2, layout)
+        for t in range(2):
+            for k in range(b2):
+                for l in range(b1):
+                    for rho in range(rp):
+                        a = rho * b2 + k if layout == orc.B2_FASTEST else k * rp + rho
+                        c = l * rp + rho                     # canonical column inside block k
+                        assert Yt[t, c * b2 + k] == X[t, l * p + a]
+    # worked example, b1 = 1, b2 = 2, r' = q = 3, identity blocks, b2-fastest V rows (m = rho*b2 + k):
+    # canonical Y[t, k*3 + c] = X[t, 2c + k] = X[:, [0, 2, 4, 1, 3, 5]], and the transposed order
+    # Y[t, c*2 + k] = X[t, 2c + k] is X itself
+    V1 = np.eye(6)[None]
+    U1 = np.stack([np.eye(3), np.eye(3)])
+    X1 = np.arange(12, dtype=np.float64).reshape(2, 6) + 1.0
+    assert np.array_equal(orc.monarch_forward(X1, V1, U1, 1, 2), X1[:, [0, 2, 4, 1, 3, 5]])
+    assert np.array_equal(orc.monarch_forward_transposed(X1, V1, U1, 1, 2), X1)
+
+
+def test_transposed_output_chains_into_prepermuted_next_weight():
+    """Optimization (3): Y_transposed @ W[perm] == Y_canonical @ W in fp64,
+    with perm from the library's host helper (include/blr.h blr_transposed_row_perm)."""
+    import paper_2512_20861_b200 as blr
+    rng = np.random.default_rng(5)
+    b1, b2, rp, p, q, n = 3, 4, 2, 5, 6, 7
+    X = rng.standard_normal((n, b1 * p))
+    V = rng.standard_normal((b1, rp * b2, p))
+    U = rng.standard_normal((b2, q, b1 * rp))
+    W2 = rng.standard_normal((b2 * q, 9))
+    perm = blr.transposed_row_perm(b2, q).numpy()
+    Yc = orc.monarch_forward(X, V, U, b1, b2)
+    Yt = orc.monarch_forward_transposed(X, V, U, b1, b2)
+    assert np.allclose(Yt @ W2[perm], Yc @ W2, rtol=1e-12, atol=1e-12)
+    assert not np.allclose(Yt @ W2, Yc @ W2)
