@@ -41,13 +41,15 @@ def lib_path() -> str:
 
 
 def load():
-    """Load libblr.so (raises if it is missing; never falls back)."""
+    """Load libblr.so (raises if it is missing; never falls back).  BLR_LIB=<path> loads another
+    build of the same library instead (A/B timing of two builds only)."""
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
-        raise RuntimeError(f"libblr.so not found at {LIB_PATH}; run __graft_entry__.build()")
-    lib = ctypes.CDLL(LIB_PATH)
+    path = os.environ.get("BLR_LIB", LIB_PATH)
+    if not os.path.exists(path):
+        raise RuntimeError(f"libblr.so not found at {path}; run __graft_entry__.build()")
+    lib = ctypes.CDLL(path)
     i64, vp, sz = ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
     lib.blr_lowrank_matmul.argtypes = [vp, i64, i64, i64, i64, vp, vp, vp, vp, sz, vp]
     lib.blr_monarch_matmul.argtypes = [vp, i64, i64, i64, i64, i64, i64, vp, vp, ctypes.c_int,

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/blr.h"
 #include "blr_kernels.cuh"
@@ -185,7 +186,8 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) 
     for (int resident = (allow_resident && reuse) ? 1 : 0; resident >= 0; --resident) {
         int best_score = -1;
         KParams best = p;
-        for (int kbox = kbox_max; kbox >= 1; --kbox) {
+        const int kbox_min = (kb_env && kb_env[0] == '2' && p.k_blocks >= 2) ? 2 : 1;  // BLR_KBOX=2 forces 2
+        for (int kbox = kbox_max; kbox >= kbox_min; --kbox) {
             for (int bufs = 2; bufs >= 1; --bufs) {
                 if (bufs_env && atoi(bufs_env) != bufs) continue;
                 KParams q = p;
@@ -238,6 +240,8 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     KParams p = p_in;
     p.trace = t_trace;
     p.first = t_last_launches == 0 ? 1 : 0;  // first launch of this API call (PDL ordering, kernel)
+    p.mma_burst = (PAIR == 1 || p.b_resident || KIND != blr::KIND_GEMM) ? 1 : 0;
+    if (const char* e = getenv("BLR_BURST")) p.mma_burst = atoi(e);
 #ifdef BLR_DEBUG_KNOBS
     if (const char* e = getenv("BLR_DBG")) p.dbg = atoi(e);  // debug experiments only
     if (const char* e = getenv("BLR_DBG_LAUNCH"); e && atoi(e) != t_last_launches) p.dbg = 0;  // only launch k
@@ -255,15 +259,40 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
             g_attr_set[slot][dev] = true;
         }
     }
-    const int units = d.sm_count / PAIR;  // CTAs (or CTA pairs) that fit one wave
-    int grid = static_cast<int>(std::min<int64_t>(p.total_tiles, units)) * PAIR;
+    const int csz = PAIR * std::max(1, p.mc);  // CTAs per cluster
+    int units = d.sm_count / csz;              // CTAs (pairs, clusters) that fit one wave
+    if (csz > 2) {
+        // clusters of 4+ CTAs must fit inside a GPC: ask how many can be co-resident
+        static int cached[8] = {};
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!cached[csz]) {
+            cudaLaunchConfig_t oc = {};
+            oc.gridDim = dim3(csz);
+            oc.blockDim = dim3(blr::NUM_THREADS);
+            oc.dynamicSmemBytes = SMEM_LIMIT;
+            cudaLaunchAttribute oa[1];
+            oa[0].id = cudaLaunchAttributeClusterDimension;
+            oa[0].val.clusterDim.x = csz;
+            oa[0].val.clusterDim.y = 1;
+            oa[0].val.clusterDim.z = 1;
+            oc.attrs = oa;
+            oc.numAttrs = 1;
+            int nc = 0;
+            if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT) != cudaSuccess ||
+                cudaOccupancyMaxActiveClusters(&nc, kfn, &oc) != cudaSuccess || nc <= 0)
+                return BLR_ERR_CUDA;
+            cached[csz] = nc;
+        }
+        units = std::min(units, cached[csz]);
+    }
+    int grid = static_cast<int>(std::min<int64_t>(p.total_tiles, units)) * csz;
     if (p.b_resident && p.cps > 0) grid = p.groups * p.tiles_n * p.cps * PAIR;
     else if (p.b_resident) grid = std::min(units, p.groups * p.tiles_n) * PAIR;  // slice round-robin
     if (const char* pe = getenv("BLR_PLAN"); pe && pe[0] == '1')
         fprintf(stderr,
-                "[blr plan] kind=%d pair=%d grid=%d tiles=%dx%dx%d BN=%d mma=%d bbox=%d kblk=%d kbox=%d stages=%d res=%d "
+                "[blr plan] kind=%d pair=%d mc=%d grid=%d tiles=%dx%dx%d BN=%d mma=%d bbox=%d kblk=%d kbox=%d stages=%d res=%d "
                 "cps=%d bufs=%d acc=%d cbox=%d smem=%d\n",
-                KIND, PAIR, grid, p.tiles_m, p.groups, p.tiles_n, p.BN, p.n_mma, p.b_box_n, p.k_blocks, p.kbox, p.stages,
+                KIND, PAIR, p.mc, grid, p.tiles_m, p.groups, p.tiles_n, p.BN, p.n_mma, p.b_box_n, p.k_blocks, p.kbox, p.stages,
                 p.b_resident, p.cps, p.stage_bufs, p.acc_bufs, p.c_box_w, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -274,7 +303,7 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = PAIR;
+    attr[1].val.clusterDim.x = csz;
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
@@ -366,11 +395,12 @@ struct OutMap {  // 4-D view (N, comp, groups, rows) of a GEMM phase's output
 // wide: a CTA-pair tile of up to 512 columns as two MMAs per K step (KParams::n_mma), single
 // accumulator buffer, streamed B only.
 bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok, int64_t K, int64_t groups,
-               int64_t N, bool b_mn_major, const OutMap& out, int comp, bool wide = false) {
+               int64_t N, bool b_mn_major, const OutMap& out, int comp, bool wide = false, int mc = 1) {
     p = KParams{};
     p.a_gmid = a_gmid;
     p.n_tok = static_cast<int>(n_tok);
-    p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM * pair));
+    p.mc = mc;
+    p.tiles_m = static_cast<int>(cdiv(n_tok, blr::BM * pair * mc));
     p.n_mma = wide ? 2 : 1;
     if (wide) {  // N tiles of <= 512, halves multiples of 16 (per-CTA halves multiples of 8)
         p.BN = static_cast<int>(rup(cdiv(N, cdiv(N, 512)), 32));
@@ -400,7 +430,8 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     p.c_box_w = chunk_width(p.BN);
     while (p.c_box_w * esz > 128) p.c_box_w /= 2;  // staged rows <= 128 B
     p.c_swz = out.blocked ? 0 : pick_swz(p.c_box_w * esz).mask;
-    return finish_plan(p, !wide, 32 * p.c_box_w * esz, d.sm_count / pair);
+    if (mc > 1 && !b_mn_major && (bn_full / p.n_mma / pair) % (8 * mc)) return false;  // K-major slices
+    return finish_plan(p, !wide && mc == 1, 32 * p.c_box_w * esz, d.sm_count / (pair * mc));
 }
 
 // A planned GEMM phase: parameters and tensor maps, encoded before anything is launched (so a
@@ -464,10 +495,23 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
     // down S1); BLR_WIDE=0/1 overrides
     {
         const char* we = getenv("BLR_WIDE");
-        const bool want = we ? we[0] == '1' : (pair == 2 && !p.b_resident && N >= 512 && K >= 512);
+        // measured no faster than 256-column pair tiles (C4 gate/down in-process A/B): opt-in only
+        const bool want = we && we[0] == '1';
         if (want && pair == 2 && out.col_stride == 0) {
             KParams w;
             if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, true)) p = w;
+        }
+    }
+    // B multicast across CTA pairs (cluster of 2 mc CTAs) for streamed pair plans with enough token
+    // tiles; BLR_MC=1/2/4 overrides
+    {
+        // measured slower (C4 8.98 -> 10.47 ms: 33 co-resident 4-CTA clusters instead of 37 pairs, and
+        // lock-stepped slot release): opt-in only
+        const char* me = getenv("BLR_MC");
+        int mc = me ? atoi(me) : 1;
+        if (mc > 1 && pair == 2 && !p.b_resident && n_tok >= 2048 * mc) {
+            KParams w;
+            if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, p.n_mma == 2, mc)) p = w;
         }
     }
     const int esz = 2;
@@ -512,13 +556,13 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
     if (b_mn_major) {
         const uint64_t dims[3] = {static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(groups)};
         const uint64_t str[2] = {static_cast<uint64_t>(N) * 2, static_cast<uint64_t>(N * K) * 2};
-        const uint32_t box[3] = {static_cast<uint32_t>(p.b_box_n), blr::BK, 1};
+        const uint32_t box[3] = {static_cast<uint32_t>(p.b_box_n), static_cast<uint32_t>(blr::BK / std::max(1, p.mc)), 1};
         if (!encode(&tb, B, 3, dims, str, box, p.b_box_n == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
             return BLR_ERR_CUDA;
     } else {
         const uint64_t dims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(groups)};
         const uint64_t str[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K * N) * 2};
-        const uint32_t box[3] = {blr::BK, static_cast<uint32_t>(p.BN / pair / p.n_mma), 1};
+        const uint32_t box[3] = {blr::BK, static_cast<uint32_t>(p.BN / pair / p.n_mma / std::max(1, p.mc)), 1};
         if (!encode(&tb, B, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
     }
     if (out.blocked) {
@@ -555,6 +599,7 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
     // fp16 output (BLAST split-path Z) is a separate instantiation: the bf16 epilogue stays as is
     g.pair = pair;
     g.outf = out.f32 == 3 ? 3 : out.f32 == 2 ? (out.blocked ? 2 : 1) : 0;
+
     return BLR_OK;
 }
 
@@ -1312,6 +1357,26 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
                               OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
     if (s != BLR_OK) return s;
 
+    // Token-chunked S2 -> S3 (BLR_S23_CHUNK = tokens per chunk, a multiple of 256; 0 = off): S1 runs
+    // over all tokens, then S2 and S3 alternate chunk by chunk through ONE chunk-sized Z'' buffer,
+    // small enough to stay in L2 next to U, so S3 reads its A operand from L2 and Z'' is overwritten
+    // in L2 instead of written back
+    int64_t chunk = 0;
+    if (const char* ce = getenv("BLR_S23_CHUNK")) chunk = rup(std::max<int64_t>(0, atoll(ce)), 256);
+    if (!s2_mma || chunk <= 0 || chunk >= n_tok) chunk = 0;
+    std::vector<GemmPrep> g3c;
+    if (chunk > 0) {
+        for (int64_t c0 = 0; c0 < n_tok; c0 += chunk) {
+            const int64_t nc = std::min(chunk, n_tok - c0);
+            GemmPrep g;
+            s = gemm_prepare(g, d, zpp, 0, r, nc * r, nc, r, b2, qdim, U, true,
+                             OutMap{static_cast<__nv_bfloat16*>(Y) + c0 * d_out, 0, 1, d_out, qdim, d_out}, 1,
+                             /*a_blocked=*/1);
+            if (s != BLR_OK) return s;
+            g3c.push_back(g);
+        }
+    }
+
     if (s2_mma) {
         // ---- S2 on the tensor cores (blast_s2_mma_kernel): tile-blocked fp16 Z [l][T][r/8][128][8]
         //      in, tile-blocked bf16 Z'' [k][T][r/8][128][8] out
@@ -1335,9 +1400,12 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             const uint32_t bz[4] = {64, 16, 1, static_cast<uint32_t>(b1)};
             const uint64_t sz8[3] = {64, 1024, static_cast<uint64_t>(np) * 1024};  // e4m3: 1-KB panels
             if (!encode(&tmz, zl, 4, dz, z8 ? sz8 : sz, bz, CU_TENSOR_MAP_SWIZZLE_NONE, z8 ? 3 : 2)) return BLR_ERR_CUDA;
-            const uint64_t dp[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b2)};
+            // Z'' of all tokens, or of one chunk (its own tile numbering, group stride chunk tiles)
+            const int64_t npp = chunk > 0 ? (chunk / blr::BM) * (r / 8) : np;
+            const uint64_t dp[4] = {64, 16, static_cast<uint64_t>(npp), static_cast<uint64_t>(b2)};
+            const uint64_t spp[3] = {128, 2048, static_cast<uint64_t>(npp) * 2048};
             const uint32_t bp[4] = {64, 16, 1, static_cast<uint32_t>(b2)};
-            if (!encode(&tmzpp, zpp, 4, dp, sz, bp, CU_TENSOR_MAP_SWIZZLE_NONE)) return BLR_ERR_CUDA;
+            if (!encode(&tmzpp, zpp, 4, dp, spp, bp, CU_TENSOR_MAP_SWIZZLE_NONE)) return BLR_ERR_CUDA;
         }
         {
             std::lock_guard<std::mutex> lk(g_mu);
@@ -1356,29 +1424,45 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
         }
         s = gemm_run(g1, d, dev, st);
         if (s != BLR_OK) return s;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(items, static_cast<int64_t>(per_sm) * d.sm_count)));
-        cfg.blockDim = dim3(blr::S2M_THREADS);
-        cfg.dynamicSmemBytes = sl8.total + 1024;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[0].val.programmaticStreamSerializationAllowed = s2_pdl ? 1 : 0;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
-        if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
-        if (cudaLaunchKernelEx(&cfg, s2fn, tmz, tmzpp, static_cast<const void*>(zl),
-                               static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
-                               static_cast<int>(n_tok), static_cast<int>(b1), static_cast<int>(b2),
-                               static_cast<int>(r), s2_order) != cudaSuccess)
-            return BLR_ERR_CUDA;
-        if (prof) {
-            if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
-            ++t_prof_n;
+        auto run_s2 = [&](int64_t t0, int64_t ntok) -> blr_status {
+            const int64_t its = cdiv(ntok, 128) * (r / 8);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(its, static_cast<int64_t>(per_sm) * d.sm_count)));
+            cfg.blockDim = dim3(blr::S2M_THREADS);
+            cfg.dynamicSmemBytes = sl8.total + 1024;
+            cfg.stream = st;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = s2_pdl ? 1 : 0;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+            if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+            if (cudaLaunchKernelEx(&cfg, s2fn, tmz, tmzpp, static_cast<const void*>(zl),
+                                   static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
+                                   static_cast<int>(ntok), static_cast<int>(b1), static_cast<int>(b2),
+                                   static_cast<int>(r), s2_order, static_cast<int>(t0)) != cudaSuccess)
+                return BLR_ERR_CUDA;
+            if (prof) {
+                if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+                ++t_prof_n;
+            }
+            ++t_last_launches;
+            return BLR_OK;
+        };
+        if (chunk > 0) {
+            size_t ci = 0;
+            for (int64_t c0 = 0; c0 < n_tok; c0 += chunk, ++ci) {
+                s = run_s2(c0 / blr::BM, std::min(chunk, n_tok - c0));
+                if (s != BLR_OK) return s;
+                s = gemm_run(g3c[ci], d, dev, st);
+                if (s != BLR_OK) return s;
+            }
+            return BLR_OK;
         }
-        ++t_last_launches;
-        return gemm_run(g3, d, dev, st);
+        (void)items;
+        s = run_s2(0, n_tok);
+        return s != BLR_OK ? s : gemm_run(g3, d, dev, st);
     }
     // ---- CUDA-core S2 (blast_s2_kernel; used for compensated Z'' (r < 128) or with BLR_S2=cuda):
     // fp16 Z viewed (rho, t, l), box (64, S2_ROWS, b1): one item's b1 row segments per request

@@ -80,6 +80,10 @@ struct KParams {
                          // N = BN/2 from the same A into adjacent TMEM columns; B is staged as two
                          // halves of b_half_bytes (half h covers tile columns [h BN/2, (h+1) BN/2))
     uint32_t b_half_bytes;
+    int mc;              // PAIR 2, streamed B: CTA pairs per cluster sharing the tile's B (same group and
+                         // N block, consecutive token tiles): each loads 1/mc of the K rows of every B
+                         // box and TMA-multicasts it to the same-rank CTA of every pair (L2 -> SM bytes
+                         // per MAC drop; the streamed GEMMs run at the chip's L2 read rate)
     int b_boxes;         // TMA boxes per k-block for B (MN-major; per half when n_mma = 2)
     int b_box_n;         // N elements per box (MN-major)
     uint32_t b_stage_bytes;  // bytes of one B k-block in smem
@@ -103,6 +107,7 @@ struct KParams {
     const __nv_bfloat16* S;  // BLAST: S [b1][b2][r]
     unsigned long long* trace;  // debug: per-CTA %globaltimer stamps [grid][64] (nullptr = off)
     int first;                  // 1: first launch of an API call (see the PDL note in the kernel)
+    int mma_burst;              // 1: full K blocks issued as one unrolled MMA burst (MMA issuer)
     int dbg;                    // debug bits (BLR_DEBUG_KNOBS builds only): 1 skip bulk stores, 2 skip staging,
                                 //   4 skip the whole GEMM epilogue, 8 skip MMAs, 16 plain-arrive slot release (PAIR 1),
                                 //   32 no accumulator hand-off, 64 no resident weight loads
@@ -175,8 +180,9 @@ struct TileIter {
 };
 __device__ __forceinline__ TileIter tile_iter(const KParams& p, int pair) {
     TileIter t;
-    t.unit = blockIdx.x / pair;
-    t.units = gridDim.x / pair;
+    const int csz = pair * (p.mc > 1 ? p.mc : 1);  // CTAs per unit (cluster)
+    t.unit = blockIdx.x / csz;
+    t.units = gridDim.x / csz;
     t.slices = p.groups * p.tiles_n;
     return t;
 }
@@ -297,7 +303,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const uint32_t crank = PAIR == 2 ? ptx::cluster_ctarank() : 0u;  // rank within the pair
+    // rank within the pair (crank), pair index within a B-multicast cluster (pidx), its leader's rank
+    const uint32_t cl_rank = PAIR == 2 ? ptx::cluster_ctarank() : 0u;
+    const uint32_t crank = cl_rank & 1u;
+    const uint32_t pidx = cl_rank >> 1;
+    const int mcs = (PAIR == 2 && p.mc > 1) ? p.mc : 1;
+    const uint32_t lead_rank = cl_rank & ~1u;
     const bool leader = crank == 0;
     unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 128 : nullptr;
     // trace stamps: [0] %globaltimer at entry, [8] %clock64 at entry; every other stamp is a
@@ -313,7 +324,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int nres = p.b_resident ? kb_resident(p) : 0;
         for (int s = lane; s < p.stages; s += 32) {
             ptx::mbar_init(full_bar + 8 * s, 1);
-            ptx::mbar_init(empty_bar + 8 * s, 1);
+            ptx::mbar_init(empty_bar + 8 * s, mcs);  // multicast: every pair leader frees the slot
         }
         if (lane < 2) {
             ptx::mbar_init(tfull_bar + 8 * lane, 1);
@@ -396,7 +407,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int nstep_tr = 0;
             for (int it = 0; it < ntiles; ++it) {
                 const TileCoord tc = tile_get(p, titer, tile_tab, it);
-                const int m0 = (tc.m_blk * PAIR + static_cast<int>(crank)) * BM;
+                const int m0 = ((tc.m_blk * mcs + static_cast<int>(pidx)) * PAIR + static_cast<int>(crank)) * BM;
                 const int n0 = tc.n_blk * p.BN + static_cast<int>(crank) * (p.BN / PAIR);  // this CTA's B half
                 // Monarch: first output block k of this CTA's share of the tile's k blocks
                 const int kblk0 = tc.n_blk * p.kb_per_tile + static_cast<int>(crank) * (p.kb_per_tile / PAIR);
@@ -450,7 +461,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                         // this CTA's 128-row tile are 128 consecutive 128-B rows of
                                         // the map (panels past K read the following panels or TMA's
                                         // zero fill: finite values against B's zero-filled rows)
-                                        const int t128 = tc.m_blk * PAIR + static_cast<int>(crank);
+                                        const int t128 = (tc.m_blk * mcs + static_cast<int>(pidx)) * PAIR + static_cast<int>(crank);
                                         const int row = ((tc.g * p.a_tiles + t128) * a_nch + (k0 >> 3)) * 16;
                                         load3(a_dst, &tmA, fb, 0, row, 0);
                                     } else if (p.a_gmid)
@@ -463,6 +474,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                             const int n0h = tc.n_blk * p.BN + h * (p.BN / p.n_mma) +
                                                             static_cast<int>(crank) * (p.BN / p.n_mma / PAIR);
                                             const uint32_t bh = b_dst + h * p.b_half_bytes;
+                                            if constexpr (PAIR == 2) {
+                                                if (mcs > 1) {
+                                                    // this pair's slice of every B box, multicast to the
+                                                    // same-rank CTA of every pair of the cluster
+                                                    uint16_t mask = 0;
+                                                    for (int j2 = 0; j2 < mcs; ++j2) mask |= static_cast<uint16_t>(1u << (2 * j2 + crank));
+                                                    if (p.b_mn_major) {
+                                                        const int kr = BK / mcs;  // K rows per slice
+                                                        for (int q = 0; q < p.b_boxes; ++q)
+                                                            ptx::tma_load_3d_pair_mc(bh + q * (p.b_box_n * BK * 2) + pidx * kr * (p.b_box_n * 2),
+                                                                                     &tmB, fb, n0h + q * p.b_box_n, k0 + pidx * kr, tc.g, mask);
+                                                    } else {
+                                                        const int nr = p.BN / p.n_mma / PAIR / mcs;  // N rows per slice
+                                                        ptx::tma_load_3d_pair_mc(bh + pidx * nr * 128, &tmB, fb, k0, n0h + pidx * nr, tc.g, mask);
+                                                    }
+                                                    continue;
+                                                }
+                                            }
                                             if (p.b_mn_major) {
                                                 for (int q = 0; q < p.b_boxes; ++q)
                                                     load3(bh + q * (p.b_box_n * BK * 2), &tmB, fb, n0h + q * p.b_box_n, k0,
@@ -496,8 +525,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // Warp-wide schedule (uniform registers); one elected lane issues the MMAs and commits.
         if (leader) {
             const uint32_t idesc = ptx::idesc_bf16(BM * PAIR, p.BN / p.n_mma, p.b_mn_major);
-            auto commit = [&](uint32_t bar) {
-                if constexpr (PAIR == 2) ptx::mma_commit_pair(bar);  // arrives in both CTAs
+            const uint16_t pair_mask = static_cast<uint16_t>(3u << (2 * pidx));
+            const uint16_t all_mask = static_cast<uint16_t>((1u << (2 * mcs)) - 1u);
+            auto commit = [&](uint32_t bar) {  // own pair (accumulator / resident-B hand-offs)
+                if constexpr (PAIR == 2) ptx::mma_commit_pair_mask(bar, pair_mask);
+                else ptx::mma_commit(bar);
+            };
+            auto commit_slot = [&](uint32_t bar) {  // a ring slot: every CTA whose loads land in it
+                if constexpr (PAIR == 2) ptx::mma_commit_pair_mask(bar, all_mask);
                 else ptx::mma_commit(bar);
             };
             // descriptors are built once; per-MMA only the 14-bit start-address field advances
@@ -515,6 +550,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int n_steps = (p.k_blocks + p.kbox - 1) / p.kbox;
             const int kbr = kb_resident(p);
             const bool wait_b = p.b_resident && !BLR_DBG_ON(p, 64);
+            // loop-invariant parameters, hoisted (the asm memory clobbers would otherwise make the
+            // compiler re-read them from the parameter bank every step)
+            const int kbox_h = p.kbox, kb_half_h = p.kb_half, a_lo_off_h = p.a_lo_off;
+            const bool b_res_h = p.b_resident != 0, two_h = p.n_mma == 2;
+            const uint32_t b_stage_h = p.b_stage_bytes;
+            const uint32_t a_ks = a_kstep >> 4, b_ks = p.b_kstep >> 4, b_hh = p.b_half_bytes >> 4;
+            const uint32_t d_half = static_cast<uint32_t>(p.BN / 2);
+            // K blocks issued as one unrolled burst of four K = 16 MMAs (all 8 panels valid).  Streamed
+            // pair plans keep the per-step loop: the burst measured ~5% slower there at full size
+            // (C4 gate S3 2.49 -> 2.62 ms, down S1 2.35 -> 2.49 ms, same box), while it speeds up
+            // the weight-resident and Monarch-projection plans (C4 gate S1 1.6 -> 1.44 ms)
+            const int full_kb = !p.mma_burst ? -1 : p.a_blocked ? (p.a_nchunks >> 3) : 0x7fffffff;
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -544,17 +591,40 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             }
                         }
                         ptx::tc_fence_after();
+                        // Descriptors of this step are formed warp-wide (uniform registers, params
+                        // hoisted out of the loop): the MMA issue is a short dependency-free burst
+                        // (per-step issue overhead directly stalls the tensor pipe)
+                        const uint32_t a_st = static_cast<uint32_t>(stage) * (a_blk * kbox_h);
+                        const uint32_t b_st = static_cast<uint32_t>(stage) * (b_stage_h * kbox_h);
                         if (ptx::elect_one()) {
                             if (trace) {
                                 if (mstep_tr == 0) trace[3] = clock64();
                                 if (mstep_tr < 32) trace[96 + mstep_tr] = clock64();
                             }
-                            for (int j = 0; j < p.kbox; ++j) {
-                                const int kb = si * p.kbox + j;
-                                const int bkb = (p.a_lo_off > 0 && kb >= p.kb_half) ? kb - p.kb_half : kb;
-                                const uint32_t a_off = stage * (a_blk * p.kbox) + j * a_blk;
-                                const uint32_t b_off = p.b_resident ? bkb * p.b_stage_bytes
-                                                                    : stage * (p.b_stage_bytes * p.kbox) + j * p.b_stage_bytes;
+                            for (int j = 0; j < kbox_h; ++j) {
+                                const int kb = si * kbox_h + j;
+                                const int bkb = (a_lo_off_h > 0 && kb >= kb_half_h) ? kb - kb_half_h : kb;
+                                const uint32_t a_off = a_st + j * a_blk;
+                                const uint32_t b_off = b_res_h ? bkb * b_stage_h : b_st + j * b_stage_h;
+                                const uint32_t a_lo = a_lo0 + (a_off >> 4), b_lo = b_lo0 + (b_off >> 4);
+                                const uint32_t accf = (si | j) != 0 ? 1u : 0u;
+                                if (kb < full_kb) {  // fast path: all four K = 16 steps
+#pragma unroll
+                                    for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                                        const uint64_t ad = ptx::desc_make(a_lo + kk * a_ks, a_hi);
+                                        const uint64_t bd = ptx::desc_make(b_lo + kk * b_ks, b_hi);
+                                        const uint32_t acc1 = accf | (kk != 0 ? 1u : 0u);
+                                        if (BLR_DBG_ON(p, 8)) continue;  // debug: skip the MMA itself
+                                        if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc, acc1);
+                                        else ptx::mma_bf16(d_tmem, ad, bd, idesc, acc1);
+                                        if (two_h) {  // second half: same A, B half 1, next TMEM columns
+                                            const uint64_t bd2 = ptx::desc_make(b_lo + b_hh + kk * b_ks, b_hi);
+                                            if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem + d_half, ad, bd2, idesc, acc1);
+                                            else ptx::mma_bf16(d_tmem + d_half, ad, bd2, idesc, acc1);
+                                        }
+                                    }
+                                    continue;
+                                }
                                 // tile-blocked A: the box of a K block that runs past K also holds the
                                 // NEXT token tile's panels; only the K = 16 steps over valid panels
                                 // are issued (a half-valid last step takes its second core matrix
@@ -589,7 +659,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 }
                             }
                             if (BLR_DBG_ON(p, 16)) ptx::mbar_arrive(empty_bar + 8 * stage);  // debug: plain release
-                            else commit(empty_bar + 8 * stage);  // frees the smem slot (both CTAs of a pair)
+                            else commit_slot(empty_bar + 8 * stage);  // frees the smem slot (every CTA of the cluster)
                         }
                         __syncwarp();
                         ++mstep_tr;
@@ -626,7 +696,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::griddep_wait();  // our stores must not overtake the previous kernel's reads
         for (int it = 0; !BLR_DBG_ON(p, 32) && it < ntiles; ++it) {
             const TileCoord tc = tile_get(p, titer, tile_tab, it);
-            const int m0 = (tc.m_blk * PAIR + static_cast<int>(crank)) * BM;
+            const int m0 = ((tc.m_blk * mcs + static_cast<int>(pidx)) * PAIR + static_cast<int>(crank)) * BM;
             const int row0 = m0 + quarter * 32;
             const int n0 = tc.n_blk * p.BN;
             if constexpr (KIND == KIND_BLAST_PROJ) {
@@ -880,7 +950,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if constexpr (PAIR == 2) ptx::mbar_arrive_remote(tempty_bar + 8 * acc, 0);  // leader's barrier
+                if constexpr (PAIR == 2) ptx::mbar_arrive_remote(tempty_bar + 8 * acc, lead_rank);  // leader's barrier
                 else ptx::mbar_arrive(tempty_bar + 8 * acc);
             }
             if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
@@ -1076,25 +1146,27 @@ __global__ void __launch_bounds__(32 * 16, 1)
 // them, so its b1 panel reads and b2 panel writes are sequential streams.
 // Roles: warp 0 TMA producer, warp 1 TMEM owner + MMA issuer, warps 2-3 build B_c, warps 4-7
 // epilogue (TMEM -> bf16 -> smem [k][t][8] -> b2 bulk stores of the (k, T, c) panels).
-constexpr int S2M_ASTAGES = 3;
+constexpr int S2M_ASTAGES = 4;  // barrier slots (fp16 Z uses 3 stages, e4m3 Z 4)
 constexpr int S2M_THREADS = 256;
 struct S2MLayout {  // byte offsets in dynamic smem (1024-aligned base)
     uint32_t a, a16, b, c, bars, tslot, total, a_bytes, b_bytes, c_bytes, stages;
 };
-// fp8: Z arrives as e4m3 panels (1 KB) in `stages` raw slots and is widened by the builder warps
-// into two fp16 A buffers (2 KB panels) for the f16 MMA (no 8-bit kind: S stays 16-bit)
+// fp8: Z arrives as e4m3 panels (1 KB) in 4 raw slots (deeper than fp16's 3 x 2 KB: the bytes in
+// flight per SM set the rate of this HBM-bound kernel) and is widened by the builder warps into two
+// fp16 A buffers (2 KB panels) for the f16 MMA (no 8-bit kind: S stays 16-bit); B_c then has one
+// buffer (it changes only when a CTA's run crosses a chunk)
 __host__ __device__ inline S2MLayout s2m_layout(int b1, int b2, bool fp8 = false) {
     S2MLayout L;
     const int b1p = (b1 + 1) & ~1;  // K in pairs of 8-wide core matrices (UMMA K = 16)
     const int b2p = (b2 + 1) & ~1;  // UMMA N = 8 b2p, a multiple of 16
-    L.stages = fp8 ? 2 : S2M_ASTAGES;
+    L.stages = fp8 ? 4 : 3;
     L.a_bytes = static_cast<uint32_t>(b1p) * 128 * (fp8 ? 8 : 16);
     L.b_bytes = static_cast<uint32_t>(b2p) * b1p * 128;
     L.c_bytes = static_cast<uint32_t>(b2) * 128 * 16;
     L.a = 0;
     L.a16 = L.a + L.stages * L.a_bytes;
     L.b = L.a16 + (fp8 ? 2u * b1p * 2048u : 0u);
-    L.c = L.b + 2 * L.b_bytes;
+    L.c = L.b + (fp8 ? 1 : 2) * L.b_bytes;
     L.bars = L.c + 2 * L.c_bytes;
     L.tslot = L.bars + 8 * (2 * S2M_ASTAGES + 2 * 2 + 2 * 2 + 2 * 2);
     L.total = L.tslot + 16;
@@ -1109,7 +1181,10 @@ template <int MAXB2, bool FP8 = false>
 __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
     blast_s2_mma_kernel(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmZpp,
                         const void* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
-                        const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order) {
+                        const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order,
+                        int t0 = 0) {
+    // t0: first 128-token tile of Z this launch reads (token-chunked S2/S3);
+    // Z'' tiles are numbered from 0 in the launch's output
     extern __shared__ __align__(1024) uint8_t s2m_smem[];
     const S2MLayout L = s2m_layout(b1, b2, FP8);
     const int nst = static_cast<int>(L.stages);
@@ -1120,6 +1195,7 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
     const uint32_t d_full = b_empty + 16, d_empty = d_full + 16;
     const uint32_t w_full = d_empty + 16, w_empty = w_full + 16;  // FP8: widened fp16 A buffers
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NB = FP8 ? 1 : 2;  // B_c buffers
     const int nchunks = r / 8;
     const int tiles = (n_tok + 127) / 128;
     const int total = tiles * nchunks;
@@ -1155,7 +1231,7 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
         ptx::fence_barrier_init();
     }
     // zero both B_c buffers (the off-diagonal pattern never changes) and the A pad plane (b1 odd)
-    for (uint32_t o = threadIdx.x * 16; o < 2 * L.b_bytes; o += S2M_THREADS * 16)
+    for (uint32_t o = threadIdx.x * 16; o < NB * L.b_bytes; o += S2M_THREADS * 16)
         ptx::st_shared_v4(base + L.b + o, make_uint4(0, 0, 0, 0));
     if (b1p != b1) {
         if constexpr (FP8) {
@@ -1187,21 +1263,21 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
                 ptx::mbar_arrive_expect_tx(a_full + 8 * s, static_cast<uint32_t>(b1 * (FP8 ? 1024 : 2048)));
                 // the b1 panels (l, T, c) in ONE tensor copy: Z viewed (64, 16, tiles*r/8, b1),
                 // box (64, 16, 1, b1) -> smem [l][2 KB] (fp8: 1-KB panels, 64-B rows)
-                ptx::tma_load_4d(base + L.a + s * L.a_bytes, &tmZ, a_full + 8 * s, 0, 0, T * nchunks + c, 0);
+                ptx::tma_load_4d(base + L.a + s * L.a_bytes, &tmZ, a_full + 8 * s, 0, 0, (T + t0) * nchunks + c, 0);
             }
         }
         __syncwarp();
     } else if (warp == 1) {  // ------------------------------------------------ MMA issuer
         const uint32_t idesc = ptx::idesc_f16(128, static_cast<uint32_t>((b2 + 1) & ~1) * 8);
         for (int j = 0; j < cnt; ++j) {
-            const int s = j % nst, bb = j & 1, acc = j & 1;
+            const int s = j % nst, bb = j % NB, wb = j & 1, acc = j & 1;
             if (j >= 2) ptx::mbar_wait(d_empty + 8 * acc, ((j >> 1) - 1) & 1);
-            if constexpr (FP8) ptx::mbar_wait(w_full + 8 * bb, (j >> 1) & 1);
+            if constexpr (FP8) ptx::mbar_wait(w_full + 8 * wb, (j >> 1) & 1);
             else ptx::mbar_wait(a_full + 8 * s, (j / nst) & 1);
-            ptx::mbar_wait(b_full + 8 * bb, (j >> 1) & 1);
+            ptx::mbar_wait(b_full + 8 * bb, (j / NB) & 1);
             ptx::tc_fence_after();
             if (ptx::elect_one()) {
-                const uint32_t a0 = FP8 ? base + L.a16 + bb * b1p * 2048 : base + L.a + s * L.a_bytes;
+                const uint32_t a0 = FP8 ? base + L.a16 + wb * b1p * 2048 : base + L.a + s * L.a_bytes;
                 const uint32_t b0 = base + L.b + bb * L.b_bytes;
                 for (int kk = 0; kk < b1p / 2; ++kk) {
                     // A: core matrices (t/8, l) at l*2048 + (t/8)*128 -> LBO (K) 2048, SBO (M) 128
@@ -1210,7 +1286,7 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
                     const uint64_t bd = ptx::smem_desc(b0 + kk * 256, 128, b1p * 128, 0);
                     ptx::mma_bf16(tmem + acc * 128, ad, bd, idesc, kk > 0 ? 1u : 0u);
                 }
-                if constexpr (FP8) ptx::mma_commit(w_empty + 8 * bb);
+                if constexpr (FP8) ptx::mma_commit(w_empty + 8 * wb);
                 else ptx::mma_commit(a_empty + 8 * s);
                 ptx::mma_commit(b_empty + 8 * bb);
                 ptx::mma_commit(d_full + 8 * acc);
@@ -1223,11 +1299,11 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
         for (int j = 0; j < cnt; ++j) {
             int T, c;
             item(j, T, c);
-            const int bb = j & 1;
-            if (j >= 2) ptx::mbar_wait(b_empty + 8 * bb, ((j >> 1) - 1) & 1);
+            const int bb = j % NB, wb = j & 1;
+            if (j >= NB) ptx::mbar_wait(b_empty + 8 * bb, ((j / NB) - 1) & 1);
             const uint32_t b0 = base + L.b + bb * L.b_bytes;
             int Tp = 0, cp = -1;
-            if (j >= 2) item(j - 2, Tp, cp);  // the item that last used this buffer
+            if (j >= NB) item(j - NB, Tp, cp);  // the item that last used this buffer
             for (int lk = tb; lk < b1 * b2 && c != cp; lk += 64) {
                 const int l = lk / b2, k = lk - l * b2;
                 const uint4 w = __ldg(reinterpret_cast<const uint4*>(S + static_cast<long long>(lk) * r + c * 8));
@@ -1248,8 +1324,8 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
                 // widen the item's b1 e4m3 panels (1 KB) into fp16 panels (2 KB) of buffer bb
                 const int s = j % nst;
                 ptx::mbar_wait(a_full + 8 * s, (j / nst) & 1);
-                if (j >= 2) ptx::mbar_wait(w_empty + 8 * bb, ((j >> 1) - 1) & 1);
-                const uint32_t src = base + L.a + s * L.a_bytes, dst = base + L.a16 + bb * b1p * 2048;
+                if (j >= 2) ptx::mbar_wait(w_empty + 8 * wb, ((j >> 1) - 1) & 1);
+                const uint32_t src = base + L.a + s * L.a_bytes, dst = base + L.a16 + wb * b1p * 2048;
                 for (int e = tb; e < b1 * 128; e += 64) {  // one 8-value panel row per step
                     const uint2 v = ptx::ld_shared_v2u32(src + e * 8);
                     uint4 o;
@@ -1262,7 +1338,7 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
                 ptx::fence_async_smem();
                 ptx::named_bar_sync(3, 64);  // every converter is done reading the raw slot
                 if (tb == 0) ptx::mbar_arrive(a_empty + 8 * s);
-                ptx::mbar_arrive(w_full + 8 * bb);
+                ptx::mbar_arrive(w_full + 8 * wb);
             }
         }
     } else {  // --------------------------------------------------------- epilogue (warps 4-7)
