@@ -449,6 +449,9 @@ def measure(w, n, dev, stream, args, ws, rank, flush, full=True):
     lib = arm.lib
     ph = arm.phases()
     n_launch = len(ph)
+    if os.environ.get("BLR_DUMP_PHASES"):  # launch labels for the ncu summaries (scripts/profile_summary.py)
+        json.dump([f"{w.layers[j].model}.{w.layers[j].name}.{w.layers[j].method}.{nm}" for j, nm in ph],
+                  open(os.environ["BLR_DUMP_PHASES"], "w"))
     K, W = args.steps, args.warmup
     graph = None if args.eager else graph_of(arm.step)
     run = graph.replay if graph is not None else arm.step
@@ -564,7 +567,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
-    ap.add_argument("--variants", default="C4M,C4X,C4F8", help="comma-separated extra workloads (N = 1 only)")
+    ap.add_argument("--variants", default="C4M,C4X,C4F8,C2", help="comma-separated extra workloads (N = 1 only)")
     ap.add_argument("--eager", action="store_true", help="launch every step from the host (no CUDA graph)")
     ap.add_argument("--flush", default="write+read", choices=["write+read", "write"],
                     help="L2 flush between timed steps (see L2Flush)")

@@ -1357,26 +1357,6 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
                               OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
     if (s != BLR_OK) return s;
 
-    // Token-chunked S2 -> S3 (BLR_S23_CHUNK = tokens per chunk, a multiple of 256; 0 = off): S1 runs
-    // over all tokens, then S2 and S3 alternate chunk by chunk through ONE chunk-sized Z'' buffer,
-    // small enough to stay in L2 next to U, so S3 reads its A operand from L2 and Z'' is overwritten
-    // in L2 instead of written back
-    int64_t chunk = 0;
-    if (const char* ce = getenv("BLR_S23_CHUNK")) chunk = rup(std::max<int64_t>(0, atoll(ce)), 256);
-    if (!s2_mma || chunk <= 0 || chunk >= n_tok) chunk = 0;
-    std::vector<GemmPrep> g3c;
-    if (chunk > 0) {
-        for (int64_t c0 = 0; c0 < n_tok; c0 += chunk) {
-            const int64_t nc = std::min(chunk, n_tok - c0);
-            GemmPrep g;
-            s = gemm_prepare(g, d, zpp, 0, r, nc * r, nc, r, b2, qdim, U, true,
-                             OutMap{static_cast<__nv_bfloat16*>(Y) + c0 * d_out, 0, 1, d_out, qdim, d_out}, 1,
-                             /*a_blocked=*/1);
-            if (s != BLR_OK) return s;
-            g3c.push_back(g);
-        }
-    }
-
     if (s2_mma) {
         // ---- S2 on the tensor cores (blast_s2_mma_kernel): tile-blocked fp16 Z [l][T][r/8][128][8]
         //      in, tile-blocked bf16 Z'' [k][T][r/8][128][8] out
@@ -1400,12 +1380,9 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             const uint32_t bz[4] = {64, 16, 1, static_cast<uint32_t>(b1)};
             const uint64_t sz8[3] = {64, 1024, static_cast<uint64_t>(np) * 1024};  // e4m3: 1-KB panels
             if (!encode(&tmz, zl, 4, dz, z8 ? sz8 : sz, bz, CU_TENSOR_MAP_SWIZZLE_NONE, z8 ? 3 : 2)) return BLR_ERR_CUDA;
-            // Z'' of all tokens, or of one chunk (its own tile numbering, group stride chunk tiles)
-            const int64_t npp = chunk > 0 ? (chunk / blr::BM) * (r / 8) : np;
-            const uint64_t dp[4] = {64, 16, static_cast<uint64_t>(npp), static_cast<uint64_t>(b2)};
-            const uint64_t spp[3] = {128, 2048, static_cast<uint64_t>(npp) * 2048};
+            const uint64_t dp[4] = {64, 16, static_cast<uint64_t>(np), static_cast<uint64_t>(b2)};
             const uint32_t bp[4] = {64, 16, 1, static_cast<uint32_t>(b2)};
-            if (!encode(&tmzpp, zpp, 4, dp, spp, bp, CU_TENSOR_MAP_SWIZZLE_NONE)) return BLR_ERR_CUDA;
+            if (!encode(&tmzpp, zpp, 4, dp, sz, bp, CU_TENSOR_MAP_SWIZZLE_NONE)) return BLR_ERR_CUDA;
         }
         {
             std::lock_guard<std::mutex> lk(g_mu);
@@ -1450,16 +1427,6 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             ++t_last_launches;
             return BLR_OK;
         };
-        if (chunk > 0) {
-            size_t ci = 0;
-            for (int64_t c0 = 0; c0 < n_tok; c0 += chunk, ++ci) {
-                s = run_s2(c0 / blr::BM, std::min(chunk, n_tok - c0));
-                if (s != BLR_OK) return s;
-                s = gemm_run(g3c[ci], d, dev, st);
-                if (s != BLR_OK) return s;
-            }
-            return BLR_OK;
-        }
         (void)items;
         s = run_s2(0, n_tok);
         return s != BLR_OK ? s : gemm_run(g3, d, dev, st);
