@@ -1399,9 +1399,7 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
                 g_attr_set[20][dev] = true;
             }
         }
-        s = gemm_run(g1, d, dev, st);
-        if (s != BLR_OK) return s;
-        auto run_s2 = [&](int64_t t0, int64_t ntok) -> blr_status {
+        auto run_s2 = [&](int64_t t0o, int64_t ntok, const CUtensorMap& mz) -> blr_status {  // t0o: Z'' tile offset
             const int64_t its = cdiv(ntok, 128) * (r / 8);
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(its, static_cast<int64_t>(per_sm) * d.sm_count)));
@@ -1415,10 +1413,10 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             cfg.numAttrs = 1;
             const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
             if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
-            if (cudaLaunchKernelEx(&cfg, s2fn, tmz, tmzpp, static_cast<const void*>(zl),
+            if (cudaLaunchKernelEx(&cfg, s2fn, mz, tmzpp, static_cast<const void*>(zl),
                                    static_cast<__nv_bfloat16*>(zpp), static_cast<const __nv_bfloat16*>(S),
                                    static_cast<int>(ntok), static_cast<int>(b1), static_cast<int>(b2),
-                                   static_cast<int>(r), s2_order, static_cast<int>(t0)) != cudaSuccess)
+                                   static_cast<int>(r), s2_order, 0, static_cast<int>(t0o)) != cudaSuccess)
                 return BLR_ERR_CUDA;
             if (prof) {
                 if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
@@ -1428,7 +1426,9 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             return BLR_OK;
         };
         (void)items;
-        s = run_s2(0, n_tok);
+        s = gemm_run(g1, d, dev, st);
+        if (s != BLR_OK) return s;
+        s = run_s2(0, n_tok, tmz);
         return s != BLR_OK ? s : gemm_run(g3, d, dev, st);
     }
     // ---- CUDA-core S2 (blast_s2_kernel; used for compensated Z'' (r < 128) or with BLR_S2=cuda):

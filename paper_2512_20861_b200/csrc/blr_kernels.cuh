@@ -1182,9 +1182,9 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
     blast_s2_mma_kernel(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmZpp,
                         const void* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
                         const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order,
-                        int t0 = 0) {
-    // t0: first 128-token tile of Z this launch reads (token-chunked S2/S3);
-    // Z'' tiles are numbered from 0 in the launch's output
+                        int t0 = 0, int t0o = 0) {
+    // t0 / t0o: first 128-token tile of Z this launch reads / of Z'' it writes (token-chunked
+    // S1 -> S2); the items' tiles are numbered from 0
     extern __shared__ __align__(1024) uint8_t s2m_smem[];
     const S2MLayout L = s2m_layout(b1, b2, FP8);
     const int nst = static_cast<int>(L.stages);
@@ -1380,7 +1380,7 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
             ptx::named_bar_sync(1, 128);
             if (issuer) {
                 // panels (k, T, c) for all k in ONE tensor store (Z'' viewed like Z)
-                ptx::tma_store_4d(&tmZpp, base + L.c + cb * L.c_bytes, 0, 0, T * nchunks + c, 0);
+                ptx::tma_store_4d(&tmZpp, base + L.c + cb * L.c_bytes, 0, 0, (T + t0o) * nchunks + c, 0);
                 ptx::bulk_commit();
             }
         }
