@@ -263,7 +263,7 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     int units = d.sm_count / csz;              // CTAs (pairs, clusters) that fit one wave
     if (csz > 2) {
         // clusters of 4+ CTAs must fit inside a GPC: ask how many can be co-resident
-        static int cached[8] = {};
+        static int cached[17] = {};
         std::lock_guard<std::mutex> lk(g_mu);
         if (!cached[csz]) {
             cudaLaunchConfig_t oc = {};

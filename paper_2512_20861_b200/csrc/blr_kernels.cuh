@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (leader) {
             const uint32_t idesc = ptx::idesc_bf16(BM * PAIR, p.BN / p.n_mma, p.b_mn_major);
             const uint16_t pair_mask = static_cast<uint16_t>(3u << (2 * pidx));
-            const uint16_t all_mask = static_cast<uint16_t>((1u << (2 * mcs)) - 1u);
+            const uint16_t all_mask = mcs > 1 ? static_cast<uint16_t>((1u << (2 * mcs)) - 1u) : pair_mask;
             auto commit = [&](uint32_t bar) {  // own pair (accumulator / resident-B hand-offs)
                 if constexpr (PAIR == 2) ptx::mma_commit_pair_mask(bar, pair_mask);
                 else ptx::mma_commit(bar);
