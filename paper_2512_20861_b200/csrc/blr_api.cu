@@ -324,7 +324,7 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
 // N tile: <= 256 columns, multiple of 16, balanced.  While the grid would leave SMs idle, split
 // N further (down to 64) -- but only toward a width whose B slice (K x BN) can stay resident,
 // since in streaming mode every extra N tile re-reads the whole A tile.
-int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int64_t groups, int sms, int pair) {
+int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int64_t groups, int sms, int pair, bool blocked = false) {
     int64_t tiles = cdiv(N, 256);
     int bn = static_cast<int>(rup(cdiv(N, tiles), 16));
     // split while the grid leaves SMs idle, but never past one wave (a partial second wave
@@ -362,7 +362,7 @@ int choose_bn(int64_t N, int64_t K, int64_t other_tiles, int64_t groups, int sms
         if (best > 0 && slices0 < sms && 2 * slices0 > sms) {
             for (int64_t tn = cdiv(N, 256); tn <= cdiv(N, 128); ++tn) {
                 const int b = static_cast<int>(rup(cdiv(N, tn), 16));
-                if (chunk_width(b) < 32) continue;
+                if (!blocked && chunk_width(b) < 32) continue;  // (tile-blocked outputs store BN/2-wide chunks)
                 const double s = score(b);
                 if (s > best + 0.05) {
                     best = s;
@@ -405,7 +405,7 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     if (wide) {  // N tiles of <= 512, halves multiples of 16 (per-CTA halves multiples of 8)
         p.BN = static_cast<int>(rup(cdiv(N, cdiv(N, 512)), 32));
     } else {
-        p.BN = choose_bn(N, K, p.tiles_m * groups, groups, d.sm_count / pair, pair);
+        p.BN = choose_bn(N, K, p.tiles_m * groups, groups, d.sm_count / pair, pair, out.blocked != 0);
         if (pair == 2 && (p.BN / 2) % 8) p.BN = static_cast<int>(rup(p.BN, 32));
     }
     p.N = static_cast<int>(N);
@@ -429,6 +429,14 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     const int esz = 2;
     p.c_box_w = chunk_width(p.BN);
     while (p.c_box_w * esz > 128) p.c_box_w /= 2;  // staged rows <= 128 B
+    // tile-blocked outputs (BLAST S1's Z) store whole panels: one BN/2-wide chunk per column half
+    // (<= 128 columns, staged in 64-column passes), so no width is forced down to 16-column boxes
+    const char* bce = getenv("BLR_BLK_CW_OLD");
+    // -- only where the default chunking is narrow or leaves the two column halves unbalanced (an odd
+    // chunk count): a wider staging chunk costs ring stages
+    const bool unbalanced = (p.BN / p.c_box_w) % 2 == 1 || p.c_box_w < 32;
+    if (out.blocked && unbalanced && (p.BN / 2) % 8 == 0 && p.BN / 2 <= 128 && !(bce && bce[0] == '1'))
+        p.c_box_w = p.BN / 2;
     p.c_swz = out.blocked ? 0 : pick_swz(p.c_box_w * esz).mask;
     if (mc > 1 && !b_mn_major && (bn_full / p.n_mma / pair) % (8 * mc)) return false;  // K-major slices
     return finish_plan(p, !wide && mc == 1, 32 * p.c_box_w * esz, d.sm_count / (pair * mc));

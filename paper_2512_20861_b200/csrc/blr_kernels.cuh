@@ -837,15 +837,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             else ptx::bulk_wait_read<0>();
                         }
                         ptx::named_bar_sync(2 + half, 128);
+                        for (int h0 = 0; h0 < CW; h0 += 64) {  // chunks wider than 64: two passes
+                            if (h0 > 0) {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            if (j * 8 < CW) {
-                                uint2 w;
-                                w.x = ptx::pack_e4m3x2(fv[j * 8 + 0], fv[j * 8 + 1]) |
-                                      (ptx::pack_e4m3x2(fv[j * 8 + 2], fv[j * 8 + 3]) << 16);
-                                w.y = ptx::pack_e4m3x2(fv[j * 8 + 4], fv[j * 8 + 5]) |
-                                      (ptx::pack_e4m3x2(fv[j * 8 + 6], fv[j * 8 + 7]) << 16);
-                                ptx::st_shared_v2u32(hbuf + j * 1024u + (quarter * 32u + lane) * 8u, w);
+                                for (int j = 0; j < 8; ++j)
+                                    if (h0 + j * 8 < CW)
+                                        ptx::tmem_ld_x8(tbase + c0 + h0 + j * 8, *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
+                                ptx::tmem_wait_ld();
+                            }
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                if (h0 + j * 8 < CW) {
+                                    uint2 w;
+                                    w.x = ptx::pack_e4m3x2(fv[j * 8 + 0], fv[j * 8 + 1]) |
+                                          (ptx::pack_e4m3x2(fv[j * 8 + 2], fv[j * 8 + 3]) << 16);
+                                    w.y = ptx::pack_e4m3x2(fv[j * 8 + 4], fv[j * 8 + 5]) |
+                                          (ptx::pack_e4m3x2(fv[j * 8 + 6], fv[j * 8 + 7]) << 16);
+                                    ptx::st_shared_v2u32(hbuf + (h0 / 8 + j) * 1024u + (quarter * 32u + lane) * 8u, w);
+                                }
                             }
                         }
                         ptx::fence_async_smem();
@@ -872,15 +881,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             else ptx::bulk_wait_read<0>();
                         }
                         ptx::named_bar_sync(2 + half, 128);
+                        for (int h0 = 0; h0 < CW; h0 += 64) {  // chunks wider than 64: two passes
+                            if (h0 > 0) {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            if (j * 8 < CW) {
-                                uint4 w;
-                                w.x = ptx::pack_f16x2(fv[j * 8 + 0], fv[j * 8 + 1]);
-                                w.y = ptx::pack_f16x2(fv[j * 8 + 2], fv[j * 8 + 3]);
-                                w.z = ptx::pack_f16x2(fv[j * 8 + 4], fv[j * 8 + 5]);
-                                w.w = ptx::pack_f16x2(fv[j * 8 + 6], fv[j * 8 + 7]);
-                                ptx::st_shared_v4(hbuf + j * 2048u + (quarter * 32u + lane) * 16u, w);
+                                for (int j = 0; j < 8; ++j)
+                                    if (h0 + j * 8 < CW)
+                                        ptx::tmem_ld_x8(tbase + c0 + h0 + j * 8, *reinterpret_cast<float(*)[8]>(&fv[j * 8]));
+                                ptx::tmem_wait_ld();
+                            }
+#pragma unroll
+                            for (int j = 0; j < 8; ++j) {
+                                if (h0 + j * 8 < CW) {
+                                    uint4 w;
+                                    w.x = ptx::pack_f16x2(fv[j * 8 + 0], fv[j * 8 + 1]);
+                                    w.y = ptx::pack_f16x2(fv[j * 8 + 2], fv[j * 8 + 3]);
+                                    w.z = ptx::pack_f16x2(fv[j * 8 + 4], fv[j * 8 + 5]);
+                                    w.w = ptx::pack_f16x2(fv[j * 8 + 6], fv[j * 8 + 7]);
+                                    ptx::st_shared_v4(hbuf + (h0 / 8 + j) * 2048u + (quarter * 32u + lane) * 16u, w);
+                                }
                             }
                         }
                         ptx::fence_async_smem();
