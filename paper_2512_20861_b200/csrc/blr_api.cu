@@ -1411,7 +1411,7 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             const int64_t its = cdiv(ntok, 128) * (r / 8);
             cudaLaunchConfig_t cfg = {};
             cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(its, static_cast<int64_t>(per_sm) * d.sm_count)));
-            cfg.blockDim = dim3(blr::S2M_THREADS);
+            cfg.blockDim = dim3(z8 ? blr::S2M_THREADS_FP8 : blr::S2M_THREADS);
             cfg.dynamicSmemBytes = sl8.total + 1024;
             cfg.stream = st;
             cudaLaunchAttribute attr[1];

@@ -1166,6 +1166,9 @@ __global__ void __launch_bounds__(32 * 16, 1)
 // epilogue (TMEM -> bf16 -> smem [k][t][8] -> b2 bulk stores of the (k, T, c) panels).
 constexpr int S2M_ASTAGES = 4;  // barrier slots (fp16 Z uses 3 stages, e4m3 Z 4)
 constexpr int S2M_THREADS = 256;
+constexpr int S2M_THREADS_FP8 = 384;  // + warps 8-11 widening e4m3 Z with the builder warps 2-3
+template <bool FP8>
+__host__ __device__ constexpr int s2m_threads() { return FP8 ? S2M_THREADS_FP8 : S2M_THREADS; }
 struct S2MLayout {  // byte offsets in dynamic smem (1024-aligned base)
     uint32_t a, a16, b, c, bars, tslot, total, a_bytes, b_bytes, c_bytes, stages;
 };
@@ -1196,7 +1199,7 @@ __host__ __device__ inline S2MLayout s2m_layout(int b1, int b2, bool fp8 = false
 // FP8: Z is e4m3; the widening to fp16 is exact, the MMA and everything after
 // it are unchanged.
 template <int MAXB2, bool FP8 = false>
-__global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
+__global__ void __launch_bounds__(s2m_threads<FP8>(), MAXB2 <= 8 ? 2 : 1)
     blast_s2_mma_kernel(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmZpp,
                         const void* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
                         const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order,
@@ -1214,6 +1217,8 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
     const uint32_t w_full = d_empty + 16, w_empty = w_full + 16;  // FP8: widened fp16 A buffers
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int NB = FP8 ? 1 : 2;  // B_c buffers
+    constexpr int NT = s2m_threads<FP8>();
+    constexpr int NCONV = FP8 ? 192 : 64;  // threads widening Z (FP8: warps 2-3 and 8-11)
     const int nchunks = r / 8;
     const int tiles = (n_tok + 127) / 128;
     const int total = tiles * nchunks;
@@ -1243,22 +1248,22 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
             ptx::mbar_init(b_empty + 8 * s, 1);
             ptx::mbar_init(d_full + 8 * s, 1);
             ptx::mbar_init(d_empty + 8 * s, 4);
-            ptx::mbar_init(w_full + 8 * s, 64);
+            ptx::mbar_init(w_full + 8 * s, NCONV);
             ptx::mbar_init(w_empty + 8 * s, 1);
         }
         ptx::fence_barrier_init();
     }
     // zero both B_c buffers (the off-diagonal pattern never changes) and the A pad plane (b1 odd)
-    for (uint32_t o = threadIdx.x * 16; o < NB * L.b_bytes; o += S2M_THREADS * 16)
+    for (uint32_t o = threadIdx.x * 16; o < NB * L.b_bytes; o += NT * 16)
         ptx::st_shared_v4(base + L.b + o, make_uint4(0, 0, 0, 0));
     if (b1p != b1) {
         if constexpr (FP8) {
             for (int s = 0; s < 2; ++s)
-                for (uint32_t o = threadIdx.x * 16; o < 128 * 16; o += S2M_THREADS * 16)
+                for (uint32_t o = threadIdx.x * 16; o < 128 * 16; o += NT * 16)
                     ptx::st_shared_v4(base + L.a16 + s * b1p * 2048 + b1 * 2048 + o, make_uint4(0, 0, 0, 0));
         } else {
             for (int s = 0; s < S2M_ASTAGES; ++s)
-                for (uint32_t o = threadIdx.x * 16; o < 128 * 16; o += S2M_THREADS * 16)
+                for (uint32_t o = threadIdx.x * 16; o < 128 * 16; o += NT * 16)
                     ptx::st_shared_v4(base + L.a + s * L.a_bytes + b1 * 2048 + o, make_uint4(0, 0, 0, 0));
         }
     }
@@ -1311,40 +1316,43 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
             }
             __syncwarp();
         }
-    } else if (warp < 4) {  // ------------------------ B_c builders (64 threads); FP8: Z widening
-        const int tb = threadIdx.x - 64;
+    } else if (warp < 4 || warp >= 8) {  // --- B_c builders (warps 2-3); FP8: Z widening (+ warps 8-11)
+        const bool builder = warp < 4;
+        const int tb = builder ? threadIdx.x - 64 : 64 + (threadIdx.x - 256);  // converter index
         const uint32_t sbo = static_cast<uint32_t>(b1p) * 128;
         for (int j = 0; j < cnt; ++j) {
             int T, c;
             item(j, T, c);
             const int bb = j % NB, wb = j & 1;
-            if (j >= NB) ptx::mbar_wait(b_empty + 8 * bb, ((j / NB) - 1) & 1);
-            const uint32_t b0 = base + L.b + bb * L.b_bytes;
-            int Tp = 0, cp = -1;
-            if (j >= NB) item(j - NB, Tp, cp);  // the item that last used this buffer
-            for (int lk = tb; lk < b1 * b2 && c != cp; lk += 64) {
-                const int l = lk / b2, k = lk - l * b2;
-                const uint4 w = __ldg(reinterpret_cast<const uint4*>(S + static_cast<long long>(lk) * r + c * 8));
-                const uint32_t cm = b0 + k * sbo + l * 128;  // core matrix (k, l): diag at rho*18 B
-                // every core matrix starts on bank 0, so entry rho's bank depends on rho alone:
-                // lane-rotated rho order -> 8 distinct banks per store (4-way instead of 32-way)
+            if (builder) {
+                if (j >= NB) ptx::mbar_wait(b_empty + 8 * bb, ((j / NB) - 1) & 1);
+                const uint32_t b0 = base + L.b + bb * L.b_bytes;
+                int Tp = 0, cp = -1;
+                if (j >= NB) item(j - NB, Tp, cp);  // the item that last used this buffer
+                for (int lk = tb; lk < b1 * b2 && c != cp; lk += 64) {
+                    const int l = lk / b2, k = lk - l * b2;
+                    const uint4 w = __ldg(reinterpret_cast<const uint4*>(S + static_cast<long long>(lk) * r + c * 8));
+                    const uint32_t cm = b0 + k * sbo + l * 128;  // core matrix (k, l): diag at rho*18 B
+                    // every core matrix starts on bank 0, so entry rho's bank depends on rho alone:
+                    // lane-rotated rho order -> 8 distinct banks per store (4-way instead of 32-way)
 #pragma unroll
-                for (int e8 = 0; e8 < 8; ++e8) {
-                    const int rho = (e8 + lane) & 7;
-                    const uint32_t wd = (rho & 4) ? ((rho & 2) ? w.w : w.z) : ((rho & 2) ? w.y : w.x);
-                    const float f = __uint_as_float((rho & 1) ? (wd & 0xFFFF0000u) : (wd << 16));
-                    ptx::st_shared_u16(cm + rho * 18, __half_as_ushort(__float2half_rn(f)));
+                    for (int e8 = 0; e8 < 8; ++e8) {
+                        const int rho = (e8 + lane) & 7;
+                        const uint32_t wd = (rho & 4) ? ((rho & 2) ? w.w : w.z) : ((rho & 2) ? w.y : w.x);
+                        const float f = __uint_as_float((rho & 1) ? (wd & 0xFFFF0000u) : (wd << 16));
+                        ptx::st_shared_u16(cm + rho * 18, __half_as_ushort(__float2half_rn(f)));
+                    }
                 }
+                ptx::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
+                ptx::mbar_arrive(b_full + 8 * bb);
             }
-            ptx::fence_async_smem();  // generic-proxy writes -> visible to the tensor core
-            ptx::mbar_arrive(b_full + 8 * bb);
             if constexpr (FP8) {
-                // widen the item's b1 e4m3 panels (1 KB) into fp16 panels (2 KB) of buffer bb
+                // widen the item's b1 e4m3 panels (1 KB) into fp16 panels (2 KB) of buffer wb
                 const int s = j % nst;
                 ptx::mbar_wait(a_full + 8 * s, (j / nst) & 1);
                 if (j >= 2) ptx::mbar_wait(w_empty + 8 * wb, ((j >> 1) - 1) & 1);
                 const uint32_t src = base + L.a + s * L.a_bytes, dst = base + L.a16 + wb * b1p * 2048;
-                for (int e = tb; e < b1 * 128; e += 64) {  // one 8-value panel row per step
+                for (int e = tb; e < b1 * 128; e += NCONV) {  // one 8-value panel row per step
                     const uint2 v = ptx::ld_shared_v2u32(src + e * 8);
                     uint4 o;
                     o.x = ptx::e4m3x2_to_f16x2(static_cast<uint16_t>(v.x));
@@ -1354,7 +1362,7 @@ __global__ void __launch_bounds__(S2M_THREADS, MAXB2 <= 8 ? 2 : 1)
                     ptx::st_shared_v4(dst + e * 16, o);
                 }
                 ptx::fence_async_smem();
-                ptx::named_bar_sync(3, 64);  // every converter is done reading the raw slot
+                ptx::named_bar_sync(3, NCONV);  // every converter is done reading the raw slot
                 if (tb == 0) ptx::mbar_arrive(a_empty + 8 * s);
                 ptx::mbar_arrive(w_full + 8 * wb);
             }
