@@ -811,7 +811,7 @@ blr_status decode_launch(K kfn, dim3 grid, size_t smem, const P& prm, cudaStream
 // out[g][t][c] = sum_k A[g][t][k] B[g][k][c], B MN-major; split-K through `part` when planned.
 blr_status decode_mn(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int64_t a_gs, const void* B,
                      int64_t b_rs, int64_t b_gs, void* out, int out_bf16, int64_t o_rs, int64_t o_gs, int64_t n,
-                     int64_t K, int64_t N, int64_t groups, float* part) {
+                     int64_t K, int64_t N, int64_t groups, float* part, int pre = 0) {
     const MNPlan pl = mn_plan(K, N, groups);
     blr::DecodeMN d = {};
     d.A = A;
@@ -825,6 +825,7 @@ blr_status decode_mn(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, in
     d.K = static_cast<int>(K);
     d.N = static_cast<int>(N);
     d.k_chunk = pl.k_chunk;
+    d.pre = pre;
     if (pl.splits > 1) {  // fp32 partials [split][g][t][c], reduced below in a fixed order
         d.out = part;
         d.out_bf16 = 0;
@@ -855,7 +856,7 @@ blr_status decode_mn(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, in
     };
     cudaLaunchConfig_t cfg = {};
     const int64_t count = groups * n * N;
-    cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(cdiv(count, blr::DECODE_THREADS), 4 * 148)));
+    cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(cdiv(count, 8 * (blr::DECODE_THREADS / 32)), 8 * 148)));
     cfg.blockDim = dim3(blr::DECODE_THREADS);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -881,7 +882,7 @@ blr_status decode_mn(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, in
 blr_status decode_k(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int64_t a_gs, const void* B,
                     int64_t b_rs, int64_t b_gs, void* out, int out_bf16, int64_t o_rs, int64_t o_gs, int64_t n,
                     int64_t K, int64_t N, int64_t groups, int col_map, int64_t mon_b2, int64_t mon_r,
-                    int64_t o_cs = 1) {
+                    int64_t o_cs = 1, int pre = 0) {
     blr::DecodeK d = {};
     d.A = A;
     d.a_f32 = a_f32;
@@ -901,6 +902,7 @@ blr_status decode_k(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int
     d.mon_b2 = static_cast<int>(mon_b2);
     d.mon_r = static_cast<int>(mon_r);
     d.o_cs = o_cs;
+    d.pre = pre;
     // enough blocks for the SMs, >= 64 columns per block (the A stage is re-read per block)
     int64_t cpb = std::max<int64_t>(64, rup(cdiv(N * groups, DECODE_TARGET_BLOCKS), 8));
     cpb = std::min<int64_t>(cpb, rup(N, 8));
@@ -1019,7 +1021,7 @@ blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         float* part = zf + n_tok * r;
         s = decode_mn(st, X, 0, d_in, 0, V, r, 0, zf, 0, r, 0, n_tok, d_in, r, 1, part);
         if (s != BLR_OK) return s;
-        return decode_mn(st, zf, 1, r, 0, U, d_out, 0, Y, 1, d_out, 0, n_tok, r, d_out, 1, part);
+        return decode_mn(st, zf, 1, r, 0, U, d_out, 0, Y, 1, d_out, 0, n_tok, r, d_out, 1, part, /*pre=*/1);
     }
     if (fused_wanted(n_tok, r, r, d_in > d_out)) {  // one launch, Z on chip (blr_fused.cuh)
         blr::FParams p = {};
@@ -1098,7 +1100,7 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
                      r_blk * b2, b1, v_layout == BLR_MON_V_B2_FASTEST ? 1 : 2, b2, r_blk);
         if (s != BLR_OK) return s;
         return decode_k(st, zp, 1, K2, n_tok * K2, U, K2, qdim * K2, Y, 1, d_out, ytr ? 1 : qdim, n_tok, K2, qdim, b2,
-                        0, 1, 1, ytr ? b2 : 1);
+                        0, 1, 1, ytr ? b2 : 1, /*pre=*/1);
     }
     if (fused_wanted(n_tok, K2, r_blk, false)) {  // one launch, Z'_k on chip (blr_fused.cuh)
         blr::FParams p = {};
@@ -1288,7 +1290,8 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             }
             ++t_last_launches;
         }
-        return decode_mn(st, zp2, 1, r, n_tok * r, U, qdim, r * qdim, Y, 1, d_out, qdim, n_tok, r, qdim, b2, part);
+        return decode_mn(st, zp2, 1, r, n_tok * r, U, qdim, r * qdim, Y, 1, d_out, qdim, n_tok, r, qdim, b2, part,
+                         /*pre=*/1);
     }
     const int comp = comp_factor(r);
     void* zpp = workspace;  // Z'' [b2][n][r*comp] (split path: tile-blocked, then fp16 Z after it)

@@ -11,7 +11,8 @@
 //   decode_k_kernel  : out[g][t][c]   = sum_k A[g][t][k] * B[g][c][k]   (B "K-major": [N][K])
 //                      one warp per output column, lanes stride K with 16-B loads.
 //   decode_s2_kernel : BLAST S2, Z''[k][t][rho] = sum_l S[l,k,rho] Z[l][t][rho]  (fp32)
-//   decode_reduce    : out[g][t][c] = sum_z part[z][g][t][c], fp32 or RNE bf16, strided dest.
+//   decode_reduce    : out[g][t][c] = sum_z part[z][g][t][c] (warp-parallel over z, fixed order),
+//                      fp32 or RNE bf16, strided dest.
 #pragma once
 #include <cuda_bf16.h>
 #include <cstdint>
@@ -32,6 +33,8 @@ struct DecodeMN {
     int out_bf16;         // 1: RNE bf16 store (only when k_split == 1)
     long long o_rs, o_gs, o_zs;  // element strides of out: token rows, groups, K splits
     int n_tok, K, N, k_chunk;
+    int pre;  // 1 (not the first launch of a call): prefetch the block's weight slice into L2 before
+              // griddepcontrol.wait, so it streams while the previous stage runs
 };
 
 __device__ __forceinline__ float4 bf16x4_to_f32(uint2 w) {
@@ -48,8 +51,17 @@ __global__ void __launch_bounds__(DECODE_THREADS) decode_mn_kernel(const DecodeM
     const int kc = k1 - k0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c0 = blockIdx.x * DECODE_MN_COLS + lane * 8;
+    if (d.pre) {  // weights are never written by this library: stream the block's slice into L2 now
+        const int cb0 = blockIdx.x * DECODE_MN_COLS;
+        const int ncb = min(DECODE_MN_COLS, d.N - cb0);
+        const __nv_bfloat16* bp0 = d.B + static_cast<long long>(g) * d.b_gs + cb0;
+        for (int k = k0 + threadIdx.x; k < k1; k += DECODE_THREADS)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(bp0 + static_cast<long long>(k) * d.b_rs),
+                         "r"(static_cast<uint32_t>(ncb * 2)) : "memory");
+    }
     // stage A[g][t][k0:k1] as fp32, [k][t] so one k's NT values are contiguous (float4 reads)
     asm volatile("griddepcontrol.wait;" ::: "memory");  // A may be the previous kernel's output
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (after the wait: first-launch rule)
     for (int e = threadIdx.x; e < NT * kc; e += DECODE_THREADS) {
         const int t = e / kc, k = e - t * kc;
         float v = 0.f;
@@ -171,6 +183,7 @@ struct DecodeK {
     int col_map, mon_b2, mon_r;
     int cols_per_block;
     long long o_cs;  // col_map 0: elements between output columns (1; b2 for Monarch's transposed order)
+    int pre;         // 1: prefetch the block's weight rows into L2 before griddepcontrol.wait
 };
 
 template <int NT>
@@ -178,7 +191,15 @@ __global__ void __launch_bounds__(DECODE_THREADS) decode_k_kernel(const DecodeK 
     extern __shared__ float dsm[];  // A [NT][K] fp32
     const int g = blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (d.pre) {
+        const int cb = blockIdx.x * d.cols_per_block, ce = min(d.N, cb + d.cols_per_block);
+        for (int c = cb + threadIdx.x; c < ce; c += DECODE_THREADS)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(d.B + static_cast<long long>(g) * d.b_gs +
+                                                                               static_cast<long long>(c) * d.b_rs),
+                         "r"(static_cast<uint32_t>(d.K * 2)) : "memory");
+    }
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int e = threadIdx.x; e < NT * d.K; e += DECODE_THREADS) {
         const int t = e / d.K, k = e - t * d.K;
         float v = 0.f;
@@ -263,6 +284,7 @@ __global__ void __launch_bounds__(DECODE_THREADS)
     decode_s2_kernel(const float* __restrict__ Z, const __nv_bfloat16* __restrict__ S, float* __restrict__ Zpp,
                      int n_tok, int b1, int b2, int r) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const long long total = static_cast<long long>(b2) * n_tok * r;
     for (long long e = blockIdx.x * static_cast<long long>(DECODE_THREADS) + threadIdx.x; e < total;
          e += static_cast<long long>(gridDim.x) * DECODE_THREADS) {
@@ -278,23 +300,38 @@ __global__ void __launch_bounds__(DECODE_THREADS)
     }
 }
 
-// Split-K reduction: part is [splits][groups][n_tok][N] fp32; out[g*gs + t*rs + c].
+// Split-K reduction: part is [splits][groups][n_tok][N] fp32; out[g*gs + t*rs + c].  One warp
+// per 32 consecutive outputs with the splits spread over 4 lane groups... -> here: one warp per
+// 8 consecutive outputs; lane = (split residue s8 in 0..3, output j in 0..7): each lane sums the
+// splits z = s8, s8 + 4, ... of its output in ascending order, then the 4 partial sums are combined
+// by two fixed shuffle steps (a fixed tree: bitwise run-to-run deterministic).  A
+// thread-per-output loop over 40-50 splits was latency-bound (~10 us for 1488 outputs).
 __global__ void __launch_bounds__(DECODE_THREADS)
     decode_reduce(const float* __restrict__ part, int splits, int groups, int n_tok, int N, void* out, int out_bf16,
                   long long o_rs, long long o_gs) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const long long count = static_cast<long long>(groups) * n_tok * N;
-    for (long long e = blockIdx.x * static_cast<long long>(DECODE_THREADS) + threadIdx.x; e < count;
-         e += static_cast<long long>(gridDim.x) * DECODE_THREADS) {
+    const int lane = threadIdx.x & 31;
+    const int j = lane & 7, s4 = lane >> 3;
+    const long long warps = static_cast<long long>(gridDim.x) * (DECODE_THREADS / 32);
+    for (long long wb = (static_cast<long long>(blockIdx.x) * (DECODE_THREADS / 32) + (threadIdx.x >> 5)) * 8;
+         wb < count; wb += warps * 8) {
+        const long long e = wb + j;
         float s = 0.f;
-        for (int z = 0; z < splits; ++z) s += part[static_cast<long long>(z) * count + e];
-        const int c = static_cast<int>(e % N);
-        const long long gt = e / N;
-        const int t = static_cast<int>(gt % n_tok);
-        const int g = static_cast<int>(gt / n_tok);
-        const long long off = static_cast<long long>(g) * o_gs + static_cast<long long>(t) * o_rs + c;
-        if (out_bf16) static_cast<__nv_bfloat16*>(out)[off] = __float2bfloat16_rn(s);
-        else static_cast<float*>(out)[off] = s;
+        if (e < count)
+            for (int z = s4; z < splits; z += 4) s += __ldcg(part + static_cast<long long>(z) * count + e);
+        s += __shfl_down_sync(0xffffffffu, s, 16);  // (s4, s4 + 2)
+        s += __shfl_down_sync(0xffffffffu, s, 8);   // (0+2) + (1+3)
+        if (s4 == 0 && e < count) {
+            const int c = static_cast<int>(e % N);
+            const long long gt = e / N;
+            const int t = static_cast<int>(gt % n_tok);
+            const int g = static_cast<int>(gt / n_tok);
+            const long long off = static_cast<long long>(g) * o_gs + static_cast<long long>(t) * o_rs + c;
+            if (out_bf16) static_cast<__nv_bfloat16*>(out)[off] = __float2bfloat16_rn(s);
+            else static_cast<float*>(out)[off] = s;
+        }
     }
 }
 
