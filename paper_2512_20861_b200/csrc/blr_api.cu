@@ -14,6 +14,7 @@
 #include "../../include/blr.h"
 #include "blr_kernels.cuh"
 #include "blr_decode.cuh"
+#include "blr_decode_tc.cuh"
 #include "blr_fused.cuh"
 
 namespace {
@@ -741,11 +742,11 @@ bool encode_x_blocked(CUtensorMap* m, const void* X, int64_t n_tok, int64_t b1, 
 }
 
 // ------------------------------------------------------------------ decode (small n) path ----
-// Small n runs the weight-streaming CUDA-core kernels of blr_decode.cuh up to a
-// per-method token count where they measured faster than the tcgen05 path (scripts/decode_bench.py,
-// profiles/r01_decode.txt): LR n <= 4, BLAST n <= 2, Monarch never by default.  BLR_DECODE=1
-// forces the decode path for every n <= DECODE_MAX_TOKENS, BLR_DECODE=0 disables it (tests cover
-// both paths at every small n).
+// Small n runs the weight-streaming tensor-core decode stages of blr_decode_tc.cuh
+// up to a per-method token count where they measured faster than the tcgen05 prefill path
+// (scripts/decode_bench.py, profiles/r02_decode.txt): low rank n <= 16, Monarch and BLAST n <= 8.
+// BLR_DECODE=1 forces the decode path for every n <= DECODE_MAX_TOKENS, BLR_DECODE=0 disables it
+// (tests cover both paths at every small n).
 bool use_decode(int64_t n_tok, int64_t default_max) {
     if (n_tok > blr::DECODE_MAX_TOKENS) return false;
     const char* e = getenv("BLR_DECODE");
@@ -753,167 +754,255 @@ bool use_decode(int64_t n_tok, int64_t default_max) {
     if (e && e[0] == '1') return true;
     return n_tok <= default_max;
 }
-constexpr int64_t DECODE_TARGET_BLOCKS = 2 * 148;  // fixed (workspace sizes must not query the device)
-
-struct MNPlan {
-    int splits, k_chunk;
-};
-MNPlan mn_plan(int64_t K, int64_t N, int64_t groups) {
-    const int64_t blocks = cdiv(N, blr::DECODE_MN_COLS) * groups;
-    int64_t splits = std::max<int64_t>(1, std::min<int64_t>(cdiv(DECODE_TARGET_BLOCKS, blocks), cdiv(K, 64)));
-    const int64_t kc = rup(cdiv(K, splits), 8);
-    splits = cdiv(K, kc);
-    return {static_cast<int>(splits), static_cast<int>(kc)};
-}
-size_t mn_part_bytes(int64_t n_tok, int64_t K, int64_t N, int64_t groups) {
-    const MNPlan pl = mn_plan(K, N, groups);
-    return pl.splits > 1 ? static_cast<size_t>(pl.splits) * groups * n_tok * N * 4 : 0;
-}
-inline int decode_nt(int64_t n_tok) { return n_tok <= 4 ? 4 : n_tok <= 8 ? 8 : 16; }
-
-size_t lowrank_decode_ws(int64_t n, int64_t i, int64_t o, int64_t r) {
-    return static_cast<size_t>(n) * r * 4 + std::max(mn_part_bytes(n, i, r, 1), mn_part_bytes(n, r, o, 1));
-}
-size_t blast_decode_ws(int64_t n, int64_t i, int64_t o, int64_t b1, int64_t b2, int64_t r) {
-    return static_cast<size_t>(b1 + b2) * n * r * 4 +
-           std::max(mn_part_bytes(n, i / b1, r, b1), mn_part_bytes(n, r, o / b2, b2));
-}
+// decode-path workspace: fp32 intermediates only (K splits are reduced on chip)
+size_t lowrank_decode_ws(int64_t n, int64_t r) { return static_cast<size_t>(n) * r * 4; }
+size_t blast_decode_ws(int64_t n, int64_t b1, int64_t b2, int64_t r) { return static_cast<size_t>(b1 + b2) * n * r * 4; }
 size_t monarch_decode_ws(int64_t n, int64_t b1, int64_t b2, int64_t r_blk) {
     return static_cast<size_t>(b2) * n * b1 * r_blk * 4;
 }
 
-template <typename K, typename P>
-blr_status decode_launch(K kfn, dim3 grid, size_t smem, const P& prm, cudaStream_t st) {
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT) != cudaSuccess)
-        return BLR_ERR_CUDA;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(blr::DECODE_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
-    if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
-    if (cudaLaunchKernelEx(&cfg, kfn, prm) != cudaSuccess) return BLR_ERR_CUDA;
-    if (prof) {
-        if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
-        ++t_prof_n;
-    }
-    ++t_last_launches;
-    return BLR_OK;
+// ---- tensor-core decode stages (blr_decode_tc.cuh): planned and encoded before any launch ----
+struct DtcPrep {
+    blr::DecodeTC d;
+    CUtensorMap tm;
+    dim3 grid;
+    int cluster, epi, kmaj, w;
+    size_t smem;
+};
+
+// Time estimate (us) of one decode stage: `ctas` CTAs each streaming `bytes_cta` weight bytes
+// through a ring of `ring` bytes.  Measured (benchmarks/micro/dtc_stream.cu): HBM
+// ~6.2 TB/s (64-column strips of a row-major weight ~20% slower), and a TMA load takes ~2.5 us
+// under load, so one CTA streams at most ring / 2.5 us; waves beyond the first repeat that;
+// ~1 us for the in-cluster K reduction.
+double dtc_estimate(int64_t ctas, double bytes_cta, double ring, int w, bool kmaj, int64_t per_sm, bool split) {
+    const double eff = kmaj ? 0.9 : w == 64 ? 0.8 : w == 128 ? 0.95 : 1.0;
+    const double t_hbm = ctas * bytes_cta / (6.2e6 * eff);
+    const double t_cta = 2.0 + bytes_cta * 2.5 / ring;  // + start-up: A slice, first loads' latency
+    const int64_t waves = cdiv(ctas, 148 * per_sm);
+    return std::max(t_hbm, t_cta * waves) + (split ? 1.0 : 0.0);
 }
 
-// out[g][t][c] = sum_k A[g][t][k] B[g][k][c], B MN-major; split-K through `part` when planned.
-blr_status decode_mn(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int64_t a_gs, const void* B,
-                     int64_t b_rs, int64_t b_gs, void* out, int out_bf16, int64_t o_rs, int64_t o_gs, int64_t n,
-                     int64_t K, int64_t N, int64_t groups, float* part, int pre = 0) {
-    const MNPlan pl = mn_plan(K, N, groups);
-    blr::DecodeMN d = {};
+// smem per CTA for a tile; the ring gets whatever keeps `per_sm` CTAs resident (<= 12 stages)
+bool dtc_fit(int kc, int a_f32, int units, int epi, int w, int bk, int s_elems, int per_sm, int& stages, size_t& smem) {
+    const blr::dtc::Layout L0 = blr::dtc::layout(kc, a_f32, units, 0, epi, w, bk, s_elems);
+    const int64_t budget = (228 * 1024) / per_sm - 1024 - static_cast<int64_t>(L0.total);
+    stages = static_cast<int>(std::min<int64_t>(12, budget / (blr::DTC_STAGE + 16)));
+    stages = std::min(stages, std::max(2, units * ((kc + bk - 1) / bk)));  // no deeper than the CTA's data
+    if (epi == 1) stages = std::max(stages, (16 * w * 4 + blr::DTC_STAGE - 1) / blr::DTC_STAGE);  // tile fits the ring
+    if (stages < 2) return false;
+    smem = blr::dtc::layout(kc, a_f32, units, stages, epi, w, bk, s_elems).total;
+    return smem + 1024 <= static_cast<size_t>(228 * 1024) / per_sm;
+}
+
+// Choose the tile width W, the K split S (= cluster size) and the ring depth of an (N, K, G)
+// weight stream.  BLR_DTC_S / BLR_DTC_W force S / W (experiments).
+void dtc_plan(DtcPrep& P, int64_t K, int64_t N, int64_t G, int a_f32, int kmaj) {
+    const char* fs = getenv(P.d.pre ? "BLR_DTC_S1" : "BLR_DTC_S0");  // per launch of the call
+    const char* fw = getenv(P.d.pre ? "BLR_DTC_W1" : "BLR_DTC_W0");
+    if (!fs) fs = getenv("BLR_DTC_S");
+    if (!fw) fw = getenv("BLR_DTC_W");
+    const int force_s = fs ? atoi(fs) : 0, force_w = fw ? atoi(fw) : 0;
+    double best = 1e300;
+    P.cluster = 0;
+    for (int w : {64, 128, 256}) {
+        if (kmaj && w != 64) continue;
+        if (force_w && w != force_w) continue;
+        const int bk = blr::dtc_bk(kmaj != 0, w);
+        const int64_t nt = cdiv(N, w);
+        for (int S = 1; S <= blr::DTC_MAX_CLUSTER; ++S) {
+            const int64_t kc = rup(cdiv(K, S), bk);
+            if (kc > blr::DTC_MAX_KC || cdiv(K, kc) != S) continue;
+            if (force_s && S != force_s) continue;
+            const int epi = S > 1 ? 1 : 0;
+            for (int per_sm = 1; per_sm <= 3; ++per_sm) {
+                int stages;
+                size_t smem;
+                if (!dtc_fit(static_cast<int>(kc), a_f32, 1, epi, w, bk, 0, per_sm, stages, smem)) continue;
+                if (stages < 3 && per_sm > 1) continue;
+                const int64_t ctas = nt * G * S;
+                const double c = dtc_estimate(ctas, static_cast<double>(kc) * w * 2, static_cast<double>(stages) * blr::DTC_STAGE,
+                                              w, kmaj != 0, per_sm, S > 1) + 0.3 * smem / (228.0 * 1024);
+                if (c < best) {
+                    best = c;
+                    P.cluster = S;
+                    P.epi = epi;
+                    P.w = w;
+                    P.d.k_chunk = static_cast<int>(kc);
+                    P.d.stages = stages;
+                    P.smem = smem;
+                    P.grid = dim3(static_cast<unsigned>(S), static_cast<unsigned>(nt), static_cast<unsigned>(G));
+                }
+            }
+        }
+    }
+}
+
+// out[g][t][c] = sum_k A[g][t][k] B[g][k][c] (kmaj = 0, B [K][N]) or B[g][c][k] (kmaj = 1, B [N][K]).
+blr_status dtc_prepare(DtcPrep& P, const void* A, int a_f32, int64_t a_rs, int64_t a_gs, const void* B, int kmaj,
+                       int64_t b_rs, int64_t b_gs, void* out, int out_bf16, int64_t o_rs, int64_t o_gs, int64_t o_cs,
+                       int64_t n, int64_t K, int64_t N, int64_t G, int pre) {
+    P = DtcPrep();
+    blr::DecodeTC& d = P.d;
+    if (a_rs % 8 || a_gs % 8) return BLR_ERR_ALIGN;
     d.A = A;
     d.a_f32 = a_f32;
     d.a_rs = a_rs;
     d.a_gs = a_gs;
-    d.B = static_cast<const __nv_bfloat16*>(B);
-    d.b_rs = b_rs;
-    d.b_gs = b_gs;
     d.n_tok = static_cast<int>(n);
     d.K = static_cast<int>(K);
     d.N = static_cast<int>(N);
-    d.k_chunk = pl.k_chunk;
-    d.pre = pre;
-    if (pl.splits > 1) {  // fp32 partials [split][g][t][c], reduced below in a fixed order
-        d.out = part;
-        d.out_bf16 = 0;
-        d.o_rs = N;
-        d.o_gs = n * N;
-        d.o_zs = groups * n * N;
-    } else {
-        d.out = out;
-        d.out_bf16 = out_bf16;
-        d.o_rs = o_rs;
-        d.o_gs = o_gs;
-        d.o_zs = 0;
-    }
-    const int nt = decode_nt(n);
-    const size_t smem = static_cast<size_t>(nt) * std::max<int>(pl.k_chunk, 4 * blr::DECODE_MN_COLS) * 4;
-    const dim3 grid(static_cast<unsigned>(cdiv(N, blr::DECODE_MN_COLS)), static_cast<unsigned>(groups),
-                    static_cast<unsigned>(pl.splits));
-    blr_status s = nt == 4    ? decode_launch(blr::decode_mn_kernel<4>, grid, smem, d, st)
-                   : nt == 8 ? decode_launch(blr::decode_mn_kernel<8>, grid, smem, d, st)
-                             : decode_launch(blr::decode_mn_kernel<16>, grid, smem, d, st);
-    if (s != BLR_OK || pl.splits == 1) return s;
-    struct RedArgs {
-        const float* part;
-        int splits, groups, n_tok, N;
-        void* out;
-        int out_bf16;
-        long long o_rs, o_gs;
-    };
-    cudaLaunchConfig_t cfg = {};
-    const int64_t count = groups * n * N;
-    cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(cdiv(count, 8 * (blr::DECODE_THREADS / 32)), 8 * 148)));
-    cfg.blockDim = dim3(blr::DECODE_THREADS);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
-    if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
-    if (cudaLaunchKernelEx(&cfg, blr::decode_reduce, static_cast<const float*>(part), pl.splits,
-                           static_cast<int>(groups), static_cast<int>(n), static_cast<int>(N), out, out_bf16,
-                           static_cast<long long>(o_rs), static_cast<long long>(o_gs)) != cudaSuccess)
-        return BLR_ERR_CUDA;
-    if (prof) {
-        if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
-        ++t_prof_n;
-    }
-    ++t_last_launches;
-    return BLR_OK;
-}
-
-// out[g][t][c] = sum_k A[g][t][k] B[g][c][k], B K-major (one warp per output column).
-blr_status decode_k(cudaStream_t st, const void* A, int a_f32, int64_t a_rs, int64_t a_gs, const void* B,
-                    int64_t b_rs, int64_t b_gs, void* out, int out_bf16, int64_t o_rs, int64_t o_gs, int64_t n,
-                    int64_t K, int64_t N, int64_t groups, int col_map, int64_t mon_b2, int64_t mon_r,
-                    int64_t o_cs = 1, int pre = 0) {
-    blr::DecodeK d = {};
-    d.A = A;
-    d.a_f32 = a_f32;
-    d.a_rs = a_rs;
-    d.a_gs = a_gs;
-    d.B = static_cast<const __nv_bfloat16*>(B);
-    d.b_rs = b_rs;
-    d.b_gs = b_gs;
+    d.n_units = 1;
     d.out = out;
     d.out_bf16 = out_bf16;
     d.o_rs = o_rs;
     d.o_gs = o_gs;
-    d.n_tok = static_cast<int>(n);
-    d.K = static_cast<int>(K);
-    d.N = static_cast<int>(N);
-    d.col_map = col_map;
-    d.mon_b2 = static_cast<int>(mon_b2);
-    d.mon_r = static_cast<int>(mon_r);
     d.o_cs = o_cs;
     d.pre = pre;
-    // enough blocks for the SMs, >= 64 columns per block (the A stage is re-read per block)
-    int64_t cpb = std::max<int64_t>(64, rup(cdiv(N * groups, DECODE_TARGET_BLOCKS), 8));
-    cpb = std::min<int64_t>(cpb, rup(N, 8));
-    d.cols_per_block = static_cast<int>(cpb);
-    const int nt = decode_nt(n);
-    const size_t smem = static_cast<size_t>(nt) * K * 4;
-    if (smem + 1024 > static_cast<size_t>(SMEM_LIMIT)) return BLR_ERR_UNSUPPORTED;
-    const dim3 grid(static_cast<unsigned>(cdiv(N, cpb)), static_cast<unsigned>(groups));
-    return nt == 4   ? decode_launch(blr::decode_k_kernel<4>, grid, smem, d, st)
-           : nt == 8 ? decode_launch(blr::decode_k_kernel<8>, grid, smem, d, st)
-                     : decode_launch(blr::decode_k_kernel<16>, grid, smem, d, st);
+    P.kmaj = kmaj;
+    dtc_plan(P, K, N, G, a_f32, kmaj);
+    if (P.cluster == 0) return BLR_ERR_UNSUPPORTED;
+    if (getenv("BLR_DTC_VERBOSE"))
+        fprintf(stderr, "dtc K=%lld N=%lld G=%lld kmaj=%d a_f32=%d: W=%d S=%d kc=%d stages=%d smem=%zu grid=%u\n",
+                (long long)K, (long long)N, (long long)G, kmaj, a_f32, P.w, P.cluster, P.d.k_chunk, P.d.stages, P.smem,
+                P.grid.x * P.grid.y * P.grid.z);
+    const int bk = blr::dtc_bk(kmaj != 0, P.w);
+    const uint64_t gs = static_cast<uint64_t>(b_gs > 0 ? b_gs : b_rs * (kmaj ? N : K)) * 2;
+    if (kmaj) {  // B [N][K] per group: map (K, N, G), box 64 k x 64 columns
+        const uint64_t dims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(G)};
+        const uint64_t str[2] = {static_cast<uint64_t>(b_rs) * 2, gs};
+        const uint32_t box[3] = {64, 64, 1};
+        if (!encode(&P.tm, B, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+    } else {  // B [K][N] per group: map (N, K, G), box 64 columns x bk k
+        const uint64_t dims[3] = {static_cast<uint64_t>(N), static_cast<uint64_t>(K), static_cast<uint64_t>(G)};
+        const uint64_t str[2] = {static_cast<uint64_t>(b_rs) * 2, gs};
+        const uint32_t box[3] = {64, static_cast<uint32_t>(bk), 1};
+        if (!encode(&P.tm, B, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+    }
+    return BLR_OK;
+}
+
+template <bool KMAJ, int EPI, int W>
+blr_status dtc_launch_t(const DtcPrep& P, cudaStream_t st) {
+    auto kfn = blr::decode_tc_kernel<KMAJ, EPI, W>;
+    static bool attr_set[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return BLR_ERR_CUDA;
+    if (!attr_set[dev & 63]) {
+        if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT) != cudaSuccess)
+            return BLR_ERR_CUDA;
+        attr_set[dev & 63] = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = P.grid;
+    cfg.blockDim = dim3(blr::DTC_THREADS);
+    cfg.dynamicSmemBytes = P.smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = static_cast<unsigned>(P.cluster);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+    if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+    blr::DecodeTC dd = P.d;
+    dd.trace = t_trace;
+    if (t_trace) t_trace += 128 * 256;  // next launch traces into the next slot
+    if (cudaLaunchKernelEx(&cfg, kfn, P.tm, dd) != cudaSuccess) return BLR_ERR_CUDA;
+    if (prof) {
+        if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+        ++t_prof_n;
+    }
+    ++t_last_launches;
+    return BLR_OK;
+}
+
+template <int EPI>
+blr_status dtc_launch_w(const DtcPrep& P, cudaStream_t st) {
+    if (P.w == 64) return dtc_launch_t<false, EPI, 64>(P, st);
+    return P.w == 128 ? dtc_launch_t<false, EPI, 128>(P, st) : dtc_launch_t<false, EPI, 256>(P, st);
+}
+
+blr_status dtc_launch(const DtcPrep& P, cudaStream_t st) {
+    if (P.kmaj) return P.epi == 0 ? dtc_launch_t<true, 0, 64>(P, st) : dtc_launch_t<true, 1, 64>(P, st);
+    return P.epi == 0 ? dtc_launch_w<0>(P, st) : P.epi == 1 ? dtc_launch_w<1>(P, st) : dtc_launch_w<2>(P, st);
+}
+
+bool dtc_blast_mix_ok(int64_t b1, int64_t pdim, int& cs, int& units) {
+    if (pdim > blr::DTC_MAX_KC) return false;
+    for (int u = 1; u <= blr::DTC_MAX_UNITS; ++u)
+        if (b1 % u == 0 && b1 / u <= blr::DTC_MAX_CLUSTER) {
+            units = u;
+            cs = static_cast<int>(b1 / u);
+            return true;
+        }
+    return false;
+}
+blr_status dtc_prepare_blast_mix(DtcPrep& P, const void* X, int64_t d_in, int64_t pdim, const void* V, const void* S,
+                                 float* zpp, int64_t n, int64_t b1, int64_t b2, int64_t r, int cs, int units) {
+    P = DtcPrep();
+    blr::DecodeTC& d = P.d;
+    d.A = X;
+    d.a_f32 = 0;
+    d.a_rs = d_in;
+    d.a_gs = pdim;
+    d.n_tok = static_cast<int>(n);
+    d.K = static_cast<int>(pdim);
+    d.N = static_cast<int>(r);
+    d.n_units = units;
+    d.out = zpp;
+    d.out_bf16 = 0;
+    d.o_rs = r;
+    d.o_gs = n * r;
+    d.o_cs = 1;
+    d.s2 = static_cast<const __nv_bfloat16*>(S);
+    d.b1 = static_cast<int>(b1);
+    d.b2 = static_cast<int>(b2);
+    d.pre = 0;
+    P.cluster = cs;
+    P.epi = 2;
+    P.kmaj = 0;
+    const char* fw = getenv("BLR_DTC_W0");
+    if (!fw) fw = getenv("BLR_DTC_W");
+    const int force_w = fw ? atoi(fw) : 0;
+    double best = 1e300;
+    const int64_t nk = cdiv(b2, cs);
+    for (int w : {64, 128, 256}) {
+        if (force_w && w != force_w) continue;
+        const int bk = blr::dtc_bk(false, w);
+        const int kc = static_cast<int>(rup(pdim, bk));
+        for (int per_sm = 1; per_sm <= 3; ++per_sm) {
+            int stages;
+            size_t smem;
+            if (!dtc_fit(kc, 0, units, 2, w, bk, static_cast<int>(nk * b1 * w), per_sm, stages, smem)) continue;
+            if (stages < 3 && per_sm > 1) continue;
+            const int64_t ctas = cs * cdiv(r, w);
+            const double c = dtc_estimate(ctas, static_cast<double>(units) * kc * w * 2,
+                                          static_cast<double>(stages) * blr::DTC_STAGE, w, false, per_sm, true) +
+                             0.3 * smem / (228.0 * 1024);
+            if (c < best) {
+                best = c;
+                P.w = w;
+                d.k_chunk = kc;
+                d.stages = stages;
+                P.smem = smem;
+                P.grid = dim3(static_cast<unsigned>(cs), static_cast<unsigned>(cdiv(r, w)), 1);
+            }
+        }
+    }
+    if (best >= 1e300) return BLR_ERR_UNSUPPORTED;
+    if (getenv("BLR_DTC_VERBOSE"))
+        fprintf(stderr, "dtc blast-mix p=%lld r=%lld b1=%lld: cs=%d units=%d W=%d stages=%d smem=%zu grid=%u\n",
+                (long long)pdim, (long long)r, (long long)b1, cs, units, P.w, d.stages, P.smem, P.grid.x * P.grid.y);
+    const uint64_t dims[3] = {static_cast<uint64_t>(r), static_cast<uint64_t>(pdim), static_cast<uint64_t>(b1)};
+    const uint64_t str[2] = {static_cast<uint64_t>(r) * 2, static_cast<uint64_t>(pdim * r) * 2};
+    const uint32_t box[3] = {64, static_cast<uint32_t>(blr::dtc_bk(false, P.w)), 1};
+    if (!encode(&P.tm, V, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+    return BLR_OK;
 }
 
 size_t blast_ws_bytes(int64_t n_tok, int64_t b1, int64_t b2, int64_t r) {
@@ -983,7 +1072,7 @@ size_t blr_lowrank_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, in
     if (n_tok <= 0 || r <= 0) return 0;
     size_t b = static_cast<size_t>(n_tok) * r * 2 * comp_factor(r);
     if (n_tok <= blr::DECODE_MAX_TOKENS && d_in > 0 && d_out > 0)
-        b = std::max(b, lowrank_decode_ws(n_tok, d_in, d_out, r));
+        b = std::max(b, lowrank_decode_ws(n_tok, r));
     return b;
 }
 size_t blr_monarch_workspace_size(int64_t n_tok, int64_t, int64_t, int64_t b1, int64_t b2, int64_t r_blk) {
@@ -996,7 +1085,7 @@ size_t blr_blast_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, int6
     if (n_tok <= 0 || b1 <= 0 || b2 <= 0 || r <= 0) return 0;
     size_t b = blast_ws_bytes(n_tok, b1, b2, r);
     if (n_tok <= blr::DECODE_MAX_TOKENS && d_in > 0 && d_out > 0 && d_in % b1 == 0 && d_out % b2 == 0)
-        b = std::max(b, blast_decode_ws(n_tok, d_in, d_out, b1, b2, r));
+        b = std::max(b, blast_decode_ws(n_tok, b1, b2, r));
     return b;
 }
 
@@ -1016,12 +1105,15 @@ blr_status blr_lowrank_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     blr_status s = device_info(d, dev);
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (use_decode(n_tok, 4)) {  // weight-streaming small-n path, fp32 Z [n][r]
+    if (use_decode(n_tok, 16)) {  // weight-streaming small-n path: two tensor-core stages, fp32 Z [n][r]
         float* zf = static_cast<float*>(workspace);
-        float* part = zf + n_tok * r;
-        s = decode_mn(st, X, 0, d_in, 0, V, r, 0, zf, 0, r, 0, n_tok, d_in, r, 1, part);
+        DtcPrep p1, p2;
+        s = dtc_prepare(p1, X, 0, d_in, 0, V, 0, r, 0, zf, 0, r, 0, 1, n_tok, d_in, r, 1, 0);
         if (s != BLR_OK) return s;
-        return decode_mn(st, zf, 1, r, 0, U, d_out, 0, Y, 1, d_out, 0, n_tok, r, d_out, 1, part, /*pre=*/1);
+        s = dtc_prepare(p2, zf, 1, r, 0, U, 0, d_out, 0, Y, 1, d_out, 0, 1, n_tok, r, d_out, 1, 1);
+        if (s != BLR_OK) return s;
+        s = dtc_launch(p1, st);
+        return s != BLR_OK ? s : dtc_launch(p2, st);
     }
     if (fused_wanted(n_tok, r, r, d_in > d_out)) {  // one launch, Z on chip (blr_fused.cuh)
         blr::FParams p = {};
@@ -1094,13 +1186,20 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     blr_status s = device_info(d, dev);
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (use_decode(n_tok, 0)) {  // small-n path: fp32 Z' [b2][n][b1 r'], permutations in the index maps
+    if (use_decode(n_tok, 8)) {  // small-n path: fp32 Z' [b2][n][b1 r'], permutations in the index maps
         float* zp = static_cast<float*>(workspace);
-        s = decode_k(st, X, 0, d_in, pdim, V, pdim, r_blk * b2 * pdim, zp, 0, K2, n_tok * K2, n_tok, pdim,
-                     r_blk * b2, b1, v_layout == BLR_MON_V_B2_FASTEST ? 1 : 2, b2, r_blk);
+        DtcPrep p1, p2;
+        s = dtc_prepare(p1, X, 0, d_in, pdim, V, 1, pdim, r_blk * b2 * pdim, zp, 0, K2, n_tok * K2, 1, n_tok, pdim,
+                        r_blk * b2, b1, 0);
         if (s != BLR_OK) return s;
-        return decode_k(st, zp, 1, K2, n_tok * K2, U, K2, qdim * K2, Y, 1, d_out, ytr ? 1 : qdim, n_tok, K2, qdim, b2,
-                        0, 1, 1, ytr ? b2 : 1, /*pre=*/1);
+        p1.d.col_map = v_layout == BLR_MON_V_B2_FASTEST ? 1 : 2;  // column c of block l -> (k, rho)
+        p1.d.mon_b2 = static_cast<int>(b2);
+        p1.d.mon_r = static_cast<int>(r_blk);
+        s = dtc_prepare(p2, zp, 1, K2, n_tok * K2, U, 1, K2, qdim * K2, Y, 1, d_out, ytr ? 1 : qdim, ytr ? b2 : 1,
+                        n_tok, K2, qdim, b2, 1);
+        if (s != BLR_OK) return s;
+        s = dtc_launch(p1, st);
+        return s != BLR_OK ? s : dtc_launch(p2, st);
     }
     if (fused_wanted(n_tok, K2, r_blk, false)) {  // one launch, Z'_k on chip (blr_fused.cuh)
         blr::FParams p = {};
@@ -1261,13 +1360,22 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
     blr_status s = device_info(d, dev);
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (use_decode(n_tok, 2)) {  // small-n path: fp32 Z [b1][n][r] and Z'' [b2][n][r]
+    if (use_decode(n_tok, 8)) {  // small-n path: fp32 Z [b1][n][r] (unless fused away) and Z'' [b2][n][r]
         float* z = static_cast<float*>(workspace);
         float* zp2 = z + b1 * n_tok * r;
-        float* part = zp2 + b2 * n_tok * r;
-        s = decode_mn(st, X, 0, d_in, pdim, V, r, pdim * r, z, 0, r, n_tok * r, n_tok, pdim, r, b1, part);
+        int cs = 0, units = 0;
+        DtcPrep p1, p3;
+        const bool mix = dtc_blast_mix_ok(b1, pdim, cs, units);
+        if (mix)  // S1 + S2 in one launch: Z stays in the cluster's shared memory
+            s = dtc_prepare_blast_mix(p1, X, d_in, pdim, V, S, zp2, n_tok, b1, b2, r, cs, units);
+        else
+            s = dtc_prepare(p1, X, 0, d_in, pdim, V, 0, r, pdim * r, z, 0, r, n_tok * r, 1, n_tok, pdim, r, b1, 0);
         if (s != BLR_OK) return s;
-        {
+        s = dtc_prepare(p3, zp2, 1, r, n_tok * r, U, 0, qdim, r * qdim, Y, 1, d_out, qdim, 1, n_tok, r, qdim, b2, 1);
+        if (s != BLR_OK) return s;
+        s = dtc_launch(p1, st);
+        if (s != BLR_OK) return s;
+        if (!mix) {  // S2 on its own: Z'' = sum_l S_l,k * Z_l (fp32)
             cudaLaunchConfig_t cfg = {};
             const int64_t count = b2 * n_tok * r;
             cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(cdiv(count, blr::DECODE_THREADS), 4 * 148)));
@@ -1290,8 +1398,7 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             }
             ++t_last_launches;
         }
-        return decode_mn(st, zp2, 1, r, n_tok * r, U, qdim, r * qdim, Y, 1, d_out, qdim, n_tok, r, qdim, b2, part,
-                         /*pre=*/1);
+        return dtc_launch(p3, st);
     }
     const int comp = comp_factor(r);
     void* zpp = workspace;  // Z'' [b2][n][r*comp] (split path: tile-blocked, then fp16 Z after it)
