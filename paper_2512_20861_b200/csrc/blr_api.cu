@@ -803,8 +803,12 @@ void dtc_plan(DtcPrep& P, int64_t K, int64_t N, int64_t G, int a_f32, int kmaj) 
     if (!fs) fs = getenv("BLR_DTC_S");
     if (!fw) fw = getenv("BLR_DTC_W");
     const int force_s = fs ? atoi(fs) : 0, force_w = fw ? atoi(fw) : 0;
+    const char* fm = getenv("BLR_DTC_MINPERSM");
+    int min_per_sm = fm ? atoi(fm) : 2;  // prefer two resident CTAs per SM: the next launch's CTAs
+                                         // can then start streaming their weights during this one
     double best = 1e300;
     P.cluster = 0;
+  retry:
     for (int w : {64, 128, 256}) {
         if (kmaj && w != 64) continue;
         if (force_w && w != force_w) continue;
@@ -815,14 +819,15 @@ void dtc_plan(DtcPrep& P, int64_t K, int64_t N, int64_t G, int a_f32, int kmaj) 
             if (kc > blr::DTC_MAX_KC || cdiv(K, kc) != S) continue;
             if (force_s && S != force_s) continue;
             const int epi = S > 1 ? 1 : 0;
-            for (int per_sm = 1; per_sm <= 3; ++per_sm) {
+            for (int per_sm = min_per_sm; per_sm <= 3; ++per_sm) {
                 int stages;
                 size_t smem;
                 if (!dtc_fit(static_cast<int>(kc), a_f32, 1, epi, w, bk, 0, per_sm, stages, smem)) continue;
-                if (stages < 3 && per_sm > 1) continue;
+                if (stages < std::min<int64_t>(3, cdiv(kc, bk)) && per_sm > 1) continue;
                 const int64_t ctas = nt * G * S;
+                const int64_t resident = std::min<int64_t>(8, (228 * 1024) / (smem + 1024));
                 const double c = dtc_estimate(ctas, static_cast<double>(kc) * w * 2, static_cast<double>(stages) * blr::DTC_STAGE,
-                                              w, kmaj != 0, per_sm, S > 1) + 0.3 * smem / (228.0 * 1024);
+                                              w, kmaj != 0, resident, S > 1) + 0.3 * smem / (228.0 * 1024);
                 if (c < best) {
                     best = c;
                     P.cluster = S;
@@ -835,6 +840,10 @@ void dtc_plan(DtcPrep& P, int64_t K, int64_t N, int64_t G, int a_f32, int kmaj) 
                 }
             }
         }
+    }
+    if (P.cluster == 0 && min_per_sm > 1) {  // a preference, not a requirement
+        min_per_sm = 1;
+        goto retry;
     }
 }
 
@@ -971,26 +980,30 @@ blr_status dtc_prepare_blast_mix(DtcPrep& P, const void* X, int64_t d_in, int64_
     const int force_w = fw ? atoi(fw) : 0;
     double best = 1e300;
     const int64_t nk = cdiv(b2, cs);
-    for (int w : {64, 128, 256}) {
-        if (force_w && w != force_w) continue;
-        const int bk = blr::dtc_bk(false, w);
-        const int kc = static_cast<int>(rup(pdim, bk));
-        for (int per_sm = 1; per_sm <= 3; ++per_sm) {
-            int stages;
-            size_t smem;
-            if (!dtc_fit(kc, 0, units, 2, w, bk, static_cast<int>(nk * b1 * w), per_sm, stages, smem)) continue;
-            if (stages < 3 && per_sm > 1) continue;
-            const int64_t ctas = cs * cdiv(r, w);
-            const double c = dtc_estimate(ctas, static_cast<double>(units) * kc * w * 2,
-                                          static_cast<double>(stages) * blr::DTC_STAGE, w, false, per_sm, true) +
-                             0.3 * smem / (228.0 * 1024);
-            if (c < best) {
-                best = c;
-                P.w = w;
-                d.k_chunk = kc;
-                d.stages = stages;
-                P.smem = smem;
-                P.grid = dim3(static_cast<unsigned>(cs), static_cast<unsigned>(cdiv(r, w)), 1);
+    const char* fm = getenv("BLR_DTC_MINPERSM");
+    for (int min_per_sm = fm ? std::min(2, atoi(fm)) : 2; min_per_sm >= 1 && best >= 1e300; --min_per_sm) {
+        for (int w : {64, 128, 256}) {
+            if (force_w && w != force_w) continue;
+            const int bk = blr::dtc_bk(false, w);
+            const int kc = static_cast<int>(rup(pdim, bk));
+            for (int per_sm = min_per_sm; per_sm <= 3; ++per_sm) {
+                int stages;
+                size_t smem;
+                if (!dtc_fit(kc, 0, units, 2, w, bk, static_cast<int>(nk * b1 * w), per_sm, stages, smem)) continue;
+                if (stages < std::min(3, units * kc / bk) && per_sm > 1) continue;
+                const int64_t ctas = cs * cdiv(r, w);
+                const int64_t resident = std::min<int64_t>(8, (228 * 1024) / (smem + 1024));
+                const double c = dtc_estimate(ctas, static_cast<double>(units) * kc * w * 2,
+                                              static_cast<double>(stages) * blr::DTC_STAGE, w, false, resident, true) +
+                                 0.3 * smem / (228.0 * 1024);
+                if (c < best) {
+                    best = c;
+                    P.w = w;
+                    d.k_chunk = kc;
+                    d.stages = stages;
+                    P.smem = smem;
+                    P.grid = dim3(static_cast<unsigned>(cs), static_cast<unsigned>(cdiv(r, w)), 1);
+                }
             }
         }
     }
@@ -1365,12 +1378,16 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
         float* zp2 = z + b1 * n_tok * r;
         int cs = 0, units = 0;
         DtcPrep p1, p3;
-        const bool mix = dtc_blast_mix_ok(b1, pdim, cs, units);
-        if (mix)  // S1 + S2 in one launch: Z stays in the cluster's shared memory
+        bool mix = dtc_blast_mix_ok(b1, pdim, cs, units);
+        if (mix) {  // S1 + S2 in one launch: Z stays in the cluster's shared memory
             s = dtc_prepare_blast_mix(p1, X, d_in, pdim, V, S, zp2, n_tok, b1, b2, r, cs, units);
-        else
+            if (s == BLR_ERR_UNSUPPORTED) mix = false;
+            else if (s != BLR_OK) return s;
+        }
+        if (!mix) {
             s = dtc_prepare(p1, X, 0, d_in, pdim, V, 0, r, pdim * r, z, 0, r, n_tok * r, 1, n_tok, pdim, r, b1, 0);
-        if (s != BLR_OK) return s;
+            if (s != BLR_OK) return s;
+        }
         s = dtc_prepare(p3, zp2, 1, r, n_tok * r, U, 0, qdim, r * qdim, Y, 1, d_out, qdim, 1, n_tok, r, qdim, b2, 1);
         if (s != BLR_OK) return s;
         s = dtc_launch(p1, st);

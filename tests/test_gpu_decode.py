@@ -1,7 +1,8 @@
 """GPU parity of the small-token (decode) path: n_tok <= 16 runs the
-weight-streaming CUDA-core kernels (csrc/blr_decode.cuh) with fp32 intermediates.  Same
-tolerance as the prefill path (north_star); the tcgen05 path is also forced at these sizes
-(BLR_DECODE=0) so both stay covered."""
+weight-streaming tensor-core decode stages (csrc/blr_decode_tc.cuh: TMA weight ring, mma.sync,
+K splits reduced in-cluster, BLAST S2 in S1's cluster epilogue) with fp32 intermediates staged as
+bf16 hi + lo pairs.  Same tolerance as the prefill path (north_star); the tcgen05 path is also
+forced at these sizes (BLR_DECODE=0) so both stay covered."""
 import numpy as np
 import pytest
 import torch
@@ -65,10 +66,26 @@ def test_decode_monarch(cuda_lib, n, b1, b2, rp, p, q, layout):
 
 @pytest.mark.parametrize("n", NS)
 @pytest.mark.parametrize("b1,b2,r,p,q", [(1, 1, 16, 8, 8), (3, 2, 24, 40, 56), (6, 6, 192, 128, 512),
-                                         (16, 16, 1488, 256, 688), (16, 16, 1488, 688, 256)])
+                                         (16, 16, 1488, 256, 688), (16, 16, 1488, 688, 256),
+                                         (11, 3, 40, 16, 24),      # b1 = 11: no cluster split -> S1, S2, S3
+                                         (2, 2, 64, 1040, 64),     # p > 1024: S1 with a K split, then S2
+                                         (12, 5, 72, 64, 40)])     # 6-CTA cluster x 2 blocks, b2 % 6 != 0
 def test_decode_blast(cuda_lib, n, b1, b2, r, p, q):
     Y, ref = _blast(cuda_lib, n, b1, b2, r, p, q)
     assert_parity(Y, ref, f"BLAST decode {n,b1,b2,r,p,q}")
+
+
+@pytest.mark.parametrize("w,s", [(64, 1), (64, 3), (64, 8), (128, 2), (128, 6), (256, 4), (256, 7)])
+def test_decode_forced_plans(cuda_lib, monkeypatch, w, s):
+    """Every tile width W and cluster (K split) size S of the decode kernel against the oracle: the
+    planner's choice is forced for both launches of a low-rank layer with K = 1000 (every S listed
+    is a valid split of 1000 rows into W's row granularity, the last split ragged) and N = 1000 /
+    1040 (ragged last tile)."""
+    monkeypatch.setenv("BLR_DTC_W", str(w))
+    monkeypatch.setenv("BLR_DTC_S", str(s))
+    for n in (1, 13):
+        Y, ref = _lr(cuda_lib, n, 1000, 1040, 1000)
+        assert_parity(Y, ref, f"LR decode W={w} S={s} n={n}")
 
 
 @pytest.mark.parametrize("n", [1, 16])
