@@ -17,7 +17,7 @@
 //    as the M dimension (ldmatrix from the A slice staged once in shared memory; .trans for
 //    MN-major weights).  An fp32 A (a previous stage's intermediate) is staged as a bf16 pair
 //    hi + lo with hi = bf16(a), lo = bf16(a - hi), both multiplied against the same weight
-//    fragments: the intermediate keeps ~16 significant bits (R15) at no HBM cost;
+//    fragments: the intermediate keeps ~16 significant bits at no HBM cost;
 //  * a K split (EPI 1) is reduced on chip: the S split CTAs of one output tile form a thread-block
 //    cluster, park their fp32 partial tiles in shared memory and each sums a 1/S share of the tile
 //    over the S peers through DSMEM in ascending split order (fixed order: bitwise deterministic,
