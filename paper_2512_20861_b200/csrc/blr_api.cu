@@ -744,14 +744,17 @@ bool encode_x_blocked(CUtensorMap* m, const void* X, int64_t n_tok, int64_t b1, 
 // ------------------------------------------------------------------ decode (small n) path ----
 // Small n runs the weight-streaming tensor-core decode stages of blr_decode_tc.cuh
 // up to a per-method token count where they measured faster than the tcgen05 prefill path
-// (scripts/decode_bench.py, profiles/r02_decode.txt): low rank n <= 16, Monarch and BLAST n <= 8.
-// BLR_DECODE=1 forces the decode path for every n <= DECODE_MAX_TOKENS, BLR_DECODE=0 disables it
-// (tests cover both paths at every small n).
+// (scripts/decode_bench.py, profiles/r02_decode.txt, profiles/r02_small_n.txt): low rank n <= 16,
+// Monarch n <= 256, BLAST n <= 8 (n <= 2048 when the tcgen05 path would be the S1+S2-fused
+// projection); n > 16 runs as independent 16-token chunks.  BLR_DECODE=1 forces the path for
+// every n <= DECODE_MAX_TOKENS, BLR_DECODE_MAXN=m for n <= m, BLR_DECODE=0 disables it.
 bool use_decode(int64_t n_tok, int64_t default_max) {
-    if (n_tok > blr::DECODE_MAX_TOKENS) return false;
+    if (n_tok > blr::DTC_MAX_N) return false;
     const char* e = getenv("BLR_DECODE");
     if (e && e[0] == '0') return false;
-    if (e && e[0] == '1') return true;
+    if (e && e[0] == '1') return n_tok <= blr::DECODE_MAX_TOKENS;
+    const char* m = getenv("BLR_DECODE_MAXN");  // force the weight-streaming path up to this n
+    if (m) return n_tok <= atoll(m);
     return n_tok <= default_max;
 }
 // decode-path workspace: fp32 intermediates only (K splits are reduced on chip)
@@ -775,11 +778,12 @@ struct DtcPrep {
 // ~6.2 TB/s (64-column strips of a row-major weight ~20% slower), and a TMA load takes ~2.5 us
 // under load, so one CTA streams at most ring / 2.5 us; waves beyond the first repeat that;
 // ~1 us for the in-cluster K reduction.
-double dtc_estimate(int64_t ctas, double bytes_cta, double ring, int w, bool kmaj, int64_t per_sm, bool split) {
+double dtc_estimate(int64_t ctas, double bytes_cta, double ring, int w, bool kmaj, int64_t per_sm, bool split,
+                    int64_t chunks = 1) {
     const double eff = kmaj ? 0.9 : w == 64 ? 0.8 : w == 128 ? 0.95 : 1.0;
-    const double t_hbm = ctas * bytes_cta / (6.2e6 * eff);
+    const double t_hbm = ctas * bytes_cta / (6.2e6 * eff);  // each token chunk re-reads the weights from L2
     const double t_cta = 2.0 + bytes_cta * 2.5 / ring;  // + start-up: A slice, first loads' latency
-    const int64_t waves = cdiv(ctas, 148 * per_sm);
+    const int64_t waves = cdiv(ctas * chunks, 148 * per_sm);
     return std::max(t_hbm, t_cta * waves) + (split ? 1.0 : 0.0);
 }
 
@@ -797,7 +801,7 @@ bool dtc_fit(int kc, int a_f32, int units, int epi, int w, int bk, int s_elems, 
 
 // Choose the tile width W, the K split S (= cluster size) and the ring depth of an (N, K, G)
 // weight stream.  BLR_DTC_S / BLR_DTC_W force S / W (experiments).
-void dtc_plan(DtcPrep& P, int64_t K, int64_t N, int64_t G, int a_f32, int kmaj) {
+void dtc_plan(DtcPrep& P, int64_t K, int64_t N, int64_t G, int a_f32, int kmaj, int64_t chunks) {
     const char* fs = getenv(P.d.pre ? "BLR_DTC_S1" : "BLR_DTC_S0");  // per launch of the call
     const char* fw = getenv(P.d.pre ? "BLR_DTC_W1" : "BLR_DTC_W0");
     if (!fs) fs = getenv("BLR_DTC_S");
@@ -827,7 +831,7 @@ void dtc_plan(DtcPrep& P, int64_t K, int64_t N, int64_t G, int a_f32, int kmaj) 
                 const int64_t ctas = nt * G * S;
                 const int64_t resident = std::min<int64_t>(8, (228 * 1024) / (smem + 1024));
                 const double c = dtc_estimate(ctas, static_cast<double>(kc) * w * 2, static_cast<double>(stages) * blr::DTC_STAGE,
-                                              w, kmaj != 0, resident, S > 1) + 0.3 * smem / (228.0 * 1024);
+                                              w, kmaj != 0, resident, S > 1, chunks) + 0.3 * smem / (228.0 * 1024);
                 if (c < best) {
                     best = c;
                     P.cluster = S;
@@ -836,7 +840,7 @@ void dtc_plan(DtcPrep& P, int64_t K, int64_t N, int64_t G, int a_f32, int kmaj) 
                     P.d.k_chunk = static_cast<int>(kc);
                     P.d.stages = stages;
                     P.smem = smem;
-                    P.grid = dim3(static_cast<unsigned>(S), static_cast<unsigned>(nt), static_cast<unsigned>(G));
+                    P.grid = dim3(static_cast<unsigned>(S), static_cast<unsigned>(nt), static_cast<unsigned>(G * chunks));
                 }
             }
         }
@@ -862,6 +866,7 @@ blr_status dtc_prepare(DtcPrep& P, const void* A, int a_f32, int64_t a_rs, int64
     d.K = static_cast<int>(K);
     d.N = static_cast<int>(N);
     d.n_units = 1;
+    d.groups = static_cast<int>(G);
     d.out = out;
     d.out_bf16 = out_bf16;
     d.o_rs = o_rs;
@@ -869,7 +874,9 @@ blr_status dtc_prepare(DtcPrep& P, const void* A, int a_f32, int64_t a_rs, int64
     d.o_cs = o_cs;
     d.pre = pre;
     P.kmaj = kmaj;
-    dtc_plan(P, K, N, G, a_f32, kmaj);
+    const int64_t chunks = cdiv(n, 16);
+    if (G * chunks > 65535) return BLR_ERR_UNSUPPORTED;
+    dtc_plan(P, K, N, G, a_f32, kmaj, chunks);
     if (P.cluster == 0) return BLR_ERR_UNSUPPORTED;
     if (getenv("BLR_DTC_VERBOSE"))
         fprintf(stderr, "dtc K=%lld N=%lld G=%lld kmaj=%d a_f32=%d: W=%d S=%d kc=%d stages=%d smem=%zu grid=%u\n",
@@ -963,6 +970,7 @@ blr_status dtc_prepare_blast_mix(DtcPrep& P, const void* X, int64_t d_in, int64_
     d.K = static_cast<int>(pdim);
     d.N = static_cast<int>(r);
     d.n_units = units;
+    d.groups = 1;
     d.out = zpp;
     d.out_bf16 = 0;
     d.o_rs = r;
@@ -994,7 +1002,8 @@ blr_status dtc_prepare_blast_mix(DtcPrep& P, const void* X, int64_t d_in, int64_
                 const int64_t ctas = cs * cdiv(r, w);
                 const int64_t resident = std::min<int64_t>(8, (228 * 1024) / (smem + 1024));
                 const double c = dtc_estimate(ctas, static_cast<double>(units) * kc * w * 2,
-                                              static_cast<double>(stages) * blr::DTC_STAGE, w, false, resident, true) +
+                                              static_cast<double>(stages) * blr::DTC_STAGE, w, false, resident, true,
+                                              cdiv(n, 16)) +
                                  0.3 * smem / (228.0 * 1024);
                 if (c < best) {
                     best = c;
@@ -1002,7 +1011,8 @@ blr_status dtc_prepare_blast_mix(DtcPrep& P, const void* X, int64_t d_in, int64_
                     d.k_chunk = kc;
                     d.stages = stages;
                     P.smem = smem;
-                    P.grid = dim3(static_cast<unsigned>(cs), static_cast<unsigned>(cdiv(r, w)), 1);
+                    P.grid = dim3(static_cast<unsigned>(cs), static_cast<unsigned>(cdiv(r, w)),
+                                  static_cast<unsigned>(cdiv(n, 16)));
                 }
             }
         }
@@ -1079,25 +1089,25 @@ void blr_clear_cache(void) {
     g_encode = nullptr;
 }
 
-// Workspace: the tcgen05 path's intermediate; for n_tok <= DECODE_MAX_TOKENS also enough for the
+// Workspace: the tcgen05 path's intermediate; for n_tok <= DTC_MAX_N also enough for the
 // decode path's fp32 intermediates and split-K partials (either path may run: BLR_DECODE=0).
 size_t blr_lowrank_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, int64_t r) {
     if (n_tok <= 0 || r <= 0) return 0;
     size_t b = static_cast<size_t>(n_tok) * r * 2 * comp_factor(r);
-    if (n_tok <= blr::DECODE_MAX_TOKENS && d_in > 0 && d_out > 0)
+    if (n_tok <= blr::DTC_MAX_N && d_in > 0 && d_out > 0)
         b = std::max(b, lowrank_decode_ws(n_tok, r));
     return b;
 }
 size_t blr_monarch_workspace_size(int64_t n_tok, int64_t, int64_t, int64_t b1, int64_t b2, int64_t r_blk) {
     if (n_tok <= 0 || b1 <= 0 || b2 <= 0 || r_blk <= 0) return 0;
     size_t b = static_cast<size_t>(b2) * n_tok * b1 * r_blk * 2 * comp_factor(b1 * r_blk);
-    if (n_tok <= blr::DECODE_MAX_TOKENS) b = std::max(b, monarch_decode_ws(n_tok, b1, b2, r_blk));
+    if (n_tok <= blr::DTC_MAX_N) b = std::max(b, monarch_decode_ws(n_tok, b1, b2, r_blk));
     return b;
 }
 size_t blr_blast_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2, int64_t r) {
     if (n_tok <= 0 || b1 <= 0 || b2 <= 0 || r <= 0) return 0;
     size_t b = blast_ws_bytes(n_tok, b1, b2, r);
-    if (n_tok <= blr::DECODE_MAX_TOKENS && d_in > 0 && d_out > 0 && d_in % b1 == 0 && d_out % b2 == 0)
+    if (n_tok <= blr::DTC_MAX_N && d_in > 0 && d_out > 0 && d_in % b1 == 0 && d_out % b2 == 0)
         b = std::max(b, blast_decode_ws(n_tok, b1, b2, r));
     return b;
 }
@@ -1199,7 +1209,7 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
     blr_status s = device_info(d, dev);
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (use_decode(n_tok, 8)) {  // small-n path: fp32 Z' [b2][n][b1 r'], permutations in the index maps
+    if (use_decode(n_tok, 256)) {  // small-n path: fp32 Z' [b2][n][b1 r'], permutations in the index maps
         float* zp = static_cast<float*>(workspace);
         DtcPrep p1, p2;
         s = dtc_prepare(p1, X, 0, d_in, pdim, V, 1, pdim, r_blk * b2 * pdim, zp, 0, K2, n_tok * K2, 1, n_tok, pdim,
@@ -1373,7 +1383,9 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
     blr_status s = device_info(d, dev);
     if (s != BLR_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (use_decode(n_tok, 8)) {  // small-n path: fp32 Z [b1][n][r] (unless fused away) and Z'' [b2][n][r]
+    // small n: the weight-streaming kernels; up to 2048 tokens where the tcgen05 alternative is the
+    // S1+S2-fused projection, whose parallelism is the handful of 128-token tiles (C1, C5 ViT-B)
+    if (use_decode(n_tok, blast_fused(b1, r) ? 2048 : 8)) {  // fp32 Z [b1][n][r] (unless fused away), Z'' [b2][n][r]
         float* z = static_cast<float*>(workspace);
         float* zp2 = z + b1 * n_tok * r;
         int cs = 0, units = 0;

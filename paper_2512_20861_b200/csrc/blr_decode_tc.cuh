@@ -40,6 +40,7 @@ constexpr int DTC_MAX_KC = 1024;                 // K rows per CTA (A slice <= 2
 constexpr int DTC_MAX_UNITS = 4;                 // EPI 2: BLAST blocks l per CTA
 constexpr int DTC_MAX_CLUSTER = 8;
 constexpr int DTC_MAX_B1 = 16;
+constexpr int DTC_MAX_N = 4096;                  // tokens the weight-streaming path may take (16-row chunks)
 
 // K rows per stage and TMA boxes per stage of a (KMAJ, W) tile.  MN-major: W/64 boxes of 64
 // columns x BK rows.  K-major (W = 64 output columns): 2 boxes of 64 k x 64 columns, BK = 128.
@@ -51,6 +52,7 @@ struct DecodeTC {
     int a_f32;
     long long a_rs, a_gs;   // element strides: token rows, groups
     int n_tok, K, N, k_chunk, n_units, stages;
+    int groups;             // G: grid.z = G x ceil(n_tok / 16) token chunks (EPI 2: the chunks alone)
     void* out;              // fp32 or bf16 (out_bf16, RNE)
     int out_bf16;
     long long o_rs, o_gs, o_cs;  // element strides: token rows, groups, output columns
@@ -147,7 +149,13 @@ __global__ void __launch_bounds__(DTC_THREADS)
     const int kc = min(d.k_chunk, d.K - k0);
     const int nkb = (kc + BK - 1) / BK;
     const int nt = blockIdx.y;
-    auto group_of = [&](int u) { return EPI == 2 ? static_cast<int>(blockIdx.x) * d.n_units + u : static_cast<int>(blockIdx.z); };
+    // token chunk of 16 rows (n > 16: chunks are independent CTAs re-reading the weights from L2)
+    const int chunk = EPI == 2 ? static_cast<int>(blockIdx.z) : static_cast<int>(blockIdx.z) / d.groups;
+    const int gz = EPI == 2 ? 0 : static_cast<int>(blockIdx.z) - chunk * d.groups;
+    const int n_here = min(16, d.n_tok - chunk * 16);
+    const void* Ab = static_cast<const char*>(d.A) + static_cast<long long>(chunk) * 16 * d.a_rs * (d.a_f32 ? 4 : 2);
+    void* Ob = static_cast<char*>(d.out) + static_cast<long long>(chunk) * 16 * d.o_rs * (d.out_bf16 ? 2 : 4);
+    auto group_of = [&](int u) { return EPI == 2 ? static_cast<int>(blockIdx.x) * d.n_units + u : gz; };
 
     const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
     unsigned long long* tr = (d.trace && cta_lin < 2048) ? d.trace + cta_lin * 16 : nullptr;
@@ -212,8 +220,8 @@ __global__ void __launch_bounds__(DTC_THREADS)
                         const int e = e0 + j * DTC_MMA_WARPS * 32;
                         const int t = e / k8n, k = (e - t * k8n) * 8;
                         v[j] = make_uint4(0, 0, 0, 0);
-                        if (e < total && t < d.n_tok && k < kc)
-                            v[j] = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(d.A) +
+                        if (e < total && t < n_here && k < kc)
+                            v[j] = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(Ab) +
                                                                    static_cast<long long>(g) * d.a_gs +
                                                                    static_cast<long long>(t) * d.a_rs + k0 + k);
                     }
@@ -230,8 +238,8 @@ __global__ void __launch_bounds__(DTC_THREADS)
                         const int e = e0 + j * DTC_MMA_WARPS * 32;
                         const int t = e / k8n, k = (e - t * k8n) * 8;
                         v[j][0] = v[j][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-                        if (e < total && t < d.n_tok && k < kc) {
-                            const float* p = static_cast<const float*>(d.A) + static_cast<long long>(g) * d.a_gs +
+                        if (e < total && t < n_here && k < kc) {
+                            const float* p = static_cast<const float*>(Ab) + static_cast<long long>(g) * d.a_gs +
                                              static_cast<long long>(t) * d.a_rs + k0 + k;
                             v[j][0] = *reinterpret_cast<const float4*>(p);
                             v[j][1] = *reinterpret_cast<const float4*>(p + 4);
@@ -334,14 +342,14 @@ __global__ void __launch_bounds__(DTC_THREADS)
                 for (int h = 0; h < 2; ++h) {
                     const int t = t0 + 8 * h;
                     const int c = nt * W + cw0 + j * 8 + 2 * (lane & 3);
-                    if (t >= d.n_tok || c >= d.N) continue;  // N % 8 == 0: c < N => c + 1 < N
+                    if (t >= n_here || c >= d.N) continue;  // N % 8 == 0: c < N => c + 1 < N
                     const float v0 = acc[j][2 * h], v1 = acc[j][2 * h + 1];
                     if (d.col_map == 0 && d.o_cs == 1) {
                         const long long off = static_cast<long long>(g) * d.o_gs + static_cast<long long>(t) * d.o_rs + c;
                         if (d.out_bf16)
-                            *reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(d.out) + off) = ptx::pack_bf16x2(v0, v1);
+                            *reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(Ob) + off) = ptx::pack_bf16x2(v0, v1);
                         else
-                            *reinterpret_cast<float2*>(static_cast<float*>(d.out) + off) = make_float2(v0, v1);
+                            *reinterpret_cast<float2*>(static_cast<float*>(Ob) + off) = make_float2(v0, v1);
                     } else {
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
@@ -356,8 +364,8 @@ __global__ void __launch_bounds__(DTC_THREADS)
                                       static_cast<long long>(g) * d.mon_r + rho;
                             }
                             const float v = e ? v1 : v0;
-                            if (d.out_bf16) static_cast<__nv_bfloat16*>(d.out)[off] = __float2bfloat16_rn(v);
-                            else static_cast<float*>(d.out)[off] = v;
+                            if (d.out_bf16) static_cast<__nv_bfloat16*>(Ob)[off] = __float2bfloat16_rn(v);
+                            else static_cast<float*>(Ob)[off] = v;
                         }
                     }
                 }
@@ -385,11 +393,11 @@ __global__ void __launch_bounds__(DTC_THREADS)
     const int ncl = gridDim.x;  // cluster = the grid's x extent
     const int q = blockIdx.x;
     if (EPI == 1) {  // sum the S split partials of 1/S of the tile (4 columns per item), ascending split order
-        const int g = blockIdx.z;
+        const int g = gz;
         uint32_t rz[DTC_MAX_CLUSTER];
 #pragma unroll
         for (int z = 0; z < DTC_MAX_CLUSTER; ++z) rz[z] = dtc::mapa(red_s, z < ncl ? z : 0);
-        for (int e4 = q + ncl * tid; e4 < d.n_tok * (W / 4); e4 += ncl * DTC_MMA_WARPS * 32) {
+        for (int e4 = q + ncl * tid; e4 < n_here * (W / 4); e4 += ncl * DTC_MMA_WARPS * 32) {
             const int t = e4 / (W / 4), col = (e4 - t * (W / 4)) * 4;
             const int c = nt * W + col;
             if (c >= d.N) continue;  // N % 8 == 0: c < N => c + 3 < N
@@ -409,10 +417,10 @@ __global__ void __launch_bounds__(DTC_THREADS)
             if (d.col_map == 0 && d.o_cs == 1) {
                 const long long off = static_cast<long long>(g) * d.o_gs + static_cast<long long>(t) * d.o_rs + c;
                 if (d.out_bf16)
-                    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(d.out) + off) =
+                    *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(Ob) + off) =
                         make_uint2(ptx::pack_bf16x2(v[0], v[1]), ptx::pack_bf16x2(v[2], v[3]));
                 else
-                    *reinterpret_cast<float4*>(static_cast<float*>(d.out) + off) = make_float4(v[0], v[1], v[2], v[3]);
+                    *reinterpret_cast<float4*>(static_cast<float*>(Ob) + off) = make_float4(v[0], v[1], v[2], v[3]);
                 continue;
             }
 #pragma unroll
@@ -427,8 +435,8 @@ __global__ void __launch_bounds__(DTC_THREADS)
                     off = static_cast<long long>(k) * d.o_gs + static_cast<long long>(t) * d.o_rs +
                           static_cast<long long>(g) * d.mon_r + rho;
                 }
-                if (d.out_bf16) static_cast<__nv_bfloat16*>(d.out)[off] = __float2bfloat16_rn(v[j]);
-                else static_cast<float*>(d.out)[off] = v[j];
+                if (d.out_bf16) static_cast<__nv_bfloat16*>(Ob)[off] = __float2bfloat16_rn(v[j]);
+                else static_cast<float*>(Ob)[off] = v[j];
             }
         }
     } else {  // BLAST S2: Z''_k[t][rho] = sum_l S[l,k,rho] Z_l[t][rho], l ascending, k = q, q + cs, ...
@@ -439,7 +447,7 @@ __global__ void __launch_bounds__(DTC_THREADS)
             const int ll = l < d.b1 ? l : 0;
             rz[l] = dtc::mapa(red_s + (ll % d.n_units) * 16 * W * 4, ll / d.n_units);
         }
-        for (int e4 = tid; e4 < d.n_tok * (W / 4); e4 += DTC_MMA_WARPS * 32) {
+        for (int e4 = tid; e4 < n_here * (W / 4); e4 += DTC_MMA_WARPS * 32) {
             const int t = e4 / (W / 4), col = (e4 - t * (W / 4)) * 4;
             const int rho = nt * W + col;
             if (rho >= d.N) continue;
@@ -460,7 +468,7 @@ __global__ void __launch_bounds__(DTC_THREADS)
                         v[2] = fmaf(__uint_as_float(sv.y << 16), z[l].z, v[2]);
                         v[3] = fmaf(__uint_as_float(sv.y & 0xFFFF0000u), z[l].w, v[3]);
                     }
-                *reinterpret_cast<float4*>(static_cast<float*>(d.out) + static_cast<long long>(k) * d.o_gs +
+                *reinterpret_cast<float4*>(static_cast<float*>(Ob) + static_cast<long long>(k) * d.o_gs +
                                            static_cast<long long>(t) * d.o_rs + rho) = make_float4(v[0], v[1], v[2], v[3]);
             }
         }

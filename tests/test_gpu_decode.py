@@ -88,6 +88,22 @@ def test_decode_forced_plans(cuda_lib, monkeypatch, w, s):
         assert_parity(Y, ref, f"LR decode W={w} S={s} n={n}")
 
 
+@pytest.mark.parametrize("n", [17, 100, 333])
+def test_decode_token_chunks(cuda_lib, monkeypatch, n):
+    """n > 16 on the weight-streaming kernels (BLR_DECODE_MAXN): independent 16-row token chunks,
+    the last one ragged, for all three methods (incl. the BLAST cluster S2 and a K split)."""
+    monkeypatch.delenv("BLR_DECODE", raising=False)
+    monkeypatch.setenv("BLR_DECODE_MAXN", "4096")
+    Y, ref = _lr(cuda_lib, n, 3072, 768, 192)
+    assert_parity(Y, ref, f"LR chunks n={n}")
+    Y, ref = _blast(cuda_lib, n, 6, 6, 192, 128, 512)
+    assert_parity(Y, ref, f"BLAST chunks n={n}")
+    Y, ref = _blast(cuda_lib, n, 11, 3, 40, 16, 24)
+    assert_parity(Y, ref, f"BLAST (S1, S2, S3) chunks n={n}")
+    Y, ref = _mon(cuda_lib, n, 4, 4, 48, 192, 768, orc.RPRIME_FASTEST)
+    assert_parity(Y, ref, f"Monarch chunks n={n}")
+
+
 @pytest.mark.parametrize("n", [1, 16])
 def test_small_n_on_the_tcgen05_path(cuda_lib, monkeypatch, n):
     """BLR_DECODE=0 keeps small n on the prefill kernels: both paths meet the same bar."""
