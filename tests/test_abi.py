@@ -42,18 +42,22 @@ def test_status_strings_and_version():
 
 def test_workspace_sizes():
     lib = blr.load()
+    # n above the weight-streaming path's range (DTC_MAX_N = 4096): only the tcgen05 path's intermediate
+    n = 5000
     # S3 contraction >= 128: one bf16 intermediate
-    assert lib.blr_lowrank_workspace_size(100, 64, 64, 128) == 100 * 128 * 2
-    assert lib.blr_monarch_workspace_size(100, 64, 64, 4, 2, 32) == 2 * 100 * 4 * 32 * 2
+    assert lib.blr_lowrank_workspace_size(n, 64, 64, 128) == n * 128 * 2
+    assert lib.blr_monarch_workspace_size(n, 64, 64, 4, 2, 32) == 2 * n * 4 * 32 * 2
     # BLAST with b1*r <= 512 fuses S1+S2 (only Z''); larger b1*r also keeps the S1 output Z_l
-    assert lib.blr_blast_workspace_size(100, 64, 64, 2, 2, 192) == 2 * 100 * 192 * 2
+    assert lib.blr_blast_workspace_size(n, 64, 64, 2, 2, 192) == 2 * n * 192 * 2
     # split path: Z'' and fp16 Z (R13), token rows padded to whole 128-row tiles (tile-blocked, §5.4)
-    assert lib.blr_blast_workspace_size(100, 64, 64, 4, 2, 192) == 2 * 128 * 192 * 2 + 4 * 128 * 192 * 2
+    assert lib.blr_blast_workspace_size(n, 64, 64, 4, 2, 192) == 2 * 5120 * 192 * 2 + 4 * 5120 * 192 * 2
     # shorter contractions keep a compensated hi|lo pair: twice the bytes
-    assert lib.blr_lowrank_workspace_size(100, 64, 64, 16) == 2 * 100 * 16 * 2
-    assert lib.blr_monarch_workspace_size(100, 64, 64, 4, 2, 8) == 2 * 2 * 100 * 4 * 8 * 2
-    assert lib.blr_blast_workspace_size(100, 64, 64, 4, 2, 16) == 2 * 2 * 100 * 16 * 2  # fused (b1 r <= 512)
+    assert lib.blr_lowrank_workspace_size(n, 64, 64, 16) == 2 * n * 16 * 2
+    assert lib.blr_monarch_workspace_size(n, 64, 64, 4, 2, 8) == 2 * 2 * n * 4 * 8 * 2
+    assert lib.blr_blast_workspace_size(n, 64, 64, 4, 2, 16) == 2 * 2 * n * 16 * 2  # fused (b1 r <= 512)
     assert lib.blr_blast_workspace_size(0, 64, 64, 4, 2, 16) == 0
+    # n <= DTC_MAX_N: the larger of the tcgen05 intermediate and the fp32 weight-streaming one
+    assert lib.blr_lowrank_workspace_size(100, 64, 64, 128) == max(100 * 128 * 2, 100 * 128 * 4)
 
 
 def test_workspace_sizes_cover_the_decode_path():
@@ -63,8 +67,8 @@ def test_workspace_sizes_cover_the_decode_path():
     assert lib.blr_lowrank_workspace_size(n, i, o, r) >= n * r * 4          # fp32 Z
     assert lib.blr_blast_workspace_size(n, i, o, 16, 16, r) >= (16 + 16) * n * r * 4  # fp32 Z, Z''
     assert lib.blr_monarch_workspace_size(n, i, o, 16, 16, 96) >= 16 * n * 16 * 96 * 4  # fp32 Z'
-    # above the decode threshold only the tcgen05 path's bf16 intermediate is needed
-    assert lib.blr_lowrank_workspace_size(17, i, o, r) == 17 * r * 2
+    # above the weight-streaming range only the tcgen05 path's bf16 intermediate is needed
+    assert lib.blr_lowrank_workspace_size(4097, i, o, r) == 4097 * r * 2
 
 
 FAKE = 0x10000  # 16-B aligned, never dereferenced: validation fails before any CUDA call
