@@ -241,8 +241,12 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     KParams p = p_in;
     p.trace = t_trace;
     p.first = t_last_launches == 0 ? 1 : 0;  // first launch of this API call (PDL ordering, kernel)
-    p.mma_burst = (PAIR == 1 || p.b_resident || KIND != blr::KIND_GEMM) ? 1 : 0;
+    // K blocks issued as one unrolled MMA burst (all plans: with the lean producer the burst no longer
+    // measured slower on the streamed pair plans)
+    p.mma_burst = 1;
     if (const char* e = getenv("BLR_BURST")) p.mma_burst = atoi(e);
+    p.fast_prod = 1;
+    if (const char* e = getenv("BLR_FASTPROD")) p.fast_prod = atoi(e);
 #ifdef BLR_DEBUG_KNOBS
     if (const char* e = getenv("BLR_DBG")) p.dbg = atoi(e);  // debug experiments only
     if (const char* e = getenv("BLR_DBG_LAUNCH"); e && atoi(e) != t_last_launches) p.dbg = 0;  // only launch k

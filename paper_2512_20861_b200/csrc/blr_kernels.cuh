@@ -111,6 +111,13 @@ struct KParams {
     int dbg;                    // debug bits (BLR_DEBUG_KNOBS builds only): 1 skip bulk stores, 2 skip staging,
                                 //   4 skip the whole GEMM epilogue, 8 skip MMAs, 16 plain-arrive slot release (PAIR 1),
                                 //   32 no accumulator hand-off, 64 no resident weight loads
+    int fast_prod;              // 1: the lean GEMM producer loop (BLR_FASTPROD=0 selects the generic one)
+    // ---- pipelined BLAST layer (blast_pipe_kernel): per-128-token-tile ready counters
+    const unsigned int* pipe_wait;  // A's token tile t is ready once pipe_wait[t] >= pipe_target (nullptr: off)
+    unsigned int pipe_target;
+    unsigned int* pipe_sig;         // the epilogue adds 1 per (tile, store issuer) once the tile's stores landed
+    int no_trigger;                 // 1: never trigger the dependent grid early (its CTAs could take the SMs
+                                    //    this grid's later CTAs need while the earlier ones wait on them)
 };
 
 struct SmemLayout {
@@ -405,7 +412,101 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint32_t nslices = 0;
             bool waited = p.first != 0;
             int nstep_tr = 0;
-            for (int it = 0; it < ntiles; ++it) {
+            int pipe_ok = -1;  // highest token tile of A known ready (pipelined layer)
+            bool fast_done = false;
+            if constexpr (KIND == KIND_GEMM) {
+                if (mcs == 1 && trace == nullptr && p.fast_prod) {
+                    // Lean producer for the GEMM kind: every parameter the K loop needs is hoisted
+                    // into registers and every per-tile coordinate computed once per tile, so a K
+                    // block costs a barrier wait, an expect_tx and its TMA issues.  (The generic loop
+                    // below re-read kernel parameters after every asm statement and divided per K
+                    // block: ~130 instructions at ~12 cycles each, 1.6k cycles per 480-cycle K block
+                    // of MMA work -- the producer, not the tensor pipe, bounded C4 gate S3, ncu.)
+                    fast_done = true;
+                    const int kbox = ptx::pin(p.kbox), stages = ptx::pin(p.stages), kb_half = ptx::pin(p.kb_half);
+                    const int a_lo_off = ptx::pin(p.a_lo_off);
+                    const bool a_blk_mode = p.a_blocked != 0, a_gmid = p.a_gmid != 0;
+                    const bool b_res = p.b_resident != 0, b_mn = p.b_mn_major != 0;
+                    const int n_mma = ptx::pin(p.n_mma), b_boxes = ptx::pin(p.b_boxes), b_box_n = ptx::pin(p.b_box_n);
+                    const int BNf = p.BN;
+                    const int bn_h = ptx::pin(BNf / n_mma);     // columns per MMA half
+                    const int bn_cta = bn_h / PAIR;             // this CTA's columns of a half
+                    const uint32_t b_stage_b = ptx::pin(p.b_stage_bytes), b_half_b = ptx::pin(p.b_half_bytes);
+                    const uint32_t box_b = static_cast<uint32_t>(b_box_n) * BK * 2;
+                    const int a_tiles = p.a_tiles;
+                    const int ns = ptx::pin(n_steps);
+                    const uint32_t tx_f = ptx::pin(tx);
+                    for (int it = 0; it < ntiles; ++it) {
+                        const TileCoord tc = tile_get(p, titer, tile_tab, it);
+                        const int t128 = tc.m_blk * PAIR + static_cast<int>(crank);
+                        const int m0 = t128 * BM;
+                        if (b_res && tc.slice != cur_slice) {
+                            if (nslices > 0) ptx::mbar_wait(bfree_bar, (nslices - 1) & 1);
+                            if (ptx::elect_one()) {
+                                const int n0 = tc.n_blk * BNf + static_cast<int>(crank) * (BNf / PAIR);
+                                for (int kb = 0; kb < kbr; ++kb) {
+                                    const uint32_t b_dst = b_base + kb * b_stage_b;
+                                    const uint32_t bb = bfull_bar + 8 * kb;
+                                    if (leader) ptx::mbar_arrive_expect_tx(bb, b_bytes * PAIR);
+                                    if (b_mn) {
+                                        for (int j = 0; j < b_boxes; ++j)
+                                            load3(b_dst + j * box_b, &tmB, bb, n0 + j * b_box_n, kb * BK, tc.g);
+                                    } else {
+                                        load3(b_dst, &tmB, bb, kb * BK, n0, tc.g);
+                                    }
+                                }
+                            }
+                            __syncwarp();
+                            cur_slice = tc.slice;
+                            ++nslices;
+                        }
+                        if (!waited) {
+                            ptx::griddep_wait();
+                            waited = true;
+                        }
+                        if (p.pipe_wait != nullptr && t128 > pipe_ok) {
+                            ptx::pipe_acquire(p.pipe_wait + t128, p.pipe_target);  // A's token tile is ready
+                            pipe_ok = t128;
+                        }
+                        const int a_row0 = (tc.g * a_tiles + t128) * a_nch * 16;  // tile-blocked A
+                        const int a_c1 = a_gmid ? tc.g : m0, a_c2 = a_gmid ? m0 : tc.g;
+                        const int nb0 = tc.n_blk * BNf + static_cast<int>(crank) * bn_cta;  // half 0, this CTA
+                        for (int si = 0; si < ns; ++si) {
+                            ptx::mbar_wait(empty_bar + 8 * stage, phase ^ 1);
+                            const uint32_t fb = full_bar + 8 * stage;
+                            const uint32_t a_st = a_base + stage * (a_blk * kbox);
+                            const uint32_t b_st = b_base + stage * (b_stage_b * kbox);
+                            if (ptx::elect_one()) {
+                                if (leader) ptx::mbar_arrive_expect_tx(fb, tx_f);
+                                for (int j = 0; j < kbox; ++j) {
+                                    const int kb = si * kbox + j;
+                                    const int part = (a_lo_off > 0 && kb >= kb_half) ? 1 : 0;
+                                    const int k0 = (kb - part * kb_half) * BK;  // padded block: zero-filled
+                                    const uint32_t a_dst = a_st + j * a_blk;
+                                    if (a_blk_mode) load3(a_dst, &tmA, fb, 0, a_row0 + kb * 128, 0);
+                                    else load3(a_dst, &tmA, fb, part * a_lo_off + k0, a_c1, a_c2);
+                                    if (!b_res) {
+                                        const uint32_t b_dst = b_st + j * b_stage_b;
+                                        for (int h = 0; h < n_mma; ++h) {
+                                            const int nh = nb0 + h * bn_h;
+                                            const uint32_t bh = b_dst + h * b_half_b;
+                                            if (b_mn) {
+                                                for (int q = 0; q < b_boxes; ++q)
+                                                    load3(bh + q * box_b, &tmB, fb, nh + q * b_box_n, k0, tc.g);
+                                            } else {
+                                                load3(bh, &tmB, fb, k0, nh, tc.g);
+                                            }
+                                        }
+                                    }
+                                }
+                            }
+                            __syncwarp();
+                            if (++stage == stages) { stage = 0; phase ^= 1; }
+                        }
+                    }
+                }
+            }
+            for (int it = 0; !fast_done && it < ntiles; ++it) {
                 const TileCoord tc = tile_get(p, titer, tile_tab, it);
                 const int m0 = ((tc.m_blk * mcs + static_cast<int>(pidx)) * PAIR + static_cast<int>(crank)) * BM;
                 const int n0 = tc.n_blk * p.BN + static_cast<int>(crank) * (p.BN / PAIR);  // this CTA's B half

@@ -181,7 +181,9 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) {
     uint32_t raddr;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(bar), "r"(rank));
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
+    // default semantics (release, CTA scope): the .cluster-scope release compiled to a full
+    // MEMBAR.ALL.GPU per arrive (~17% of the pair epilogue's stall samples, C4 gate S3 ncu)
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
 }
 template <int NCOLS>
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t dst_smem) {  // one warp in each CTA
@@ -364,6 +366,37 @@ __device__ __forceinline__ void unpack_f32x2(unsigned long long v, float& lo, fl
 
 // Programmatic dependent launch (griddepcontrol): wait for the preceding grid's completion and
 // memory flush / allow the next grid in the stream to start launching.
+// Pin a value in a register: the compiler otherwise re-materialises hoisted kernel parameters as
+// constant-bank loads inside loops (after every asm statement with a memory clobber).
+__device__ __forceinline__ int pin(int x) {
+    int r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+__device__ __forceinline__ uint32_t pin(uint32_t x) {
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(x));
+    return r;
+}
+
+// ---- cross-CTA ready counters (pipelined BLAST layer) -------------------------------------------
+// Producer side, after cp.async.bulk.wait_group 0 made this thread's bulk stores complete: order
+// them (async proxy) before the generic release, then publish.
+__device__ __forceinline__ void pipe_release(unsigned int* ctr) {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+}
+// Consumer side: spin until *ctr >= target (acquire), then order the async-proxy (TMA) reads
+// that follow after it.
+__device__ __forceinline__ void pipe_acquire(const unsigned int* ctr, unsigned int target) {
+    unsigned int v;
+    while (true) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+        if (v >= target) break;
+        __nanosleep(64);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
