@@ -162,8 +162,9 @@ bool pdl_enabled() {
     return !(e && e[0] == '1');
 }
 
+thread_local int t_smem_reserve = 0;  // bytes a planning caller keeps free (pipelined layer: its ticket)
 bool fits(const KParams& p) {
-    return blr::smem_layout(p).total + SMEM_SLACK <= static_cast<uint32_t>(SMEM_LIMIT);
+    return blr::smem_layout(p).total + SMEM_SLACK + t_smem_reserve <= static_cast<uint32_t>(SMEM_LIMIT);
 }
 
 // Decide weight-stationary vs streaming, staging buffers and ring depth.  `allow_resident`:
@@ -400,7 +401,8 @@ struct OutMap {  // 4-D view (N, comp, groups, rows) of a GEMM phase's output
 // wide: a CTA-pair tile of up to 512 columns as two MMAs per K step (KParams::n_mma), single
 // accumulator buffer, streamed B only.
 bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok, int64_t K, int64_t groups,
-               int64_t N, bool b_mn_major, const OutMap& out, int comp, bool wide = false, int mc = 1) {
+               int64_t N, bool b_mn_major, const OutMap& out, int comp, bool wide = false, int mc = 1,
+               bool allow_res = true) {
     p = KParams{};
     p.a_gmid = a_gmid;
     p.n_tok = static_cast<int>(n_tok);
@@ -444,7 +446,7 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
         p.c_box_w = p.BN / 2;
     p.c_swz = out.blocked ? 0 : pick_swz(p.c_box_w * esz).mask;
     if (mc > 1 && !b_mn_major && (bn_full / p.n_mma / pair) % (8 * mc)) return false;  // K-major slices
-    return finish_plan(p, !wide && mc == 1, 32 * p.c_box_w * esz, d.sm_count / (pair * mc));
+    return finish_plan(p, allow_res && !wide && mc == 1, 32 * p.c_box_w * esz, d.sm_count / (pair * mc));
 }
 
 // A planned GEMM phase: parameters and tensor maps, encoded before anything is launched (so a
@@ -475,13 +477,16 @@ blr_status gemm_run(const GemmPrep& g, const DevInfo& d, int dev, cudaStream_t s
 //   comp == 2: A rows hold [hi | lo] (lo at column offset K) multiplying the same B rows.
 // CTA pairs (cta_group::2) are used when the weight slice would otherwise stream and outweighs
 // the activation tile (BLR_PAIR=1/2 forces a mode).
+// force_pair = 2 / no_res: the pipelined BLAST layer's roles (CTA pairs, streamed weights, so that
+// every role walks the token tiles in order).
 blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid, int64_t a_row_stride,
                         int64_t a_group_stride, int64_t n_tok, int64_t K, int64_t groups, int64_t N, const void* B,
-                        bool b_mn_major, const OutMap& out, int comp, int a_blocked = 0) {
+                        bool b_mn_major, const OutMap& out, int comp, int a_blocked = 0, int force_pair = 0,
+                        bool no_res = false) {
     KParams& p = g.p;
     int pair = 1;
     const char* pe = getenv("BLR_PAIR");
-    const int force = pe ? atoi(pe) : 0;
+    const int force = force_pair ? force_pair : pe ? atoi(pe) : 0;
     if (force == 2 && n_tok >= 256) {
         pair = 2;
     } else if (force != 1) {
@@ -499,8 +504,9 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
         const char* lkp = getenv("BLR_LONGK_PAIR");
         if (!(lkp && lkp[0] == '0') && !p.b_resident && n_tok >= 1024 && p.BN >= 192 && K >= 1024) pair = 2;
     }
-    if (!plan_gemm(p, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp)) {
-        if (pair == 1 || !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp))
+    if (!plan_gemm(p, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, false, 1, !no_res)) {
+        if (force_pair || pair == 1 ||
+            !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, false, 1, !no_res))
             return BLR_ERR_UNSUPPORTED;
     }
     // wide pair tiles (two MMAs per K step, <= 512 columns, single accumulator): half the operand
@@ -509,7 +515,7 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
     {
         const char* we = getenv("BLR_WIDE");
         // measured no faster than 256-column pair tiles (C4 gate/down in-process A/B): opt-in only
-        const bool want = we && we[0] == '1';
+        const bool want = we && we[0] == '1' && !force_pair;
         if (want && pair == 2 && out.col_stride == 0) {
             KParams w;
             if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, true)) p = w;
@@ -522,7 +528,7 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
         // lock-stepped slot release): opt-in only
         const char* me = getenv("BLR_MC");
         int mc = me ? atoi(me) : 1;
-        if (mc > 1 && pair == 2 && !p.b_resident && n_tok >= 2048 * mc) {
+        if (mc > 1 && pair == 2 && !p.b_resident && n_tok >= 2048 * mc && !force_pair) {
             KParams w;
             if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, p.n_mma == 2, mc)) p = w;
         }
@@ -1032,12 +1038,20 @@ blr_status dtc_prepare_blast_mix(DtcPrep& P, const void* X, int64_t d_in, int64_
     return BLR_OK;
 }
 
+// Pipelined BLAST layer: ticket + Z-ready + Z''-ready counters, one per 128-token tile of the CTA
+// pairs' 256-row tiles (padded), after the split path's Z'' and Z
+size_t pipe_ctr_bytes(int64_t n_tok) {
+    const int64_t tiles_pad = 2 * cdiv(n_tok, 2 * blr::BM);
+    return static_cast<size_t>(rup(4 * (1 + 2 * tiles_pad), 256));
+}
+
 size_t blast_ws_bytes(int64_t n_tok, int64_t b1, int64_t b2, int64_t r) {
     if (blast_fused(b1, r)) return static_cast<size_t>(b2) * n_tok * r * 2 * comp_factor(r);
     // split path: Z'' and the fp16 Z_l of the separate S1, token count padded to whole 128-row
     // tiles (the tensor-core S2 path stores both tile-blocked)
     const int64_t np = rup(n_tok, blr::BM);
-    return static_cast<size_t>(b2) * np * r * 2 * comp_factor(r) + static_cast<size_t>(b1) * np * r * 2;
+    return static_cast<size_t>(b2) * np * r * 2 * comp_factor(r) + static_cast<size_t>(b1) * np * r * 2 +
+           pipe_ctr_bytes(n_tok);
 }
 
 }  // namespace
@@ -1369,6 +1383,153 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
 
 namespace {
 // fp8z: the split path stores Z_l as e4m3; elsewhere identical
+// ---- pipelined BLAST layer (blast_pipe_kernel) --------------------------------
+constexpr int PIPE_STATIC_SMEM = 16;  // the role ticket after the roles' smem, kept free of the plans
+// Opt-in (BLR_PIPE=1): measured slower than the three launches so far -- its S2 role needs ~40 SMs
+// to keep up (C4 gate layer 8.4 vs 4.35 ms)
+bool pipe_wanted(int64_t n_tok, int64_t b1, int64_t b2, int64_t r) {
+    if (b1 > 16 || b2 > 16 || r % 8) return false;
+    const char* e = getenv("BLR_PIPE");
+    return e && e[0] == '1' && n_tok >= 256;
+}
+
+// Clusters (CTA pairs) per role, from the phases' work: tensor FLOPs of S1 and S3, S2's bytes at
+// an assumed per-cluster rate (BLR_PIPE_SPLIT="n1,n2" overrides; the rest go to S3).
+void pipe_split(int units, double f1, double f3, double b2_bytes, int& n1, int& n2, int& n3) {
+    const char* e = getenv("BLR_PIPE_SPLIT");
+    if (e && sscanf(e, "%d,%d", &n1, &n2) == 2 && n1 >= 1 && n2 >= 1 && n1 + n2 < units) {
+        n3 = units - n1 - n2;
+        return;
+    }
+    // per-cluster rates: ~2 x 5.5 TFLOP/s on the tensor cores (measured C4 GEMM phases), ~0.2 TB/s
+    // of S2 traffic (L2-resident Z / Z'')
+    const double t1 = f1 / 11e12, t3 = f3 / 11e12, t2 = b2_bytes / 0.2e12;
+    const double tot = t1 + t2 + t3;
+    n1 = std::max(1, static_cast<int>(units * t1 / tot + 0.5));
+    n2 = std::max(1, static_cast<int>(units * t2 / tot + 0.5));
+    n3 = units - n1 - n2;
+    if (n3 < 1) {
+        n3 = 1;
+        n1 = std::max(1, units - n2 - n3);
+        n2 = units - n1 - n3;
+    }
+}
+
+blr_status blast_pipe(const DevInfo& d, int dev, cudaStream_t st, const void* X, int64_t d_in, int64_t pdim,
+                      int64_t n_tok, int64_t b1, int64_t b2, int64_t r, const void* V, const void* S, const void* U,
+                      void* Y, int64_t qdim, void* zl, void* zpp, void* ctr_mem, const CUtensorMap& tmz,
+                      const CUtensorMap& tmzpp) {
+    const int64_t n_pad = rup(n_tok, blr::BM);
+    const int tiles = static_cast<int>(cdiv(n_tok, blr::BM));
+    const int tiles_pad = static_cast<int>(2 * cdiv(n_tok, 2 * blr::BM));
+    const int64_t d_out = b2 * qdim;
+    GemmPrep g1, g3;
+    OutMap zmap{zl, 2, 1, r, n_pad * r, r};
+    zmap.blocked = 1;
+    // both GEMM roles as CTA pairs with streamed weights (token-tile-ordered walks)
+    t_smem_reserve = PIPE_STATIC_SMEM;
+    blr_status s = gemm_prepare(g1, d, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true, zmap, 1, 0, 2, true);
+    if (s == BLR_OK)
+        s = gemm_prepare(g3, d, zpp, 0, r, n_tok * r, n_tok, r, b2, qdim, U, true, OutMap{Y, 0, 1, d_out, qdim, d_out},
+                         1, /*a_blocked=*/1, 2, true);
+    t_smem_reserve = 0;
+    const bool plan_print = getenv("BLR_PLAN") && getenv("BLR_PLAN")[0] == '1';
+    if (s != BLR_OK) {
+        if (plan_print) fprintf(stderr, "[blr plan] pipe: role planning failed (%d)\n", static_cast<int>(s));
+        return s;
+    }
+    if (g1.pair != 2 || g1.outf != 2 || g1.p.b_resident || g3.pair != 2 || g3.outf != 0 || g3.p.b_resident ||
+        g1.p.mc > 1 || g3.p.mc > 1) {
+        if (plan_print) fprintf(stderr, "[blr plan] pipe: role plans unsupported, three launches\n");
+        return BLR_ERR_UNSUPPORTED;
+    }
+    const blr::S2MLayout sl = blr::s2m_layout(static_cast<int>(b1), static_cast<int>(b2), false);
+    const uint32_t tot1 = blr::smem_layout(g1.p).total, tot3 = blr::smem_layout(g3.p).total;
+    const uint32_t dyn = std::max(std::max(tot1, tot3), sl.total) + SMEM_SLACK;
+    if (dyn + PIPE_STATIC_SMEM > static_cast<uint32_t>(SMEM_LIMIT)) {
+        if (plan_print) fprintf(stderr, "[blr plan] pipe: %u B of smem, three launches\n", dyn);
+        return BLR_ERR_UNSUPPORTED;
+    }
+    unsigned int* ctr = static_cast<unsigned int*>(ctr_mem);
+    auto prep = [&](KParams& p) {
+        p.trace = nullptr;
+        p.first = 1;  // every role waits for the previous grid before loading anything
+        p.no_trigger = 1;
+        p.mma_burst = 1;
+        p.fast_prod = 1;
+        p.dbg = 0;
+    };
+    KParams p1 = g1.p, p3 = g3.p;
+    prep(p1);
+    prep(p3);
+    p1.pipe_sig = ctr + 1;
+    p3.pipe_wait = ctr + 1 + tiles_pad;
+    p3.pipe_target = static_cast<unsigned int>(r / 8);
+    blr::PipeArgs pa = {};
+    pa.ctr = ctr;
+    pa.Z = zl;
+    pa.Zpp = static_cast<__nv_bfloat16*>(zpp);
+    pa.S = static_cast<const __nv_bfloat16*>(S);
+    pa.n_tok = static_cast<int>(n_tok);
+    pa.b1 = static_cast<int>(b1);
+    pa.b2 = static_cast<int>(b2);
+    pa.r = static_cast<int>(r);
+    pa.z_target = static_cast<unsigned int>(b1 * p1.tiles_n * 2);
+    pa.tiles_pad = tiles_pad;
+    const int units = d.sm_count / 2;
+    const double f1 = 2.0 * n_tok * d_in * r, f3 = 2.0 * n_tok * r * qdim * b2;
+    pipe_split(units, f1, f3, 2.0 * n_tok * r * (b1 + b2), pa.n1, pa.n2, pa.n3);
+    (void)tiles;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        if (!g_attr_set[22][dev]) {
+            if (const cudaError_t ae = cudaFuncSetAttribute(blr::blast_pipe_kernel,
+                                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                            SMEM_LIMIT);
+                ae != cudaSuccess) {
+                if (plan_print) fprintf(stderr, "[blr plan] pipe attribute: %s\n", cudaGetErrorString(ae));
+                return BLR_ERR_CUDA;
+            }
+            g_attr_set[22][dev] = true;
+        }
+    }
+    if (const char* pe = getenv("BLR_PLAN"); pe && pe[0] == '1')
+        fprintf(stderr,
+                "[blr plan] pipe clusters S1/S2/S3 = %d/%d/%d  S1 BN=%d stages=%d  S3 BN=%d stages=%d  dyn smem=%u\n",
+                pa.n1, pa.n2, pa.n3, p1.BN, p1.stages, p3.BN, p3.stages, dyn);
+    if (const cudaError_t me = cudaMemsetAsync(ctr, 0, pipe_ctr_bytes(n_tok), st); me != cudaSuccess) {
+        if (plan_print) fprintf(stderr, "[blr plan] pipe memset: %s\n", cudaGetErrorString(me));
+        return BLR_ERR_CUDA;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * (pa.n1 + pa.n2 + pa.n3)));
+    cfg.blockDim = dim3(blr::NUM_THREADS);
+    pa.ticket_off = dyn;
+    cfg.dynamicSmemBytes = dyn + PIPE_STATIC_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
+    if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
+    if (const cudaError_t le = cudaLaunchKernelEx(&cfg, blr::blast_pipe_kernel, g1.ta, g1.tb, g1.tc, tmz, tmzpp, g3.ta,
+                                                  g3.tb, g3.tc, p1, p3, pa);
+        le != cudaSuccess) {
+        if (plan_print) fprintf(stderr, "[blr plan] pipe launch: %s\n", cudaGetErrorString(le));
+        return BLR_ERR_CUDA;
+    }
+    if (prof) {
+        if (prof_record(t_prof_events[2 * t_prof_n + 1], st) != cudaSuccess) return BLR_ERR_CUDA;
+        ++t_prof_n;
+    }
+    ++t_last_launches;
+    return BLR_OK;
+}
+
 blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2, int64_t r,
                       const void* V, const void* S, const void* U, void* Y, void* workspace, size_t ws_bytes,
                       blr_stream_t stream, bool fp8z) {
@@ -1577,6 +1738,11 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             return BLR_OK;
         };
         (void)items;
+        if (!z8 && pipe_wanted(n_tok, b1, b2, r)) {
+            s = blast_pipe(d, dev, st, X, d_in, pdim, n_tok, b1, b2, r, V, S, U, Y, qdim, zl, zpp,
+                           static_cast<char*>(zl) + static_cast<size_t>(b1) * n_pad * r * 2, tmz, tmzpp);
+            if (s != BLR_ERR_UNSUPPORTED) return s;  // (unsupported: nothing was enqueued; three launches)
+        }
         s = gemm_run(g1, d, dev, st);
         if (s != BLR_OK) return s;
         s = run_s2(0, n_tok, tmz);

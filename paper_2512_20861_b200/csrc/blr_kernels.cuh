@@ -185,11 +185,11 @@ __device__ __forceinline__ TileCoord tile_coord(const KParams& p, int tile) {
 struct TileIter {
     int unit, units, slices;
 };
-__device__ __forceinline__ TileIter tile_iter(const KParams& p, int pair) {
+__device__ __forceinline__ TileIter tile_iter(const KParams& p, int pair, int vblock, int vgrid) {
     TileIter t;
     const int csz = pair * (p.mc > 1 ? p.mc : 1);  // CTAs per unit (cluster)
-    t.unit = blockIdx.x / csz;
-    t.units = gridDim.x / csz;
+    t.unit = vblock / csz;
+    t.units = vgrid / csz;
     t.slices = p.groups * p.tiles_n;
     return t;
 }
@@ -285,13 +285,12 @@ __device__ __forceinline__ void stage_row8(uint32_t buf, int row, int chunk, uin
 // issues the MMAs; commits are multicast to both CTAs; each CTA drains its own TMEM rows.
 // OUTF (GEMM kind only): output 0 = bf16, 1 = fp16, 2 = fp16 tile-blocked [g][T][N/8][128][8],
 // 3 = e4m3 tile-blocked [g][T][N/8][128][8] (1-KB panels; the FP8 BLAST intermediate, row f4).
+// The kernel body, callable from any kernel whose dynamic smem (1024-B aligned `smem`) holds
+// smem_layout(p): blr_gemm_kernel below, and the S1 / S3 roles of the pipelined BLAST layer
+// (blast_pipe_kernel), which run it with a virtual block index / grid size.
 template <int KIND, int PAIR, int OUTF = 0>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
-    blr_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmC, const KParams p) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    // 1024-B alignment for the 128-B swizzle atoms.
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+__device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
+                                          const KParams& p, uint8_t* smem, int vblock, int vgrid) {
     const SmemLayout L = smem_layout(p);
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t a_base = sbase + L.a_off;
@@ -317,7 +316,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int mcs = (PAIR == 2 && p.mc > 1) ? p.mc : 1;
     const uint32_t lead_rank = cl_rank & ~1u;
     const bool leader = crank == 0;
-    unsigned long long* trace = p.trace ? p.trace + blockIdx.x * 128 : nullptr;
+    unsigned long long* trace = p.trace ? p.trace + vblock * 128 : nullptr;
     // trace stamps: [0] %globaltimer at entry, [8] %clock64 at entry; every other stamp is a
     // %clock64 value (cheap; converted on the host with the SM clock)
     if (trace && threadIdx.x == 0) {
@@ -352,7 +351,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         else ptx::tmem_alloc<TMEM_COLS>(ptx::smem_u32(tmem_slot));
         if (trace && lane == 0 && KIND != KIND_BLAST_PROJ) trace[14] = clock64();
     }
-    const TileIter titer = tile_iter(p, PAIR);
+    const TileIter titer = tile_iter(p, PAIR, vblock, vgrid);
     const int ntiles = tile_count(p, titer);
     const uint32_t tile_tab = sbase + L.tab_off;  // explicit shared-window addressing (see s_tile)
     for (int e = threadIdx.x; e < ntiles && e < TILE_TAB; e += NUM_THREADS)
@@ -377,7 +376,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // The FIRST launch of a call (p.first) may follow a caller kernel that wrote the weights: it
     // waits before loading anything and lets the next grid start only after that wait, so by the
     // time any later launch of the call starts, all work enqueued before the call has completed.
-    if (!p.first) ptx::griddep_launch_dependents();
+    if (!p.first && !p.no_trigger) ptx::griddep_launch_dependents();
 
     if (warp == 0) {
         // ===================================================== TMA producer =================
@@ -404,7 +403,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int kbr = BLR_DBG_ON(p, 64) ? 0 : kb_resident(p);  // dbg 64: no weight loads
             if (p.first) {
                 ptx::griddep_wait();
-                ptx::griddep_launch_dependents();
+                if (!p.no_trigger) ptx::griddep_launch_dependents();
             }
             int stage = 0;
             uint32_t phase = 0;
@@ -464,7 +463,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             ptx::griddep_wait();
                             waited = true;
                         }
-                        if (p.pipe_wait != nullptr && t128 > pipe_ok) {
+                        if (p.pipe_wait != nullptr && t128 > pipe_ok && t128 < a_tiles) {
                             ptx::pipe_acquire(p.pipe_wait + t128, p.pipe_target);  // A's token tile is ready
                             pipe_ok = t128;
                         }
@@ -795,11 +794,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         uint32_t acc_phase = 0;
         uint32_t nstore = 0;  // staged chunks written by this warp (buffer rotation)
         ptx::griddep_wait();  // our stores must not overtake the previous kernel's reads
+        // pipelined layer (tile-blocked output): the chunk-store issuer of each column half signals
+        // a token tile's ready counter once its stores have landed, two tiles later (bulk groups of
+        // the newer tile may still be in flight; their count bounds the wait)
+        const bool sig_iss = OUTF >= 2 && p.pipe_sig != nullptr && (ew & 3) == 0 && lane == 0;
+        int sig_t[2] = {-1, -1};  // token tiles of the two previous tiles (oldest first)
+        int sig_g = 0;            // bulk groups the previous tile committed
+        auto sig_flush = [&](int keep_groups) {
+            switch (keep_groups) {
+                case 0: ptx::bulk_wait<0>(); break;
+                case 1: ptx::bulk_wait<1>(); break;
+                case 2: ptx::bulk_wait<2>(); break;
+                case 3: ptx::bulk_wait<3>(); break;
+                default: ptx::bulk_wait<0>(); break;
+            }
+        };
         for (int it = 0; !BLR_DBG_ON(p, 32) && it < ntiles; ++it) {
             const TileCoord tc = tile_get(p, titer, tile_tab, it);
             const int m0 = ((tc.m_blk * mcs + static_cast<int>(pidx)) * PAIR + static_cast<int>(crank)) * BM;
             const int row0 = m0 + quarter * 32;
             const int n0 = tc.n_blk * p.BN;
+            if (sig_iss) {
+                if (sig_t[0] >= 0) {  // the tile before last: all its groups are older than sig_g
+                    sig_flush(sig_g);
+                    ptx::pipe_release(p.pipe_sig + sig_t[0]);
+                }
+                sig_t[0] = sig_t[1];
+                sig_t[1] = m0 / BM;
+                sig_g = 0;
+            }
             if constexpr (KIND == KIND_BLAST_PROJ) {
                 // stage S[l][k][n0 : n0+BN] (fp32) for the S-weighted block sum
                 ptx::named_bar_sync(1, 32 * NUM_EPI_WARPS);
@@ -964,6 +987,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             const int cc = (n0 + c0) >> 3;
                             ptx::tma_store_4d(&tmC, hbuf, 0, 0, cc, tc.g * p.o_tiles + m0 / BM);
                             ptx::bulk_commit();
+                            ++sig_g;
                         }
                         continue;
                     }
@@ -1010,6 +1034,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             const int cc = (n0 + c0) >> 3;
                             ptx::tma_store_4d(&tmC, hbuf, 0, 0, cc, tc.g * p.o_tiles + m0 / BM);
                             ptx::bulk_commit();
+                            ++sig_g;
                         }
                         continue;
                     }
@@ -1075,6 +1100,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
         }
         if (trace && ew == 0 && lane == 0) trace[5] = clock64();
+        if (sig_iss) {  // the last two tiles
+            ptx::bulk_wait<0>();
+            for (int j = 0; j < 2; ++j)
+                if (sig_t[j] >= 0) ptx::pipe_release(p.pipe_sig + sig_t[j]);
+        }
         // only the staging smem must outlive the stores: wait for their smem reads, not for the
         // global writes (those complete with the grid, before any dependent grid proceeds)
         if (lane == 0) ptx::bulk_wait_read<0>();
@@ -1091,6 +1121,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if constexpr (PAIR == 2) ptx::tmem_dealloc_pair<TMEM_COLS>(tmem_base);
         else ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
     }
+}
+
+template <int KIND, int PAIR, int OUTF = 0>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    blr_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmC, const KParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment for the 128-B swizzle atoms.
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    gemm_body<KIND, PAIR, OUTF>(tmA, tmB, tmC, p, smem, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
 }
 
 // ------------------------------------------------------------------------- BLAST S2 kernel -----
@@ -1299,15 +1339,21 @@ __host__ __device__ inline S2MLayout s2m_layout(int b1, int b2, bool fp8 = false
 // two CTAs per SM, which is what the short, latency-bound S2 of small layers needs; 16: b = 16).
 // FP8: Z is e4m3; the widening to fp16 is exact, the MMA and everything after
 // it are unchanged.
+// Pipelined-layer hooks of the S2 body (blast_pipe_kernel): items are dealt round robin over the
+// token-tile-major item list, each item waits for its token tile of Z and signals its token tile
+// of Z'' once its stores have landed.
+constexpr int S2_SIG_LAG = 8;
+struct S2Pipe {
+    const unsigned int* wait_ctr;  // Z token tile T ready once wait_ctr[T] >= wait_target
+    unsigned int wait_target;
+    unsigned int* sig_ctr;         // += 1 per item (T, c) once its Z'' panels are stored
+};
+
 template <int MAXB2, bool FP8 = false>
-__global__ void __launch_bounds__(s2m_threads<FP8>(), MAXB2 <= 8 ? 2 : 1)
-    blast_s2_mma_kernel(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmZpp,
-                        const void* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
-                        const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order,
-                        int t0 = 0, int t0o = 0) {
-    // t0 / t0o: first 128-token tile of Z this launch reads / of Z'' it writes (token-chunked
-    // S1 -> S2, DESIGN.md §5.3); the items' tiles are numbered from 0
-    extern __shared__ __align__(1024) uint8_t s2m_smem[];
+__device__ __forceinline__ void s2_body(const CUtensorMap& tmZ, const CUtensorMap& tmZpp, const void* __restrict__ Z,
+                                        __nv_bfloat16* __restrict__ Zpp, const __nv_bfloat16* __restrict__ S,
+                                        int n_tok, int b1, int b2, int r, int order, int t0, int t0o,
+                                        uint8_t* s2m_smem, int vblock, int vgrid, const S2Pipe* pipe) {
     const S2MLayout L = s2m_layout(b1, b2, FP8);
     const int nst = static_cast<int>(L.stages);
     const int b1p = (b1 + 1) & ~1;
@@ -1326,11 +1372,13 @@ __global__ void __launch_bounds__(s2m_threads<FP8>(), MAXB2 <= 8 ? 2 : 1)
     // each CTA walks one contiguous run of the chunk-major item list: its reads of every Z panel
     // (l, c) and writes of every Z'' panel (k, c) are sequential streams, and B_c changes only
     // when the run crosses a chunk (at most ~2 rebuilds per CTA)
-    const int it0 = static_cast<int>(static_cast<long long>(blockIdx.x) * total / gridDim.x);
-    const int cnt = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * total / gridDim.x) - it0;
-    const bool tile_major = order != 0;
+    const bool rr = pipe != nullptr;  // round robin over the tile-major list (pipelined layer)
+    const int it0 = rr ? vblock : static_cast<int>(static_cast<long long>(vblock) * total / vgrid);
+    const int cnt = rr ? (vblock < total ? (total - vblock + vgrid - 1) / vgrid : 0)
+                       : static_cast<int>(static_cast<long long>(vblock + 1) * total / vgrid) - it0;
+    const bool tile_major = order != 0 || rr;
     auto item = [&](int j, int& T, int& c) {
-        const int i = it0 + j;
+        const int i = rr ? it0 + j * vgrid : it0 + j;
         if (tile_major) {  // panels (l, T, c), c = 0.. adjacent: sequential streams
             T = i / nchunks;
             c = i - T * nchunks;
@@ -1374,16 +1422,21 @@ __global__ void __launch_bounds__(s2m_threads<FP8>(), MAXB2 <= 8 ? 2 : 1)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(s2m_smem + L.tslot);
-    ptx::griddep_launch_dependents();  // the S3 launch may start its prologue as SMs free up
+    if (!rr) ptx::griddep_launch_dependents();  // the S3 launch may start its prologue as SMs free up
 
     if (warp == 0) {  // ---------------------------------------------------------- TMA producer
         ptx::griddep_wait();  // Z is the previous kernel's output
         if (ptx::elect_one()) {
+            int ok_t = -1;  // highest token tile of Z known ready (pipelined layer)
             for (int j = 0; j < cnt; ++j) {
                 int T, c;
                 item(j, T, c);
                 const int s = j % nst;
                 if (j >= nst) ptx::mbar_wait(a_empty + 8 * s, ((j / nst) - 1) & 1);
+                if (rr && T > ok_t) {
+                    ptx::pipe_acquire(pipe->wait_ctr + T + t0, pipe->wait_target);
+                    ok_t = T;
+                }
                 ptx::mbar_arrive_expect_tx(a_full + 8 * s, static_cast<uint32_t>(b1 * (FP8 ? 1024 : 2048)));
                 // the b1 panels (l, T, c) in ONE tensor copy: Z viewed (64, 16, tiles*r/8, b1),
                 // box (64, 16, 1, b1) -> smem [l][2 KB] (fp8: 1-KB panels, 64-B rows)
@@ -1417,7 +1470,7 @@ __global__ void __launch_bounds__(s2m_threads<FP8>(), MAXB2 <= 8 ? 2 : 1)
             }
             __syncwarp();
         }
-    } else if (warp < 4 || warp >= 8) {  // --- B_c builders (warps 2-3); FP8: Z widening (+ warps 8-11)
+    } else if (warp < 4 || (FP8 && warp >= 8)) {  // --- B_c builders (warps 2-3); FP8: Z widening (+ warps 8-11)
         const bool builder = warp < 4;
         const int tb = builder ? threadIdx.x - 64 : 64 + (threadIdx.x - 256);  // converter index
         const uint32_t sbo = static_cast<uint32_t>(b1p) * 128;
@@ -1468,10 +1521,15 @@ __global__ void __launch_bounds__(s2m_threads<FP8>(), MAXB2 <= 8 ? 2 : 1)
                 ptx::mbar_arrive(w_full + 8 * wb);
             }
         }
-    } else {  // --------------------------------------------------------- epilogue (warps 4-7)
+    } else if (warp < 8) {  // ------------------------------------------------ epilogue (warps 4-7)
         const int q = warp & 3;  // TMEM lane quarter
         const int row = q * 32 + lane;
         const bool issuer = (warp == 4 && lane == 0);
+        // pipelined layer: token tiles of the last S2_SIG_LAG items (a store's completion is
+        // awaited S2_SIG_LAG items later, so the issuer never waits out a store's full latency)
+        int sig_t[S2_SIG_LAG];
+#pragma unroll
+        for (int e = 0; e < S2_SIG_LAG; ++e) sig_t[e] = -1;
         ptx::griddep_wait();  // Z'' may still be read by the previous kernel
         for (int j = 0; j < cnt; ++j) {
             int T, c;
@@ -1509,9 +1567,22 @@ __global__ void __launch_bounds__(s2m_threads<FP8>(), MAXB2 <= 8 ? 2 : 1)
                 // panels (k, T, c) for all k in ONE tensor store (Z'' viewed like Z)
                 ptx::tma_store_4d(&tmZpp, base + L.c + cb * L.c_bytes, 0, 0, (T + t0o) * nchunks + c, 0);
                 ptx::bulk_commit();
+                if (rr) {  // item j - S2_SIG_LAG's stores have landed: signal its token tile
+                    ptx::bulk_wait<S2_SIG_LAG>();
+                    if (sig_t[0] >= 0) ptx::pipe_release(pipe->sig_ctr + sig_t[0]);
+#pragma unroll
+                    for (int e = 0; e + 1 < S2_SIG_LAG; ++e) sig_t[e] = sig_t[e + 1];
+                    sig_t[S2_SIG_LAG - 1] = T + t0o;
+                }
             }
         }
-        if (issuer) ptx::bulk_wait<0>();
+        if (issuer) {
+            ptx::bulk_wait<0>();
+            if (rr)
+#pragma unroll
+                for (int e = 0; e < S2_SIG_LAG; ++e)
+                    if (sig_t[e] >= 0) ptx::pipe_release(pipe->sig_ctr + sig_t[e]);
+        }
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -1520,6 +1591,86 @@ __global__ void __launch_bounds__(s2m_threads<FP8>(), MAXB2 <= 8 ? 2 : 1)
         ptx::tmem_dealloc<256>(tmem);
     }
     (void)Z;
+}
+
+template <int MAXB2, bool FP8 = false>
+__global__ void __launch_bounds__(s2m_threads<FP8>(), MAXB2 <= 8 ? 2 : 1)
+    blast_s2_mma_kernel(const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmZpp,
+                        const void* __restrict__ Z, __nv_bfloat16* __restrict__ Zpp,
+                        const __nv_bfloat16* __restrict__ S, int n_tok, int b1, int b2, int r, int order,
+                        int t0 = 0, int t0o = 0) {
+    // t0 / t0o: first 128-token tile of Z this launch reads / of Z'' it writes (token-chunked
+    // S1 -> S2, DESIGN.md §5.3); the items' tiles are numbered from 0
+    extern __shared__ __align__(1024) uint8_t s2m_smem[];
+    s2_body<MAXB2, FP8>(tmZ, tmZpp, Z, Zpp, S, n_tok, b1, b2, r, order, t0, t0o, s2m_smem,
+                        static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x), nullptr);
+}
+
+}  // namespace blr
+
+namespace blr {
+
+// ------------------------------------------------------------ pipelined BLAST layer (one launch) ----
+// Y = BLAST(X) as ONE persistent launch whose CTA pairs take one of three roles:
+//   S1  Z_l = X_l V_l            gemm_body<GEMM, 2, 2>  tile-blocked fp16 Z
+//   S2  Z''_k = sum_l S_lk Z_l    s2_body<16>            tile-blocked bf16 Z''     (Fig. 6)
+//   S3  Y_k = Z''_k U_k           gemm_body<GEMM, 2, 0>  Y
+// All three walk the tokens in 128-row-tile order and hand each token tile to the next stage
+// through per-tile ready counters in global memory (release/acquire, ptx::pipe_*), so a token
+// tile's Z and Z'' are consumed while they are still in the 126-MB L2 -- the round trip through
+// HBM the paper identifies (Table 2) becomes L2 traffic -- and S2's memory-bound
+// work overlaps S1's and S3's tensor-core work instead of running between them.
+// Roles are handed out by arrival order (an atomic ticket per cluster), S1 first, then S2, then
+// S3: every wait is on work held by an earlier ticket, i.e. by a CTA that is already resident, so
+// the launch cannot deadlock however many of its CTAs are co-resident.  The grid never triggers
+// its dependent launch early (a dependent's CTAs could otherwise take the SMs later tickets need).
+struct PipeArgs {
+    unsigned int* ctr;   // [0] ticket, [1 .. tiles] Z ready, [1 + tiles .. 2 tiles] Z'' ready
+    int n1, n2, n3;      // clusters (CTA pairs) per role
+    const void* Z;       // S2 operands
+    __nv_bfloat16* Zpp;
+    const __nv_bfloat16* S;
+    int n_tok, b1, b2, r;
+    unsigned int z_target;  // S1 signals per token tile (b1 x N tiles x 2 column halves)
+    int tiles_pad;          // counters per stage (128-token tiles of the pairs' 256-row tiles)
+    uint32_t ticket_off;    // dynamic-smem byte offset of the role ticket
+};
+
+constexpr uint32_t PIPE_SMEM_ALIGN = 1024;
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    blast_pipe_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmV,
+                      const __grid_constant__ CUtensorMap tmZst, const __grid_constant__ CUtensorMap tmZ,
+                      const __grid_constant__ CUtensorMap tmZpp, const __grid_constant__ CUtensorMap tmA3,
+                      const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmY,
+                      const KParams p1, const KParams p3, const PipeArgs pa) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + (PIPE_SMEM_ALIGN - 1)) &
+                                               ~uintptr_t(PIPE_SMEM_ALIGN - 1));
+    // the role ticket lives past every role's layout (no static smem: it would cost 1-2 KB)
+    volatile uint32_t* s_ticket = reinterpret_cast<volatile uint32_t*>(smem_raw + pa.ticket_off);
+    const uint32_t crank = ptx::cluster_ctarank();
+    if (crank == 0 && threadIdx.x == 0) {
+        const uint32_t t = atomicAdd(pa.ctr, 1u);
+        *s_ticket = t;
+        ptx::st_cluster_u32(ptx::smem_u32(smem_raw + pa.ticket_off), 1u, t);  // the peer CTA's copy
+    }
+    ptx::cluster_sync();
+    const int ticket = static_cast<int>(*s_ticket);
+    if (ticket < pa.n1) {
+        gemm_body<KIND_GEMM, 2, 2>(tmX, tmV, tmZst, p1, smem, 2 * ticket + static_cast<int>(crank), 2 * pa.n1);
+    } else if (ticket < pa.n1 + pa.n2) {
+        S2Pipe sp;
+        sp.wait_ctr = pa.ctr + 1;
+        sp.wait_target = pa.z_target;
+        sp.sig_ctr = pa.ctr + 1 + pa.tiles_pad;
+        // (320 threads: warps 8-9 of the S2 role only join its barriers)
+        s2_body<16, false>(tmZ, tmZpp, pa.Z, pa.Zpp, pa.S, pa.n_tok, pa.b1, pa.b2, pa.r, 1, 0, 0, smem,
+                           2 * (ticket - pa.n1) + static_cast<int>(crank), 2 * pa.n2, &sp);
+    } else {
+        gemm_body<KIND_GEMM, 2, 0>(tmA3, tmU, tmY, p3, smem, 2 * (ticket - pa.n1 - pa.n2) + static_cast<int>(crank),
+                                   2 * pa.n3);
+    }
 }
 
 }  // namespace blr

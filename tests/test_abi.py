@@ -49,8 +49,9 @@ def test_workspace_sizes():
     assert lib.blr_monarch_workspace_size(n, 64, 64, 4, 2, 32) == 2 * n * 4 * 32 * 2
     # BLAST with b1*r <= 512 fuses S1+S2 (only Z''); larger b1*r also keeps the S1 output Z_l
     assert lib.blr_blast_workspace_size(n, 64, 64, 2, 2, 192) == 2 * n * 192 * 2
-    # split path: Z'' and fp16 Z (R13), token rows padded to whole 128-row tiles (tile-blocked, §5.4)
-    assert lib.blr_blast_workspace_size(n, 64, 64, 4, 2, 192) == 2 * 5120 * 192 * 2 + 4 * 5120 * 192 * 2
+    # split path: Z'' and fp16 Z (R13), token rows padded to whole 128-row tiles (tile-blocked, §5.4),
+    # then the pipelined layer's counters (ticket + 2 x 40 token tiles of 4 B, rounded up to 256 B)
+    assert lib.blr_blast_workspace_size(n, 64, 64, 4, 2, 192) == 2 * 5120 * 192 * 2 + 4 * 5120 * 192 * 2 + 512
     # shorter contractions keep a compensated hi|lo pair: twice the bytes
     assert lib.blr_lowrank_workspace_size(n, 64, 64, 16) == 2 * n * 16 * 2
     assert lib.blr_monarch_workspace_size(n, 64, 64, 4, 2, 8) == 2 * 2 * n * 4 * 8 * 2
