@@ -1476,6 +1476,8 @@ blr_status blast_pipe(const DevInfo& d, int dev, cudaStream_t st, const void* X,
     pa.r = static_cast<int>(r);
     pa.z_target = static_cast<unsigned int>(b1 * p1.tiles_n * 2);
     pa.tiles_pad = tiles_pad;
+    pa.win = blr::S2_PIPE_WIN;
+    if (const char* we = getenv("BLR_PIPE_WIN")) pa.win = std::max(1, atoi(we));
     const int units = d.sm_count / 2;
     const double f1 = 2.0 * n_tok * d_in * r, f3 = 2.0 * n_tok * r * qdim * b2;
     pipe_split(units, f1, f3, 2.0 * n_tok * r * (b1 + b2), pa.n1, pa.n2, pa.n3);

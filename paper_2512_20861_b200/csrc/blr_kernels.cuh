@@ -983,7 +983,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         }
                         ptx::fence_async_smem();
                         ptx::named_bar_sync(2 + half, 128);
-                        if (iss && !BLR_DBG_ON(p, 1)) {
+                        // (a CTA pair's second tile past n_tok has no tile of its own in the
+                        //  layout: its box would land on the next group's first tile)
+                        if (iss && !BLR_DBG_ON(p, 1) && m0 < p.n_tok) {
                             const int cc = (n0 + c0) >> 3;
                             ptx::tma_store_4d(&tmC, hbuf, 0, 0, cc, tc.g * p.o_tiles + m0 / BM);
                             ptx::bulk_commit();
@@ -1028,9 +1030,11 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         }
                         ptx::fence_async_smem();
                         ptx::named_bar_sync(2 + half, 128);
-                        if (iss && !BLR_DBG_ON(p, 1)) {
+                        if (iss && !BLR_DBG_ON(p, 1) && m0 < p.n_tok) {
                             // tile-blocked [g][T][N/8][128][8]: this chunk's panels of tile T are
-                            // contiguous -> one bulk copy (rows >= n_tok are zeros: A was OOB-filled)
+                            // contiguous -> one bulk copy (rows >= n_tok are zeros: A was OOB-filled;
+                            // a pair's second tile past n_tok is skipped: it would alias the next
+                            // group's first tile)
                             const int cc = (n0 + c0) >> 3;
                             ptx::tma_store_4d(&tmC, hbuf, 0, 0, cc, tc.g * p.o_tiles + m0 / BM);
                             ptx::bulk_commit();
@@ -1343,10 +1347,12 @@ __host__ __device__ inline S2MLayout s2m_layout(int b1, int b2, bool fp8 = false
 // token-tile-major item list, each item waits for its token tile of Z and signals its token tile
 // of Z'' once its stores have landed.
 constexpr int S2_SIG_LAG = 8;
+constexpr int S2_PIPE_WIN = 8;  // default token tiles per window of the pipelined S2 role
 struct S2Pipe {
     const unsigned int* wait_ctr;  // Z token tile T ready once wait_ctr[T] >= wait_target
     unsigned int wait_target;
     unsigned int* sig_ctr;         // += 1 per item (T, c) once its Z'' panels are stored
+    int win;                       // token tiles per window
 };
 
 template <int MAXB2, bool FP8 = false>
@@ -1372,13 +1378,28 @@ __device__ __forceinline__ void s2_body(const CUtensorMap& tmZ, const CUtensorMa
     // each CTA walks one contiguous run of the chunk-major item list: its reads of every Z panel
     // (l, c) and writes of every Z'' panel (k, c) are sequential streams, and B_c changes only
     // when the run crosses a chunk (at most ~2 rebuilds per CTA)
-    const bool rr = pipe != nullptr;  // round robin over the tile-major list (pipelined layer)
-    const int it0 = rr ? vblock : static_cast<int>(static_cast<long long>(vblock) * total / vgrid);
-    const int cnt = rr ? (vblock < total ? (total - vblock + vgrid - 1) / vgrid : 0)
-                       : static_cast<int>(static_cast<long long>(vblock + 1) * total / vgrid) - it0;
-    const bool tile_major = order != 0 || rr;
+    // Pipelined layer: the token tiles are walked in windows of S2_PIPE_WIN; this CTA owns the
+    // chunks c = vblock, vblock + vgrid, ... and, per window, runs each of its chunks over the
+    // window's token tiles (token tile fastest), so B_c is rebuilt once per window and chunk
+    // (a per-item rebuild, with its global loads of S, bounded the role at ~20 GB/s per SM).
+    const bool rr = pipe != nullptr;
+    const int win = rr ? pipe->win : 1;
+    const int nc_u = rr ? (vblock < nchunks ? (nchunks - vblock + vgrid - 1) / vgrid : 0) : 0;
+    const int it0 = rr ? 0 : static_cast<int>(static_cast<long long>(vblock) * total / vgrid);
+    const int cnt = rr ? nc_u * tiles : static_cast<int>(static_cast<long long>(vblock + 1) * total / vgrid) - it0;
+    const bool tile_major = order != 0;
     auto item = [&](int j, int& T, int& c) {
-        const int i = rr ? it0 + j * vgrid : it0 + j;
+        if (rr) {
+            const int per_w = nc_u * win;
+            const int w = j / per_w;
+            const int rem = j - w * per_w;
+            const int wc = min(win, tiles - w * win);  // the last window may be short
+            const int ci = rem / wc;
+            T = w * win + (rem - ci * wc);
+            c = vblock + ci * vgrid;
+            return;
+        }
+        const int i = it0 + j;
         if (tile_major) {  // panels (l, T, c), c = 0.. adjacent: sequential streams
             T = i / nchunks;
             c = i - T * nchunks;
@@ -1433,9 +1454,10 @@ __device__ __forceinline__ void s2_body(const CUtensorMap& tmZ, const CUtensorMa
                 item(j, T, c);
                 const int s = j % nst;
                 if (j >= nst) ptx::mbar_wait(a_empty + 8 * s, ((j / nst) - 1) & 1);
-                if (rr && T > ok_t) {
-                    ptx::pipe_acquire(pipe->wait_ctr + T + t0, pipe->wait_target);
-                    ok_t = T;
+                if (rr && T > ok_t) {  // the whole window of token tiles this item opens
+                    const int w_end = min(tiles, (T / win + 1) * win);
+                    for (int t = ok_t + 1; t < w_end; ++t) ptx::pipe_acquire(pipe->wait_ctr + t + t0, pipe->wait_target);
+                    ok_t = w_end - 1;
                 }
                 ptx::mbar_arrive_expect_tx(a_full + 8 * s, static_cast<uint32_t>(b1 * (FP8 ? 1024 : 2048)));
                 // the b1 panels (l, T, c) in ONE tensor copy: Z viewed (64, 16, tiles*r/8, b1),
@@ -1634,6 +1656,7 @@ struct PipeArgs {
     unsigned int z_target;  // S1 signals per token tile (b1 x N tiles x 2 column halves)
     int tiles_pad;          // counters per stage (128-token tiles of the pairs' 256-row tiles)
     uint32_t ticket_off;    // dynamic-smem byte offset of the role ticket
+    int win;                // S2 role: token tiles per window
 };
 
 constexpr uint32_t PIPE_SMEM_ALIGN = 1024;
@@ -1664,6 +1687,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sp.wait_ctr = pa.ctr + 1;
         sp.wait_target = pa.z_target;
         sp.sig_ctr = pa.ctr + 1 + pa.tiles_pad;
+        sp.win = pa.win;
         // (320 threads: warps 8-9 of the S2 role only join its barriers)
         s2_body<16, false>(tmZ, tmZpp, pa.Z, pa.Zpp, pa.S, pa.n_tok, pa.b1, pa.b2, pa.r, 1, 0, 0, smem,
                            2 * (ticket - pa.n1) + static_cast<int>(crank), 2 * pa.n2, &sp);

@@ -67,3 +67,20 @@ def test_pipe_nonfinite_row_stays_local(cuda_lib, monkeypatch):
     assert bad[300].item()
     bad[300] = False
     assert not bad.any()
+
+
+@pytest.mark.parametrize("n", [640, 1152, 1300])
+def test_pair_s1_odd_token_tiles(cuda_lib, monkeypatch, n):
+    """Split path with S1 as CTA pairs (256-row tiles) over an odd number of 128-token tiles: the
+    pair's second tile past n_tok must not store (its tile-blocked box would alias the next
+    group's first tile; found through the pipelined layer, where S1 always runs as pairs)."""
+    monkeypatch.setenv("BLR_BLAST_PATH", "split")
+    monkeypatch.setenv("BLR_PAIR", "2")
+    b1, b2, r, p, q = 16, 16, 208, 48, 40
+    X = synth.make_x(n, b1 * p, seed=14).to(DEV)
+    V, S, U = [t.to(DEV) for t in synth.blast_factors(b1 * p, b2 * q, b1, b2, r, seed=14)]
+    Y = cuda_lib.blast_matmul(X, V, S, U)
+    torch.cuda.synchronize()
+    rows = np.concatenate([np.arange(0, 128, 7), sample_rows(n, 40)])
+    ref = orc.blast_forward(to64(X[rows].cpu()), to64(V), to64(S), to64(U))
+    assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"pair S1 n={n}")
