@@ -173,8 +173,11 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) 
     const int cols = p.n_sub * p.BN;
     if (cols > blr::TMEM_COLS) return false;
     p.acc_bufs = (2 * cols <= blr::TMEM_COLS) ? 2 : 1;
-    const char* e = getenv("BLR_NO_RESIDENT");
-    const bool reuse = p.tiles_m >= 2 && p.n_sub == 1 && p.kb_half <= blr::MAX_BRES - 1 && !(e && e[0] == '1');
+    // weight-stationary plans are opt-in (BLR_RESIDENT=1): with the lean producer, streamed CTA-pair
+    // plans measured as fast or faster on every workload (C4 8.21 -> 7.61 ms, C3 0.93 -> 0.84 ms,
+    // C2 / C4M / C5V-256 unchanged; in-process A/B)
+    const char* e = getenv("BLR_RESIDENT");
+    const bool reuse = p.tiles_m >= 2 && p.n_sub == 1 && p.kb_half <= blr::MAX_BRES - 1 && e && e[0] == '1';
     const char* kb_env = getenv("BLR_KBOX");
     const char* sc_env = getenv("BLR_SCORE");
     const char* bufs_env = getenv("BLR_BUFS");
@@ -485,8 +488,10 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
                         bool no_res = false) {
     KParams& p = g.p;
     int pair = 1;
+    // CTA pairs by default from 256 tokens (BLR_PAIR=1: single CTAs, BLR_PAIR=0: the shape heuristic
+    // below, BLR_PAIR=2: pairs)
     const char* pe = getenv("BLR_PAIR");
-    const int force = force_pair ? force_pair : pe ? atoi(pe) : 0;
+    const int force = force_pair ? force_pair : pe ? atoi(pe) : 2;
     if (force == 2 && n_tok >= 256) {
         pair = 2;
     } else if (force != 1) {
@@ -833,7 +838,11 @@ void dtc_plan(DtcPrep& P, int64_t K, int64_t N, int64_t G, int a_f32, int kmaj, 
             if (kc > blr::DTC_MAX_KC || cdiv(K, kc) != S) continue;
             if (force_s && S != force_s) continue;
             const int epi = S > 1 ? 1 : 0;
-            for (int per_sm = min_per_sm; per_sm <= 3; ++per_sm) {
+            // cluster-split plans run one CTA per SM: with two co-resident CTAs per SM the first call
+            // of a process intermittently summed a stale 16-32-column slice of a peer's partial tile
+            // (Llama-7B n = 16 S3, W = 256, S = 6: 2 of ~10 fresh processes; 0 of 35 with one CTA
+            // per SM; root cause not isolated -- DESIGN.md §5.3b)
+            for (int per_sm = (S > 1 ? 1 : min_per_sm); per_sm <= (S > 1 ? 1 : 3); ++per_sm) {
                 int stages;
                 size_t smem;
                 if (!dtc_fit(static_cast<int>(kc), a_f32, 1, epi, w, bk, 0, per_sm, stages, smem)) continue;
@@ -1004,7 +1013,7 @@ blr_status dtc_prepare_blast_mix(DtcPrep& P, const void* X, int64_t d_in, int64_
             if (force_w && w != force_w) continue;
             const int bk = blr::dtc_bk(false, w);
             const int kc = static_cast<int>(rup(pdim, bk));
-            for (int per_sm = min_per_sm; per_sm <= 3; ++per_sm) {
+            for (int per_sm = 1; per_sm <= 1; ++per_sm) {  // cluster plan: one CTA per SM (see dtc_plan)
                 int stages;
                 size_t smem;
                 if (!dtc_fit(kc, 0, units, 2, w, bk, static_cast<int>(nk * b1 * w), per_sm, stages, smem)) continue;
@@ -1331,9 +1340,9 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
         KParams p;
         int pair = 1;
         const char* pe = getenv("BLR_PAIR");
-        const int force = pe ? atoi(pe) : 0;
-        // measured (Llama-7B): pairs win for a long block contraction (down S1, p = 688: 3.05 ->
-        // 2.57 ms) and lose for a short one (gate S1, p = 256: 1.33 -> 1.89 ms); BLR_PAIR forces
+        const int force = pe ? atoi(pe) : 2;  // pairs by default (see gemm_prepare)
+        // BLR_PAIR=0 heuristic (generic producer era): pairs won for a long block contraction (down
+        // S1, p = 688: 3.05 -> 2.57 ms) and lost for a short one (gate S1, p = 256: 1.33 -> 1.89 ms)
         if (force == 2 && n_tok >= 256) pair = 2;
         if (force == 0 && n_tok >= 1024 && pdim >= 512) pair = 2;
         if (!plan_mon(p, pair)) {

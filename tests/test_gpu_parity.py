@@ -233,12 +233,15 @@ def test_c5_vit_dit(cuda_lib, images):
 
 
 # ------------------------------------------------------------------------------ CTA-pair mode --
-@pytest.mark.parametrize("pair", ["1", "2"])
+@pytest.mark.parametrize("pair", ["1", "2", "0"])
+@pytest.mark.parametrize("resident", ["0", "1"])
 @pytest.mark.parametrize("method", ["lowrank", "monarch", "blast"])
-def test_forced_cta_pair_modes(cuda_lib, monkeypatch, pair, method):
-    """Both GEMM variants (one CTA, or a cta_group::2 pair with M=256 and B split across the pair)
-    on shapes with ragged token tails and multi-tile N, against the oracle."""
+def test_forced_cta_pair_modes(cuda_lib, monkeypatch, pair, resident, method):
+    """Both GEMM variants (one CTA, or a cta_group::2 pair with M=256 and B split across the pair;
+    BLR_PAIR=0 = the shape heuristic), streamed or weight-stationary (BLR_RESIDENT=1, opt-in), on
+    shapes with ragged token tails and multi-tile N, against the oracle."""
     monkeypatch.setenv("BLR_PAIR", pair)
+    monkeypatch.setenv("BLR_RESIDENT", resident)
     n = 1000
     if method == "lowrank":
         L = configs.Layer("t", "t", 1024, 1376, "lowrank", 160, 1)
