@@ -1473,6 +1473,17 @@ blr_status blast_pipe(const DevInfo& d, int dev, cudaStream_t st, const void* X,
     prep(p3);
     p1.pipe_sig = ctr + 1;
     p3.pipe_wait = ctr + 1 + tiles_pad;
+    // S1 stays at most `bp` token tiles ahead of S2 (Z still in L2 when S2 reads it; BLR_PIPE_BP=0: off).
+    // Safe because every CTA of the grid is co-resident (grid <= SMs, one CTA per SM, no early trigger).
+    // (bp >= the S2 window: a smaller distance would make S1's last tiles of a window wait for S2
+    //  items of that same window, which S2 starts only once the whole window is ready -- a cycle)
+    int bp = 2 * blr::S2_PIPE_WIN;
+    if (const char* be = getenv("BLR_PIPE_BP")) bp = atoi(be);
+    if (bp > 0) {
+        p1.pipe_bp = ctr + 1 + tiles_pad;
+        p1.pipe_bp_target = static_cast<unsigned int>(r / 8);
+        p1.pipe_bp_dist = bp;
+    }
     p3.pipe_target = static_cast<unsigned int>(r / 8);
     blr::PipeArgs pa = {};
     pa.ctr = ctr;
@@ -1487,6 +1498,11 @@ blr_status blast_pipe(const DevInfo& d, int dev, cudaStream_t st, const void* X,
     pa.tiles_pad = tiles_pad;
     pa.win = blr::S2_PIPE_WIN;
     if (const char* we = getenv("BLR_PIPE_WIN")) pa.win = std::max(1, atoi(we));
+    if (p1.pipe_bp != nullptr) p1.pipe_bp_dist = std::max(p1.pipe_bp_dist, pa.win);
+#ifdef BLR_DEBUG_KNOBS
+    if (const char* de = getenv("BLR_PIPE_DBG")) pa.dbg = atoi(de);
+    if (pa.dbg & 4) p3.pipe_wait = nullptr;  // S3 does not wait (timing experiment; results wrong)
+#endif
     const int units = d.sm_count / 2;
     const double f1 = 2.0 * n_tok * d_in * r, f3 = 2.0 * n_tok * r * qdim * b2;
     pipe_split(units, f1, f3, 2.0 * n_tok * r * (b1 + b2), pa.n1, pa.n2, pa.n3);
@@ -1725,7 +1741,9 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
         auto run_s2 = [&](int64_t t0o, int64_t ntok, const CUtensorMap& mz) -> blr_status {  // t0o: Z'' tile offset
             const int64_t its = cdiv(ntok, 128) * (r / 8);
             cudaLaunchConfig_t cfg = {};
-            cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(its, static_cast<int64_t>(per_sm) * d.sm_count)));
+            int64_t s2_grid = std::min<int64_t>(its, static_cast<int64_t>(per_sm) * d.sm_count);
+            if (const char* ge = getenv("BLR_S2_GRID")) s2_grid = std::max<int64_t>(1, std::min<int64_t>(s2_grid, atoi(ge)));
+            cfg.gridDim = dim3(static_cast<unsigned>(s2_grid));  // (BLR_S2_GRID: per-CTA throughput experiments)
             cfg.blockDim = dim3(z8 ? blr::S2M_THREADS_FP8 : blr::S2M_THREADS);
             cfg.dynamicSmemBytes = sl8.total + 1024;
             cfg.stream = st;

@@ -116,6 +116,9 @@ struct KParams {
     const unsigned int* pipe_wait;  // A's token tile t is ready once pipe_wait[t] >= pipe_target (nullptr: off)
     unsigned int pipe_target;
     unsigned int* pipe_sig;         // the epilogue adds 1 per (tile, store issuer) once the tile's stores landed
+    const unsigned int* pipe_bp;    // back-pressure: token tile t starts once pipe_bp[t - pipe_bp_dist] >=
+    unsigned int pipe_bp_target;    //   pipe_bp_target (the consumer stage is that far behind; nullptr: off)
+    int pipe_bp_dist;
     int no_trigger;                 // 1: never trigger the dependent grid early (its CTAs could take the SMs
                                     //    this grid's later CTAs need while the earlier ones wait on them)
 };
@@ -412,6 +415,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             bool waited = p.first != 0;
             int nstep_tr = 0;
             int pipe_ok = -1;  // highest token tile of A known ready (pipelined layer)
+            int bp_ok = -1;    // highest token tile cleared by back-pressure
             bool fast_done = false;
             if constexpr (KIND == KIND_GEMM) {
                 if (mcs == 1 && trace == nullptr && p.fast_prod) {
@@ -462,6 +466,12 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         if (!waited) {
                             ptx::griddep_wait();
                             waited = true;
+                        }
+                        if (p.pipe_bp != nullptr && t128 >= p.pipe_bp_dist && t128 > bp_ok) {
+                            // keep this stage at most pipe_bp_dist token tiles ahead of its consumer,
+                            // so what it hands over is still in L2 when the consumer reads it
+                            ptx::pipe_acquire(p.pipe_bp + (t128 - p.pipe_bp_dist), p.pipe_bp_target);
+                            bp_ok = t128;
                         }
                         if (p.pipe_wait != nullptr && t128 > pipe_ok && t128 < a_tiles) {
                             ptx::pipe_acquire(p.pipe_wait + t128, p.pipe_target);  // A's token tile is ready
@@ -1095,6 +1105,19 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 }
             }
             if (trace && ew == 0 && lane == 0 && it < 24) trace[40 + it] = clock64();  // epilogue done
+            if (sig_iss) {
+                // the CTA's last tile of this token-tile row: flush the deferred signals (the producer
+                // may block on back-pressure before the next tile, which would otherwise hold them)
+                const bool row_end = it + 1 >= ntiles || tile_get(p, titer, tile_tab, it + 1).m_blk != tc.m_blk;
+                if (row_end) {
+                    ptx::bulk_wait<0>();
+                    for (int j = 0; j < 2; ++j)
+                        if (sig_t[j] >= 0) ptx::pipe_release(p.pipe_sig + sig_t[j]);
+                    sig_t[0] = -1;
+                    sig_t[1] = -1;
+                    sig_g = 0;
+                }
+            }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -1353,6 +1376,7 @@ struct S2Pipe {
     unsigned int wait_target;
     unsigned int* sig_ctr;         // += 1 per item (T, c) once its Z'' panels are stored
     int win;                       // token tiles per window
+    int dbg;                       // BLR_DEBUG_KNOBS builds: 1 no acquire waits, 2 no store-completion waits
 };
 
 template <int MAXB2, bool FP8 = false>
@@ -1456,6 +1480,9 @@ __device__ __forceinline__ void s2_body(const CUtensorMap& tmZ, const CUtensorMa
                 if (j >= nst) ptx::mbar_wait(a_empty + 8 * s, ((j / nst) - 1) & 1);
                 if (rr && T > ok_t) {  // the whole window of token tiles this item opens
                     const int w_end = min(tiles, (T / win + 1) * win);
+#ifdef BLR_DEBUG_KNOBS
+                    if (!(pipe->dbg & 1))
+#endif
                     for (int t = ok_t + 1; t < w_end; ++t) ptx::pipe_acquire(pipe->wait_ctr + t + t0, pipe->wait_target);
                     ok_t = w_end - 1;
                 }
@@ -1590,11 +1617,27 @@ __device__ __forceinline__ void s2_body(const CUtensorMap& tmZ, const CUtensorMa
                 ptx::tma_store_4d(&tmZpp, base + L.c + cb * L.c_bytes, 0, 0, (T + t0o) * nchunks + c, 0);
                 ptx::bulk_commit();
                 if (rr) {  // item j - S2_SIG_LAG's stores have landed: signal its token tile
+#ifdef BLR_DEBUG_KNOBS
+                    if (!(pipe->dbg & 2))
+#endif
                     ptx::bulk_wait<S2_SIG_LAG>();
                     if (sig_t[0] >= 0) ptx::pipe_release(pipe->sig_ctr + sig_t[0]);
 #pragma unroll
                     for (int e = 0; e + 1 < S2_SIG_LAG; ++e) sig_t[e] = sig_t[e + 1];
                     sig_t[S2_SIG_LAG - 1] = T + t0o;
+                    // last item of this CTA's share of a window: flush every pending signal (the
+                    // producer may next block on the following window, and with S1 back-pressure an
+                    // unreleased signal here would close a wait cycle)
+                    int Tn = -1, cn = 0;
+                    if (j + 1 < cnt) item(j + 1, Tn, cn);
+                    if (j + 1 >= cnt || Tn / win != T / win) {
+                        ptx::bulk_wait<0>();
+#pragma unroll
+                        for (int e = 0; e < S2_SIG_LAG; ++e) {
+                            if (sig_t[e] >= 0) ptx::pipe_release(pipe->sig_ctr + sig_t[e]);
+                            sig_t[e] = -1;
+                        }
+                    }
                 }
             }
         }
@@ -1657,6 +1700,7 @@ struct PipeArgs {
     int tiles_pad;          // counters per stage (128-token tiles of the pairs' 256-row tiles)
     uint32_t ticket_off;    // dynamic-smem byte offset of the role ticket
     int win;                // S2 role: token tiles per window
+    int dbg;                // BLR_DEBUG_KNOBS builds: S2Pipe::dbg
 };
 
 constexpr uint32_t PIPE_SMEM_ALIGN = 1024;
@@ -1688,6 +1732,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sp.wait_target = pa.z_target;
         sp.sig_ctr = pa.ctr + 1 + pa.tiles_pad;
         sp.win = pa.win;
+        sp.dbg = pa.dbg;
         // (320 threads: warps 8-9 of the S2 role only join its barriers)
         s2_body<16, false>(tmZ, tmZpp, pa.Z, pa.Zpp, pa.S, pa.n_tok, pa.b1, pa.b2, pa.r, 1, 0, 0, smem,
                            2 * (ticket - pa.n1) + static_cast<int>(crank), 2 * pa.n2, &sp);
