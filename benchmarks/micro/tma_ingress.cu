@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(128, 1) ingress(const __grid_constant__ CUtens
                 for (int c = 0; c < csize; ++c) {
                     uint32_t remote;
                     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(&empty[stage])), "r"(c));
-                    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+                    // default (CTA-scope release) semantics: the .release.cluster form compiles to a
+                    // MEMBAR.ALL.GPU per arrive, which is what made this mode look 7x slower in round 1
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
                 }
             } else {
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[stage])) : "memory");

@@ -418,7 +418,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             int bp_ok = -1;    // highest token tile cleared by back-pressure
             bool fast_done = false;
             if constexpr (KIND == KIND_GEMM) {
-                if (mcs == 1 && trace == nullptr && p.fast_prod) {
+                if (trace == nullptr && p.fast_prod) {
                     // Lean producer for the GEMM kind: every parameter the K loop needs is hoisted
                     // into registers and every per-tile coordinate computed once per tile, so a K
                     // block costs a barrier wait, an expect_tx and its TMA issues.  (The generic loop
@@ -439,9 +439,15 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     const int a_tiles = p.a_tiles;
                     const int ns = ptx::pin(n_steps);
                     const uint32_t tx_f = ptx::pin(tx);
+                    // B multicast across the mcs CTA pairs of a cluster (mcs > 1): this pair loads 1/mcs
+                    // of every B box (K rows for MN-major, N rows for K-major) for all of them
+                    uint16_t mc_mask = 0;
+                    for (int j2 = 0; j2 < mcs; ++j2) mc_mask |= static_cast<uint16_t>(1u << (2 * j2 + crank));
+                    const int mc_kr = BK / mcs;                              // MN-major: K rows per slice
+                    const int mc_nr = ptx::pin(BNf / n_mma / PAIR / mcs);    // K-major: N rows per slice
                     for (int it = 0; it < ntiles; ++it) {
                         const TileCoord tc = tile_get(p, titer, tile_tab, it);
-                        const int t128 = tc.m_blk * PAIR + static_cast<int>(crank);
+                        const int t128 = (tc.m_blk * mcs + static_cast<int>(pidx)) * PAIR + static_cast<int>(crank);
                         const int m0 = t128 * BM;
                         if (b_res && tc.slice != cur_slice) {
                             if (nslices > 0) ptx::mbar_wait(bfree_bar, (nslices - 1) & 1);
@@ -499,6 +505,20 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                         for (int h = 0; h < n_mma; ++h) {
                                             const int nh = nb0 + h * bn_h;
                                             const uint32_t bh = b_dst + h * b_half_b;
+                                            if constexpr (PAIR == 2) {
+                                                if (mcs > 1) {
+                                                    if (b_mn) {
+                                                        for (int q = 0; q < b_boxes; ++q)
+                                                            ptx::tma_load_3d_pair_mc(bh + q * box_b + pidx * mc_kr * (b_box_n * 2), &tmB, fb,
+                                                                                     nh + q * b_box_n, k0 + static_cast<int>(pidx) * mc_kr,
+                                                                                     tc.g, mc_mask);
+                                                    } else {
+                                                        ptx::tma_load_3d_pair_mc(bh + pidx * mc_nr * 128, &tmB, fb, k0,
+                                                                                 nh + static_cast<int>(pidx) * mc_nr, tc.g, mc_mask);
+                                                    }
+                                                    continue;
+                                                }
+                                            }
                                             if (b_mn) {
                                                 for (int q = 0; q < b_boxes; ++q)
                                                     load3(bh + q * box_b, &tmB, fb, nh + q * b_box_n, k0, tc.g);
