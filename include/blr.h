@@ -125,7 +125,10 @@ size_t blr_monarch_workspace_size(int64_t n_tok, int64_t d_in, int64_t d_out, in
  *   V [b1, p, r], S [b1, b2, r] (the diagonals of S_{l,k}), U [b2, r, q], Y [n_tok, d_out].
  *   (north_star's s_ij is S[j, i, :]: index order (input block, output block); R5.)
  *   Workspace: the S-weighted block sums Z'' (bf16, b2 * n_tok * r values) and, when b1*r > 512,
- *   the fp16 first-stage outputs Z_l (b1 * n_tok * r values), token count padded to 128.
+ *   the fp16 first-stage outputs Z_l (b1 * n_tok * r values), token count padded to 128, then
+ *   (b1*r > 512) 4-byte ready counters of the opt-in pipelined one-launch layer (1 + 2 per
+ *   128-token tile of the padded 256-row tiles, rounded up to 256 B; the library zeroes them on
+ *   `stream` itself before that launch).  The caller owns the memory; the library keeps nothing.
  */
 blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1,
                             int64_t b2, int64_t r, const void* V, const void* S, const void* U,
