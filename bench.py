@@ -528,20 +528,28 @@ def measure(w, n, dev, stream, args, ws, rank, flush, full=True):
     bw_t = alg["bytes"] / peaks["hbm_gbs"] / 1e9
     tc_t = alg["flops"] / (peaks["bf16_tflops"] * 1e12)
     bound = "hbm" if bw_t >= tc_t else "tensor"
+    # the contract's denominator: the burst figure for a kernel timed alone, the sustained one for
+    # a kernel timed inside a long step (the dominant launch is timed inside the graph of the whole
+    # step, which runs for milliseconds at the power-capped steady-state clock)
+    long_step = t_ms >= 1.0 and bool(peaks.get("bf16_tflops_sustained"))
     if bound == "hbm":
         achieved, peak, unit = alg["bytes"] / dt_s / 1e9, peaks["hbm_gbs"], "GB/s"
+        note = "copy HBM GB/s from MEASURED_PEAKS.json"
     else:
-        achieved, peak, unit = alg["flops"] / dt_s / 1e12, peaks["bf16_tflops"], "TFLOP/s"
+        achieved, unit = alg["flops"] / dt_s / 1e12, "TFLOP/s"
+        peak = peaks["bf16_tflops_sustained"] if long_step else peaks["bf16_tflops"]
+        note = (f"sustained bf16 TF/s from MEASURED_PEAKS.json (kernel timed inside a {t_ms:.1f}-ms step)"
+                if long_step else "burst bf16 TF/s from MEASURED_PEAKS.json (short step)")
     roof = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
             "traffic": profiled_traffic(Ld, phase, w.key),
             "kernel": f"{phase_kind(Ld, phase)} ({Ld.model}.{Ld.name}.{Ld.method} {phase})",
             "algorithmic_bytes": alg["bytes"], "algorithmic_flops": alg["flops"], "launch_ms": launch_ms[jmax],
             "share_of_step": launch_ms[jmax] / t_ms, "peak_source": peaks.get("source", "measured"),
-            "peak_note": "burst bf16 / copy HBM from MEASURED_PEAKS.json",
+            "peak_note": note,
             "kernel_io_bytes": phase_io_bytes(Ld, n, phase)}
     roof["kernel_io_gbs"] = roof["kernel_io_bytes"] / dt_s / 1e9
-    if peaks.get("bf16_tflops_sustained") and bound == "tensor":
-        roof["frac_of_sustained"] = achieved / peaks["bf16_tflops_sustained"]
+    if bound == "tensor":
+        roof["frac_of_burst"] = achieved / peaks["bf16_tflops"]
 
     dense = None if args.no_dense else dense_comparator(arm, flush, stream, K, W, dev, ws, not args.eager)
     e2e = e2e_run(arm, flush, stream, min(K, 10), dev, ws) if full else None
