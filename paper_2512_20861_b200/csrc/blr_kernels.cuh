@@ -417,7 +417,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             int pipe_ok = -1;  // highest token tile of A known ready (pipelined layer)
             int bp_ok = -1;    // highest token tile cleared by back-pressure
             bool fast_done = false;
-            if constexpr (KIND == KIND_GEMM) {
+            if constexpr (KIND == KIND_GEMM || KIND == KIND_MONARCH_PROJ) {
                 if (trace == nullptr && p.fast_prod) {
                     // Lean producer for the GEMM kind: every parameter the K loop needs is hoisted
                     // into registers and every per-tile coordinate computed once per tile, so a K
@@ -449,6 +449,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         const TileCoord tc = tile_get(p, titer, tile_tab, it);
                         const int t128 = (tc.m_blk * mcs + static_cast<int>(pidx)) * PAIR + static_cast<int>(crank);
                         const int m0 = t128 * BM;
+                        // Monarch: first output block k of this CTA's share of the tile's k blocks
+                        const int kblk0 = tc.n_blk * p.kb_per_tile + static_cast<int>(crank) * (p.kb_per_tile / PAIR);
                         if (b_res && tc.slice != cur_slice) {
                             if (nslices > 0) ptx::mbar_wait(bfree_bar, (nslices - 1) & 1);
                             if (ptx::elect_one()) {
@@ -457,7 +459,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                     const uint32_t b_dst = b_base + kb * b_stage_b;
                                     const uint32_t bb = bfull_bar + 8 * kb;
                                     if (leader) ptx::mbar_arrive_expect_tx(bb, b_bytes * PAIR);
-                                    if (b_mn) {
+                                    if constexpr (KIND == KIND_MONARCH_PROJ) {
+                                        load4(b_dst, &tmB, bb, kb * BK, 0, kblk0, tc.g);
+                                    } else if (b_mn) {
                                         for (int j = 0; j < b_boxes; ++j)
                                             load3(b_dst + j * box_b, &tmB, bb, n0 + j * b_box_n, kb * BK, tc.g);
                                     } else {
@@ -498,6 +502,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                     const int part = (a_lo_off > 0 && kb >= kb_half) ? 1 : 0;
                                     const int k0 = (kb - part * kb_half) * BK;  // padded block: zero-filled
                                     const uint32_t a_dst = a_st + j * a_blk;
+                                    if constexpr (KIND == KIND_MONARCH_PROJ) {
+                                        // A = X viewed [n_tok][b1][p]; B = V viewed 4-D (a, rho', k, l): the
+                                        // permutations of PAPER.md L194 are this box's coordinates (§5.2)
+                                        load3(a_dst, &tmA, fb, k0, tc.g, m0);
+                                        if (!b_res) load4(b_st + j * b_stage_b, &tmB, fb, k0, 0, kblk0, tc.g);
+                                        continue;
+                                    }
                                     if (a_blk_mode) load3(a_dst, &tmA, fb, 0, a_row0 + kb * 128, 0);
                                     else load3(a_dst, &tmA, fb, part * a_lo_off + k0, a_c1, a_c2);
                                     if (!b_res) {
