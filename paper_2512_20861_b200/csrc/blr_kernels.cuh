@@ -417,7 +417,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             int pipe_ok = -1;  // highest token tile of A known ready (pipelined layer)
             int bp_ok = -1;    // highest token tile cleared by back-pressure
             bool fast_done = false;
-            if constexpr (KIND == KIND_GEMM || KIND == KIND_MONARCH_PROJ) {
+            {
                 if (trace == nullptr && p.fast_prod) {
                     // Lean producer for the GEMM kind: every parameter the K loop needs is hoisted
                     // into registers and every per-tile coordinate computed once per tile, so a K
@@ -490,6 +490,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         const int a_row0 = (tc.g * a_tiles + t128) * a_nch * 16;  // tile-blocked A
                         const int a_c1 = a_gmid ? tc.g : m0, a_c2 = a_gmid ? m0 : tc.g;
                         const int nb0 = tc.n_blk * BNf + static_cast<int>(crank) * bn_cta;  // half 0, this CTA
+                        const int n_sub = KIND == KIND_BLAST_PROJ ? p.n_sub : 1;  // BLAST proj: the b1 sub-GEMMs l
+                        for (int sub = 0; sub < n_sub; ++sub)
                         for (int si = 0; si < ns; ++si) {
                             ptx::mbar_wait(empty_bar + 8 * stage, phase ^ 1);
                             const uint32_t fb = full_bar + 8 * stage;
@@ -507,6 +509,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                         // permutations of PAPER.md L194 are this box's coordinates (§5.2)
                                         load3(a_dst, &tmA, fb, k0, tc.g, m0);
                                         if (!b_res) load4(b_st + j * b_stage_b, &tmB, fb, k0, 0, kblk0, tc.g);
+                                        continue;
+                                    }
+                                    if constexpr (KIND == KIND_BLAST_PROJ) {  // sub = l: X_l and V_l
+                                        ptx::tma_load_3d(a_dst, &tmA, fb, k0, sub, m0);
+                                        const uint32_t b_dst = b_st + j * b_stage_b;
+                                        for (int q = 0; q < b_boxes; ++q)
+                                            ptx::tma_load_3d(b_dst + q * box_b, &tmB, fb, nb0 + q * b_box_n, k0, sub);
                                         continue;
                                     }
                                     if (a_blk_mode) load3(a_dst, &tmA, fb, 0, a_row0 + kb * 128, 0);
