@@ -124,6 +124,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ============================================================ TMA producer ==========
         int stage = 0;
         uint32_t phase = 0;
+        // loop parameters pinned in registers (the compiler otherwise re-reads them from the
+        // constant bank after every asm statement; DESIGN.md §5.1 "lean producer")
+        const int stages = ptx::pin(p.stages), g1 = ptx::pin(p.g1), k1b = ptx::pin(p.k1_blocks);
+        const int bn2 = ptx::pin(p.bn2), b1_boxes = ptx::pin(p.b1_boxes), b2_boxes = ptx::pin(p.b2_boxes);
+        const uint32_t slot_bytes = ptx::pin(p.slot_bytes), s1_bytes = ptx::pin(p.s1_bytes);
+        const uint32_t b2_bytes = ptx::pin(p.b2_bytes);
+        const bool mon = p.mon != 0, b2_mn = p.b2_mn != 0;
         ptx::griddep_wait();  // X may be the previous kernel's output
         // the next kernel may start its prologue only once everything before this launch is
         // complete (it may read weights before its own griddepcontrol.wait)
@@ -132,41 +139,41 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             int T, kq, c_lo, c_hi;
             item_of(it, T, kq, c_lo, c_hi);
             const int m0 = T * BM;
-            for (int s = 0; s < p.g1; ++s) {  // S1 steps: X block + V block
-                for (int kb = 0; kb < p.k1_blocks; ++kb) {
+            for (int s = 0; s < g1; ++s) {  // S1 steps: X block + V block
+                for (int kb = 0; kb < k1b; ++kb) {
                     ptx::mbar_wait(empty_bar + 8 * stage, phase ^ 1);
-                    const uint32_t slot = ring + stage * p.slot_bytes, fb = full_bar + 8 * stage;
+                    const uint32_t slot = ring + stage * slot_bytes, fb = full_bar + 8 * stage;
                     if (ptx::elect_one()) {
-                        ptx::mbar_arrive_expect_tx(fb, p.s1_bytes);
+                        ptx::mbar_arrive_expect_tx(fb, s1_bytes);
                         const int k0 = kb * BK;
-                        if (p.mon) {
+                        if (mon) {
                             ptx::tma_load_3d(slot, &tmA, fb, k0, s, m0);              // X viewed (p, b1, n)
                             ptx::tma_load_4d(slot + BM * BK * 2, &tmB1, fb, k0, 0, kq, s);  // V_{l,k} rows
                         } else {
                             ptx::tma_load_3d(slot, &tmA, fb, k0, m0, 0);
-                            for (int j = 0; j < p.b1_boxes; ++j)
+                            for (int j = 0; j < b1_boxes; ++j)
                                 ptx::tma_load_3d(slot + BM * BK * 2 + j * (64 * BK * 2), &tmB1, fb, j * 64, k0, 0);
                         }
                     }
                     __syncwarp();
-                    if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    if (++stage == stages) { stage = 0; phase ^= 1; }
                 }
             }
-            for (int c0 = c_lo; c0 < c_hi; c0 += p.bn2) {  // S3 steps: U blocks
+            for (int c0 = c_lo; c0 < c_hi; c0 += bn2) {  // S3 steps: U blocks
                 for (int kb = 0; kb < k2b; ++kb) {
                     ptx::mbar_wait(empty_bar + 8 * stage, phase ^ 1);
-                    const uint32_t slot = ring + stage * p.slot_bytes, fb = full_bar + 8 * stage;
+                    const uint32_t slot = ring + stage * slot_bytes, fb = full_bar + 8 * stage;
                     if (ptx::elect_one()) {
-                        ptx::mbar_arrive_expect_tx(fb, p.b2_bytes);
-                        if (p.b2_mn) {
-                            for (int j = 0; j < p.b2_boxes; ++j)
+                        ptx::mbar_arrive_expect_tx(fb, b2_bytes);
+                        if (b2_mn) {
+                            for (int j = 0; j < b2_boxes; ++j)
                                 ptx::tma_load_3d(slot + j * (64 * BK * 2), &tmB2, fb, c0 + j * 64, kb * BK, kq);
                         } else {
                             ptx::tma_load_3d(slot, &tmB2, fb, kb * BK, c0, kq);  // U_k [q][b1 r'] K-major
                         }
                     }
                     __syncwarp();
-                    if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    if (++stage == stages) { stage = 0; phase ^= 1; }
                 }
             }
         }
@@ -174,6 +181,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // ============================================================ MMA issuer ============
         const uint32_t idesc1 = ptx::idesc_bf16(BM, p.n1, p.b1_mn);
         const uint32_t idesc2 = ptx::idesc_bf16(BM, p.bn2, p.b2_mn);
+        const int stages = ptx::pin(p.stages), g1 = ptx::pin(p.g1), k1b = ptx::pin(p.k1_blocks), n1 = ptx::pin(p.n1);
+        const int bn2 = ptx::pin(p.bn2);
+        const uint32_t slot_bytes = ptx::pin(p.slot_bytes);
+        const uint32_t b1_kstep = ptx::pin(p.b1_kstep), b1_lbo = ptx::pin(p.b1_lbo), b1_sbo = ptx::pin(p.b1_sbo);
+        const uint32_t b2_kstep = ptx::pin(p.b2_kstep), b2_lbo = ptx::pin(p.b2_lbo), b2_sbo = ptx::pin(p.b2_sbo);
         int stage = 0;
         uint32_t phase = 0;
         uint32_t use = 0;  // accumulator uses so far (buffer = use & 1)
@@ -184,24 +196,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t b = use & 1;
                 ptx::mbar_wait(tempty_bar + 8 * b, ((use >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
-                for (int s = 0; s < p.g1; ++s) {
-                    const uint32_t d = tmem_base + b * 256 + s * p.n1;
-                    for (int kb = 0; kb < p.k1_blocks; ++kb) {
+                for (int s = 0; s < g1; ++s) {
+                    const uint32_t d = tmem_base + b * 256 + s * n1;
+                    for (int kb = 0; kb < k1b; ++kb) {
                         ptx::mbar_wait(full_bar + 8 * stage, phase);
                         ptx::tc_fence_after();
                         if (ptx::elect_one()) {
-                            const uint32_t slot = ring + stage * p.slot_bytes;
+                            const uint32_t slot = ring + stage * slot_bytes;
 #pragma unroll
                             for (int kk = 0; kk < BK / UMMA_K; ++kk) {
                                 const uint64_t ad = ptx::smem_desc(slot + kk * 32, 16, 1024, ptx::LAYOUT_SW128);
-                                const uint64_t bd = ptx::smem_desc(slot + BM * BK * 2 + kk * p.b1_kstep, p.b1_lbo, p.b1_sbo,
+                                const uint64_t bd = ptx::smem_desc(slot + BM * BK * 2 + kk * b1_kstep, b1_lbo, b1_sbo,
                                                                    ptx::LAYOUT_SW128);
                                 ptx::mma_bf16(d, ad, bd, idesc1, (kb | kk) != 0);
                             }
                             ptx::mma_commit(empty_bar + 8 * stage);
                         }
                         __syncwarp();
-                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                        if (++stage == stages) { stage = 0; phase ^= 1; }
                     }
                 }
                 if (ptx::elect_one()) ptx::mma_commit(tfull_bar + 8 * b);
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             ptx::mbar_wait(zready_bar, it & 1);  // Z (bf16) is in smem
             ptx::tc_fence_after();
-            for (int c0 = c_lo; c0 < c_hi; c0 += p.bn2) {  // ---- S3 chunks
+            for (int c0 = c_lo; c0 < c_hi; c0 += bn2) {  // ---- S3 chunks
                 const uint32_t b = use & 1;
                 ptx::mbar_wait(tempty_bar + 8 * b, ((use >> 1) & 1) ^ 1);
                 ptx::tc_fence_after();
@@ -218,17 +230,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     ptx::mbar_wait(full_bar + 8 * stage, phase);
                     ptx::tc_fence_after();
                     if (ptx::elect_one()) {
-                        const uint32_t slot = ring + stage * p.slot_bytes;
+                        const uint32_t slot = ring + stage * slot_bytes;
 #pragma unroll
                         for (int kk = 0; kk < BK / UMMA_K; ++kk) {
                             const uint64_t ad = ptx::smem_desc(zs + kb * 16384 + kk * 32, 16, 1024, ptx::LAYOUT_SW128);
-                            const uint64_t bd = ptx::smem_desc(slot + kk * p.b2_kstep, p.b2_lbo, p.b2_sbo, ptx::LAYOUT_SW128);
+                            const uint64_t bd = ptx::smem_desc(slot + kk * b2_kstep, b2_lbo, b2_sbo, ptx::LAYOUT_SW128);
                             ptx::mma_bf16(tmem_base + b * 256, ad, bd, idesc2, (kb | kk) != 0);
                         }
                         ptx::mma_commit(empty_bar + 8 * stage);
                     }
                     __syncwarp();
-                    if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    if (++stage == stages) { stage = 0; phase ^= 1; }
                 }
                 if (ptx::elect_one()) ptx::mma_commit(tfull_bar + 8 * b);
                 __syncwarp();
