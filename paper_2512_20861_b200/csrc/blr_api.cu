@@ -241,7 +241,7 @@ cudaError_t prof_record(void* ev, cudaStream_t st) {
 
 template <int KIND, int PAIR, int OUTF = 0>
 blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const KParams& p_in,
-                  const DevInfo& d, int dev, cudaStream_t stream) {
+                  const DevInfo& d, int dev, cudaStream_t stream, const CUtensorMap* b2 = nullptr) {
     KParams p = p_in;
     p.trace = t_trace;
     p.first = t_last_launches == 0 ? 1 : 0;  // first launch of this API call (PDL ordering, kernel)
@@ -320,7 +320,7 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
     if (prof && prof_record(t_prof_events[2 * t_prof_n], stream) != cudaSuccess)
         return BLR_ERR_CUDA;
-    if (cudaLaunchKernelEx(&cfg, kfn, a, b, c, p) != cudaSuccess) return BLR_ERR_CUDA;
+    if (cudaLaunchKernelEx(&cfg, kfn, a, b, c, b2 ? *b2 : b, p) != cudaSuccess) return BLR_ERR_CUDA;
     if (prof) {
         if (prof_record(t_prof_events[2 * t_prof_n + 1], stream) != cudaSuccess)
             return BLR_ERR_CUDA;
@@ -417,6 +417,15 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     } else {
         p.BN = choose_bn(N, K, p.tiles_m * groups, groups, d.sm_count / pair, pair, out.blocked != 0);
         if (pair == 2 && (p.BN / 2) % 8) p.BN = static_cast<int>(rup(p.BN, 32));
+        // pair tiles over an MN-major B: 256 columns (two whole 64-column slabs per CTA) so each K block
+        // of B is ONE slab-view TMA op instead of two boxes -- the per-SM TMA op rate bounds these phases
+        // (C4 gate S3 2.18 -> 2.08 ms, down S3 0.77 -> 0.73 ms with the padding of the last N tile;
+        // BLR_SLAB=0 restores the balanced width)
+        const char* se = getenv("BLR_SLAB");
+        if (pair == 2 && b_mn_major && !wide && mc <= 1 && p.BN >= 192 && p.BN < 256 && N >= 512 && !(se && se[0] == '0'))
+            p.BN = 256;
+        if (const char* be = getenv("BLR_BN"); be && atoi(be) >= 16 * pair && atoi(be) <= 256)  // A/B experiments
+            p.BN = atoi(be);
     }
     p.N = static_cast<int>(N);
     p.tiles_n = static_cast<int>(cdiv(N, p.BN));
@@ -457,22 +466,23 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
 struct GemmPrep {
     KParams p;
     CUtensorMap ta, tb, tc;
+    CUtensorMap tb2;  // slab view of an MN-major B (KParams::b_slab2), else a copy of tb
     int pair = 1;
     int outf = 0;  // 0 bf16, 1 fp16, 2 fp16 tile-blocked, 3 e4m3 tile-blocked
 };
 
 blr_status gemm_run(const GemmPrep& g, const DevInfo& d, int dev, cudaStream_t st) {
     if (g.outf == 3)
-        return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 3>(g.ta, g.tb, g.tc, g.p, d, dev, st)
-                           : launch<blr::KIND_GEMM, 1, 3>(g.ta, g.tb, g.tc, g.p, d, dev, st);
+        return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 3>(g.ta, g.tb, g.tc, g.p, d, dev, st, &g.tb2)
+                           : launch<blr::KIND_GEMM, 1, 3>(g.ta, g.tb, g.tc, g.p, d, dev, st, &g.tb2);
     if (g.outf == 2)
-        return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st)
-                           : launch<blr::KIND_GEMM, 1, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st);
+        return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st, &g.tb2)
+                           : launch<blr::KIND_GEMM, 1, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st, &g.tb2);
     if (g.outf == 1)
-        return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 1>(g.ta, g.tb, g.tc, g.p, d, dev, st)
-                           : launch<blr::KIND_GEMM, 1, 1>(g.ta, g.tb, g.tc, g.p, d, dev, st);
-    if (g.pair == 2) return launch<blr::KIND_GEMM, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st);
-    return launch<blr::KIND_GEMM, 1>(g.ta, g.tb, g.tc, g.p, d, dev, st);
+        return g.pair == 2 ? launch<blr::KIND_GEMM, 2, 1>(g.ta, g.tb, g.tc, g.p, d, dev, st, &g.tb2)
+                           : launch<blr::KIND_GEMM, 1, 1>(g.ta, g.tb, g.tc, g.p, d, dev, st, &g.tb2);
+    if (g.pair == 2) return launch<blr::KIND_GEMM, 2>(g.ta, g.tb, g.tc, g.p, d, dev, st, &g.tb2);
+    return launch<blr::KIND_GEMM, 1>(g.ta, g.tb, g.tc, g.p, d, dev, st, &g.tb2);
 }
 
 // One plain GEMM phase: out[g](t, c) = sum_k A[g](t, k) B[g](k, c), K-major A.
@@ -583,6 +593,17 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
         const uint32_t box[3] = {static_cast<uint32_t>(p.b_box_n), static_cast<uint32_t>(blr::BK / std::max(1, p.mc)), 1};
         if (!encode(&tb, B, 3, dims, str, box, p.b_box_n == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
             return BLR_ERR_CUDA;
+        // slab view (64 columns, K, whole 64-column slabs, groups): two boxes per K block as one op.
+        // Only whole slabs are described, so a box never reads past a row (or the tensor) end.
+        const char* se = getenv("BLR_SLAB");
+        if (p.b_box_n == 64 && p.b_boxes == 2 && p.mc <= 1 && N / 64 >= 2 && !(se && se[0] == '0')) {
+            const uint64_t d4[4] = {64, static_cast<uint64_t>(K), static_cast<uint64_t>(N / 64), static_cast<uint64_t>(groups)};
+            const uint64_t s4[3] = {static_cast<uint64_t>(N) * 2, 128, static_cast<uint64_t>(N * K) * 2};
+            const uint32_t b4[4] = {64, static_cast<uint32_t>(blr::BK), 2, 1};
+            if (!encode(&g.tb2, B, 4, d4, s4, b4, CU_TENSOR_MAP_SWIZZLE_128B)) return BLR_ERR_CUDA;
+            p.b_slab2 = 1;
+            p.b_nslab = static_cast<int>(N / 64);
+        }
     } else {
         const uint64_t dims[3] = {static_cast<uint64_t>(K), static_cast<uint64_t>(N), static_cast<uint64_t>(groups)};
         const uint64_t str[2] = {static_cast<uint64_t>(K) * 2, static_cast<uint64_t>(K * N) * 2};
@@ -620,6 +641,7 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
         const uint32_t box[4] = {64, 16, static_cast<uint32_t>(p.c_box_w / 8), 1};
         if (!encode(&tc, out.ptr, 4, dims, strb, box, CU_TENSOR_MAP_SWIZZLE_NONE, out.f32)) return BLR_ERR_CUDA;
     }
+    if (!p.b_slab2) g.tb2 = tb;
     // fp16 output (BLAST split-path Z) is a separate instantiation: the bf16 epilogue stays as is
     g.pair = pair;
     g.outf = out.f32 == 3 ? 3 : out.f32 == 2 ? (out.blocked ? 2 : 1) : 0;
@@ -1544,7 +1566,7 @@ blr_status blast_pipe(const DevInfo& d, int dev, cudaStream_t st, const void* X,
     const bool prof = t_prof_events != nullptr && 2 * t_prof_n + 1 < t_prof_cap;
     if (prof && prof_record(t_prof_events[2 * t_prof_n], st) != cudaSuccess) return BLR_ERR_CUDA;
     if (const cudaError_t le = cudaLaunchKernelEx(&cfg, blr::blast_pipe_kernel, g1.ta, g1.tb, g1.tc, tmz, tmzpp, g3.ta,
-                                                  g3.tb, g3.tc, p1, p3, pa);
+                                                  g3.tb, g3.tc, g1.tb2, g3.tb2, p1, p3, pa);
         le != cudaSuccess) {
         if (plan_print) fprintf(stderr, "[blr plan] pipe launch: %s\n", cudaGetErrorString(le));
         return BLR_ERR_CUDA;

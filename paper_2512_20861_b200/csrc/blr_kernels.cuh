@@ -112,6 +112,9 @@ struct KParams {
                                 //   4 skip the whole GEMM epilogue, 8 skip MMAs, 16 plain-arrive slot release (PAIR 1),
                                 //   32 no accumulator hand-off, 64 no resident weight loads
     int fast_prod;              // 1: the lean GEMM producer loop (BLR_FASTPROD=0 selects the generic one)
+    int b_slab2;                // 1: MN-major B with two 64-column boxes per K block: a slab view of B (tmB2,
+    int b_nslab;                //    b_nslab whole 64-column slabs) loads both boxes with ONE TMA op when the
+                                //    CTA's columns are two whole slabs (the per-SM TMA op rate)
     // ---- pipelined BLAST layer (blast_pipe_kernel): per-128-token-tile ready counters
     const unsigned int* pipe_wait;  // A's token tile t is ready once pipe_wait[t] >= pipe_target (nullptr: off)
     unsigned int pipe_target;
@@ -293,7 +296,7 @@ __device__ __forceinline__ void stage_row8(uint32_t buf, int row, int chunk, uin
 // (blast_pipe_kernel), which run it with a virtual block index / grid size.
 template <int KIND, int PAIR, int OUTF = 0>
 __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensorMap& tmB, const CUtensorMap& tmC,
-                                          const KParams& p, uint8_t* smem, int vblock, int vgrid) {
+                                          const CUtensorMap& tmB2, const KParams& p, uint8_t* smem, int vblock, int vgrid) {
     const SmemLayout L = smem_layout(p);
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t a_base = sbase + L.a_off;
@@ -437,6 +440,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     const uint32_t b_stage_b = ptx::pin(p.b_stage_bytes), b_half_b = ptx::pin(p.b_half_bytes);
                     const uint32_t box_b = static_cast<uint32_t>(b_box_n) * BK * 2;
                     const int a_tiles = p.a_tiles;
+                    const bool slab2 = p.b_slab2 != 0;
+                    const int nslab = p.b_nslab;
                     const int ns = ptx::pin(n_steps);
                     const uint32_t tx_f = ptx::pin(tx);
                     // B multicast across the mcs CTA pairs of a cluster (mcs > 1): this pair loads 1/mcs
@@ -540,8 +545,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                                 }
                                             }
                                             if (b_mn) {
-                                                for (int q = 0; q < b_boxes; ++q)
-                                                    load3(bh + q * box_b, &tmB, fb, nh + q * b_box_n, k0, tc.g);
+                                                if (slab2 && (nh & 63) == 0 && (nh >> 6) + 2 <= nslab) {
+                                                    // both 64-column boxes as one op: slab view (64, K, slab, g)
+                                                    load4(bh, &tmB2, fb, 0, k0, nh >> 6, tc.g);
+                                                } else {
+                                                    for (int q = 0; q < b_boxes; ++q)
+                                                        load3(bh + q * box_b, &tmB, fb, nh + q * b_box_n, k0, tc.g);
+                                                }
                                             } else {
                                                 load3(bh, &tmB, fb, k0, nh, tc.g);
                                             }
@@ -1193,11 +1203,11 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
 template <int KIND, int PAIR, int OUTF = 0>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     blr_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ CUtensorMap tmC, const KParams p) {
+                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmB2, const KParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the 128-B swizzle atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    gemm_body<KIND, PAIR, OUTF>(tmA, tmB, tmC, p, smem, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
+    gemm_body<KIND, PAIR, OUTF>(tmA, tmB, tmC, tmB2, p, smem, static_cast<int>(blockIdx.x), static_cast<int>(gridDim.x));
 }
 
 // ------------------------------------------------------------------------- BLAST S2 kernel -----
@@ -1750,6 +1760,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                       const __grid_constant__ CUtensorMap tmZst, const __grid_constant__ CUtensorMap tmZ,
                       const __grid_constant__ CUtensorMap tmZpp, const __grid_constant__ CUtensorMap tmA3,
                       const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmY,
+                      const __grid_constant__ CUtensorMap tmV2, const __grid_constant__ CUtensorMap tmU2,
                       const KParams p1, const KParams p3, const PipeArgs pa) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + (PIPE_SMEM_ALIGN - 1)) &
@@ -1765,7 +1776,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     ptx::cluster_sync();
     const int ticket = static_cast<int>(*s_ticket);
     if (ticket < pa.n1) {
-        gemm_body<KIND_GEMM, 2, 2>(tmX, tmV, tmZst, p1, smem, 2 * ticket + static_cast<int>(crank), 2 * pa.n1);
+        gemm_body<KIND_GEMM, 2, 2>(tmX, tmV, tmZst, tmV2, p1, smem, 2 * ticket + static_cast<int>(crank), 2 * pa.n1);
     } else if (ticket < pa.n1 + pa.n2) {
         S2Pipe sp;
         sp.wait_ctr = pa.ctr + 1;
@@ -1777,7 +1788,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         s2_body<16, false>(tmZ, tmZpp, pa.Z, pa.Zpp, pa.S, pa.n_tok, pa.b1, pa.b2, pa.r, 1, 0, 0, smem,
                            2 * (ticket - pa.n1) + static_cast<int>(crank), 2 * pa.n2, &sp);
     } else {
-        gemm_body<KIND_GEMM, 2, 0>(tmA3, tmU, tmY, p3, smem, 2 * (ticket - pa.n1 - pa.n2) + static_cast<int>(crank),
+        gemm_body<KIND_GEMM, 2, 0>(tmA3, tmU, tmY, tmU2, p3, smem, 2 * (ticket - pa.n1 - pa.n2) + static_cast<int>(crank),
                                    2 * pa.n3);
     }
 }
