@@ -626,7 +626,10 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
         const uint64_t es = static_cast<uint64_t>(esz);
         const uint64_t strb[3] = {static_cast<uint64_t>(out.comp_stride) * es, static_cast<uint64_t>(out.group_stride) * es,
                                   static_cast<uint64_t>(out.row_stride) * es};
-        const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32};
+        // 128-row cooperative stores (KParams::coop_store; BLR_COOP=0: per-warp 32-row boxes)
+        const char* ce = getenv("BLR_COOP");
+        p.coop_store = (p.c_box_w <= 64 && !(ce && ce[0] == '0')) ? 1 : 0;
+        const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, p.coop_store ? 128u : 32u};
         if (!encode(&tc, out.ptr, 4, dims, strb, box, cs.mode, out.f32)) return BLR_ERR_CUDA;
     }
     if (out.blocked) {

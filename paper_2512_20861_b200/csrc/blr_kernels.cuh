@@ -112,6 +112,7 @@ struct KParams {
                                 //   4 skip the whole GEMM epilogue, 8 skip MMAs, 16 plain-arrive slot release (PAIR 1),
                                 //   32 no accumulator hand-off, 64 no resident weight loads
     int fast_prod;              // 1: the lean GEMM producer loop (BLR_FASTPROD=0 selects the generic one)
+    int coop_store;             // 1: 128-row cooperative output stores (one box per chunk per column half)
     int b_slab2;                // 1: MN-major B with two 64-column boxes per K block: a slab view of B (tmB2,
     int b_nslab;                //    b_nslab whole 64-column slabs) loads both boxes with ONE TMA op when the
                                 //    CTA's columns are two whole slabs (the per-SM TMA op rate)
@@ -1101,6 +1102,37 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             ++sig_g;
                         }
                         continue;
+                    }
+                    if constexpr (KIND == KIND_GEMM && OUTF <= 1) {
+                        if (p.coop_store) {
+                            // the four warps of this column half stage their 32 rows of the chunk into one
+                            // 128-row buffer and one thread stores it as ONE tensor box: a quarter of the
+                            // store ops (the per-SM TMA op rate bounds the streamed GEMMs)
+                            const uint32_t hbuf_bytes = 4u * buf_bytes;
+                            const bool iss = (ew & 3) == 0 && lane == 0;
+                            for (int part = 0; part < parts; ++part) {
+                                const uint32_t hbuf = sbase + L.c_off + half * 4u * p.stage_warp_bytes +
+                                                      (nstore % p.stage_bufs) * hbuf_bytes;
+                                ++nstore;
+                                if (iss) {
+                                    if (p.stage_bufs == 2) ptx::bulk_wait_read<1>();
+                                    else ptx::bulk_wait_read<0>();
+                                }
+                                ptx::named_bar_sync(2 + half, 128);
+#pragma unroll
+                                for (int j = 0; j < 8; ++j)
+                                    if (j * 8 < CW)
+                                        stage_row8<OUTF>(hbuf, quarter * 32 + lane, j, row_bytes, p.c_swz,
+                                                         *reinterpret_cast<const float(*)[8]>(&fv[j * 8]), part);
+                                ptx::fence_async_smem();
+                                ptx::named_bar_sync(2 + half, 128);
+                                if (iss && !BLR_DBG_ON(p, 1)) {
+                                    ptx::tma_store_4d(&tmC, hbuf, n0 + c0, part, tc.g, m0);
+                                    ptx::bulk_commit();
+                                }
+                            }
+                            continue;
+                        }
                     }
                     for (int part = 0; part < parts; ++part) {
                         const uint32_t buf = stg + (nstore % p.stage_bufs) * buf_bytes;
