@@ -153,6 +153,23 @@ blr_status blr_blast_matmul_fp8z(const void* X, int64_t n_tok, int64_t d_in, int
                                  void* Y, void* workspace, size_t ws_bytes, blr_stream_t stream);
 
 /*
+ * BLAST factors in a statically re-laid-out, K-major storage (the paper's optimization (1) applied
+ * to BLAST: a one-time re-layout of static weights so every operand is read contiguously along the
+ * contraction):
+ *   Vt [b1, r, p]  with Vt[l][rho][a] = V[l][a][rho]     (V of blr_blast_matmul, per block transposed)
+ *   Ut [b2, q, r]  with Ut[k][c][rho] = U[k][rho][c]
+ * S, X, Y, workspace and errors as blr_blast_matmul; the result is the same function of the same
+ * factors (bitwise equal to blr_blast_matmul on this path).  Supported on the split tensor-core path
+ * (b1*r > 512, r >= 128, n_tok above the small-n range); any other case returns
+ * BLR_ERR_UNSUPPORTED before launching anything (use blr_blast_matmul with the paper layout).
+ * Why: a K-major weight tile is one TMA box per K block whatever its width (an MN-major one needs a
+ * box per 64 columns), and the per-SM TMA op rate bounds these GEMMs.
+ */
+blr_status blr_blast_matmul_kmajor(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1,
+                                   int64_t b2, int64_t r, const void* Vt, const void* S, const void* Ut,
+                                   void* Y, void* workspace, size_t ws_bytes, blr_stream_t stream);
+
+/*
  * Row permutation for chaining a BLR_OUT_TRANSPOSED Monarch layer into the next layer without a
  * permutation pass (optimization (3)): fills the HOST array perm[b2*q] with
  * perm[c*b2 + k] = k*q + c.  If W is the next layer's weight (rows indexed by the canonical input

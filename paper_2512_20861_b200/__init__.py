@@ -18,7 +18,7 @@ import torch
 
 from .build import LIB_PATH, build  # noqa: F401
 
-__all__ = ["load", "lowrank_matmul", "monarch_matmul", "blast_matmul", "BLRError",
+__all__ = ["load", "lowrank_matmul", "monarch_matmul", "blast_matmul", "blast_kmajor_factors", "BLRError",
            "B2_FASTEST", "RPRIME_FASTEST", "OUT_CANONICAL", "OUT_TRANSPOSED", "last_launch_count",
            "lib_path", "transposed_row_perm", "permute_rows_for_transposed_input"]
 
@@ -56,7 +56,9 @@ def load():
                                        ctypes.c_int, vp, vp, sz, vp]
     lib.blr_blast_matmul.argtypes = [vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp]
     lib.blr_blast_matmul_fp8z.argtypes = lib.blr_blast_matmul.argtypes
-    for fn in ("blr_lowrank_matmul", "blr_monarch_matmul", "blr_blast_matmul", "blr_blast_matmul_fp8z"):
+    lib.blr_blast_matmul_kmajor.argtypes = lib.blr_blast_matmul.argtypes
+    for fn in ("blr_lowrank_matmul", "blr_monarch_matmul", "blr_blast_matmul", "blr_blast_matmul_fp8z",
+               "blr_blast_matmul_kmajor"):
         getattr(lib, fn).restype = ctypes.c_int
     lib.blr_lowrank_workspace_size.argtypes = [i64, i64, i64, i64]
     lib.blr_monarch_workspace_size.argtypes = [i64, i64, i64, i64, i64, i64]
@@ -169,24 +171,40 @@ def monarch_matmul(X: torch.Tensor, V: torch.Tensor, U: torch.Tensor, b1: int, b
     return Y
 
 
+def blast_kmajor_factors(V: torch.Tensor, U: torch.Tensor):
+    """The one-time static re-layout of blr_blast_matmul_kmajor (paper's optimization (1) applied to
+    BLAST): Vt [b1, r, p] = V^T per block, Ut [b2, q, r] = U^T per block."""
+    return V.transpose(1, 2).contiguous(), U.transpose(1, 2).contiguous()
+
+
 def blast_matmul(X: torch.Tensor, V: torch.Tensor, S: torch.Tensor, U: torch.Tensor, out=None,
-                 workspace=None, fp8_intermediate: bool = False):
+                 workspace=None, fp8_intermediate: bool = False, kmajor: bool = False):
     """BLAST Y_k = (sum_l (X_l V_l) S_{l,k}) U_k; V [b1,p,r], S [b1,b2,r], U [b2,r,q].
-    fp8_intermediate=True calls blr_blast_matmul_fp8z (e4m3 Z; its own accuracy contract, blr.h)."""
+    fp8_intermediate=True calls blr_blast_matmul_fp8z (e4m3 Z; its own accuracy contract, blr.h).
+    kmajor=True: V, U are blast_kmajor_factors(V, U) (Vt [b1,r,p], Ut [b2,q,r]) and the call goes to
+    blr_blast_matmul_kmajor (split tensor-core path only; same result)."""
     lib = load()
     n, i = X.shape
-    b1, p, r = V.shape
+    if kmajor:
+        if fp8_intermediate:
+            raise ValueError("kmajor and fp8_intermediate are separate entry points")
+        b1, r, p = V.shape
+        b2u, q, ru = U.shape
+    else:
+        b1, p, r = V.shape
+        b2u, ru, q = U.shape
     b1s, b2, rs = S.shape
-    b2u, ru, q = U.shape
     if b1s != b1 or rs != r or b2u != b2 or ru != r or b1 * p != i:
         raise ValueError("inconsistent BLAST factor shapes")
     o = b2 * q
     Y = _out(X, n, o, out)
     ws = _ws(X, lib.blr_blast_workspace_size(n, i, o, b1, b2, r), workspace)
     with torch.cuda.device(X.device):
-        fn = lib.blr_blast_matmul_fp8z if fp8_intermediate else lib.blr_blast_matmul
+        fn = (lib.blr_blast_matmul_kmajor if kmajor else
+              lib.blr_blast_matmul_fp8z if fp8_intermediate else lib.blr_blast_matmul)
         code = fn(_dev_bf16("X", X), n, i, o, b1, b2, r, _dev_bf16("V", V),
                   _dev_bf16("S", S), _dev_bf16("U", U), _dev_bf16("out", Y),
                   ws.data_ptr(), ws.numel() * ws.element_size(), _stream_ptr(X.device))
-    _check("blr_blast_matmul_fp8z" if fp8_intermediate else "blr_blast_matmul", code)
+    _check("blr_blast_matmul_kmajor" if kmajor else
+           "blr_blast_matmul_fp8z" if fp8_intermediate else "blr_blast_matmul", code)
     return Y

@@ -1584,7 +1584,7 @@ blr_status blast_pipe(const DevInfo& d, int dev, cudaStream_t st, const void* X,
 
 blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2, int64_t r,
                       const void* V, const void* S, const void* U, void* Y, void* workspace, size_t ws_bytes,
-                      blr_stream_t stream, bool fp8z) {
+                      blr_stream_t stream, bool fp8z, bool kmaj = false) {
     t_last_launches = 0;
     if (n_tok < 0 || d_in <= 0 || d_out <= 0 || b1 <= 0 || b2 <= 0 || r <= 0) return BLR_ERR_SHAPE;
     if (d_in % b1 || d_out % b2) return BLR_ERR_SHAPE;
@@ -1602,6 +1602,9 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // small n: the weight-streaming kernels; up to 2048 tokens where the tcgen05 alternative is the
     // S1+S2-fused projection, whose parallelism is the handful of 128-token tiles (C1, C5 ViT-B)
+    // K-major factors (blr_blast_matmul_kmajor): the split tensor-core path only
+    if (kmaj && (use_decode(n_tok, blast_fused(b1, r) ? 2048 : 8) || blast_fused(b1, r) || comp_factor(r) != 1 || fp8z))
+        return BLR_ERR_UNSUPPORTED;
     if (use_decode(n_tok, blast_fused(b1, r) ? 2048 : 8)) {  // fp32 Z [b1][n][r] (unless fused away), Z'' [b2][n][r]
         float* z = static_cast<float*>(workspace);
         float* zp2 = z + b1 * n_tok * r;
@@ -1703,6 +1706,7 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
     const char* s2e = getenv("BLR_S2");
     // tensor-core S2 (single-rounded Z''): Z and Z'' tile-blocked [g][T][r/8][128][8]
     const bool s2_mma = comp == 1 && !(s2e && !strcmp(s2e, "cuda"));
+    if (kmaj && !s2_mma) return BLR_ERR_UNSUPPORTED;  // (K-major factors: tensor-core S2 path only)
     const int64_t n_pad = rup(n_tok, blr::BM);
     void* zl = static_cast<char*>(workspace) + static_cast<size_t>(b2) * n_pad * r * 2 * comp;
     // S1: Z[l][t][rho] = (X_l V_l)[t, rho]  -- grouped GEMM over l (A = X viewed (p, b1, n));
@@ -1712,10 +1716,11 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
     OutMap zmap{zl, z8 ? 3 : 2, 1, r, s2_mma ? n_pad * r : n_tok * r, r};
     zmap.blocked = s2_mma ? 1 : 0;
     GemmPrep g1, g3;
-    s = gemm_prepare(g1, d, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, true, zmap, 1);
+    s = gemm_prepare(g1, d, X, 1, d_in, pdim, n_tok, pdim, b1, r, V, !kmaj, zmap, 1);
     if (s != BLR_OK) return s;
-    // S3: Y_k = Z''_k U_k (U is [b2][r][q]: MN-major B); A tile-blocked after the tensor-core S2
-    s = s2_mma ? gemm_prepare(g3, d, zpp, 0, r, n_tok * r, n_tok, r, b2, qdim, U, true,
+    // S3: Y_k = Z''_k U_k (U is [b2][r][q]: MN-major B; kmaj: Ut [b2][q][r], K-major); A tile-blocked
+    // after the tensor-core S2
+    s = s2_mma ? gemm_prepare(g3, d, zpp, 0, r, n_tok * r, n_tok, r, b2, qdim, U, !kmaj,
                               OutMap{Y, 0, 1, d_out, qdim, d_out}, 1, /*a_blocked=*/1)
                : gemm_prepare(g3, d, zpp, 0, r * comp, n_tok * r * comp, n_tok, r, b2, qdim, U, true,
                               OutMap{Y, 0, 1, d_out, qdim, d_out}, comp);
@@ -1792,7 +1797,7 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
             return BLR_OK;
         };
         (void)items;
-        if (!z8 && pipe_wanted(n_tok, b1, b2, r)) {
+        if (!z8 && !kmaj && pipe_wanted(n_tok, b1, b2, r)) {
             s = blast_pipe(d, dev, st, X, d_in, pdim, n_tok, b1, b2, r, V, S, U, Y, qdim, zl, zpp,
                            static_cast<char*>(zl) + static_cast<size_t>(b1) * n_pad * r * 2, tmz, tmzpp);
             if (s != BLR_ERR_UNSUPPORTED) return s;  // (unsupported: nothing was enqueued; three launches)
@@ -1890,6 +1895,12 @@ blr_status blr_blast_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_t 
                             int64_t r, const void* V, const void* S, const void* U, void* Y, void* workspace,
                             size_t ws_bytes, blr_stream_t stream) {
     return blast_impl(X, n_tok, d_in, d_out, b1, b2, r, V, S, U, Y, workspace, ws_bytes, stream, false);
+}
+
+blr_status blr_blast_matmul_kmajor(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,
+                                   int64_t r, const void* Vt, const void* S, const void* Ut, void* Y, void* workspace,
+                                   size_t ws_bytes, blr_stream_t stream) {
+    return blast_impl(X, n_tok, d_in, d_out, b1, b2, r, Vt, S, Ut, Y, workspace, ws_bytes, stream, false, true);
 }
 
 blr_status blr_blast_matmul_fp8z(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out, int64_t b1, int64_t b2,

@@ -84,3 +84,36 @@ def test_pair_s1_odd_token_tiles(cuda_lib, monkeypatch, n):
     rows = np.concatenate([np.arange(0, 128, 7), sample_rows(n, 40)])
     ref = orc.blast_forward(to64(X[rows].cpu()), to64(V), to64(S), to64(U))
     assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"pair S1 n={n}")
+
+
+@pytest.mark.parametrize("n,b1,b2,r,p,q", [
+    (1000, 16, 16, 272, 64, 88),     # ragged tails, r % 64 != 0
+    (4096, 8, 12, 512, 64, 96),      # b1 != b2
+    (130, 16, 16, 1488, 256, 688),   # Llama-7B gate/up shapes (C4)
+    (130, 16, 16, 1488, 688, 256),   # Llama-7B down shapes (C4)
+])
+def test_kmajor_factor_layout(cuda_lib, n, b1, b2, r, p, q):
+    """blr_blast_matmul_kmajor (statically re-laid-out K-major V, U) is the same
+    function of the same factors: bitwise equal to the paper layout and within tolerance of the
+    fp64 oracle (which takes the paper layout)."""
+    i, o = b1 * p, b2 * q
+    X = synth.make_x(n, i, seed=15).to(DEV)
+    V, S, U = [t.to(DEV) for t in synth.blast_factors(i, o, b1, b2, r, seed=15)]
+    Vt, Ut = cuda_lib.blast_kmajor_factors(V, U)
+    Y = cuda_lib.blast_matmul(X, V, S, U)
+    Yk = cuda_lib.blast_matmul(X, Vt, S, Ut, kmajor=True)
+    torch.cuda.synchronize()
+    rows = sample_rows(n, 64)
+    ref = orc.blast_forward(to64(X[rows].cpu()), to64(V), to64(S), to64(U))
+    assert_parity(Yk[torch.as_tensor(rows, device=DEV)], ref, f"kmajor {n, b1, b2, r, p, q}")
+    assert torch.equal(Yk, Y)
+
+
+def test_kmajor_unsupported_paths_enqueue_nothing(cuda_lib):
+    """Outside the split tensor-core path the K-major entry point refuses before any launch."""
+    from paper_2512_20861_b200 import BLRError
+    X = synth.make_x(64, 768, seed=16).to(DEV)
+    V, S, U = [t.to(DEV) for t in synth.blast_factors(768, 768, 4, 4, 16, seed=16)]  # b1 r <= 512: fused path
+    Vt, Ut = cuda_lib.blast_kmajor_factors(V, U)
+    with pytest.raises(BLRError):
+        cuda_lib.blast_matmul(X, Vt, S, Ut, kmajor=True)
