@@ -1538,7 +1538,10 @@ __device__ __forceinline__ void s2_body(const CUtensorMap& tmZ, const CUtensorMa
                 for (uint32_t o = threadIdx.x * 16; o < 128 * 16; o += NT * 16)
                     ptx::st_shared_v4(base + L.a16 + s * b1p * 2048 + b1 * 2048 + o, make_uint4(0, 0, 0, 0));
         } else {
-            for (int s = 0; s < S2M_ASTAGES; ++s)
+            // (the fp16 ring has L.stages = 3 slots, fewer than the S2M_ASTAGES barrier slots: zeroing
+            //  a 4th pad plane wrote past the layout -- past the allocation for small b2 -- found by
+            //  tests/test_gpu_fuzz.py with b1 = 11, b2 <= 2)
+            for (int s = 0; s < nst; ++s)
                 for (uint32_t o = threadIdx.x * 16; o < 128 * 16; o += NT * 16)
                     ptx::st_shared_v4(base + L.a + s * L.a_bytes + b1 * 2048 + o, make_uint4(0, 0, 0, 0));
         }

@@ -72,7 +72,12 @@ def test_fuzz_monarch(cuda_lib, case):
     assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"monarch {case}")
 
 
-@pytest.mark.parametrize("case", _cases("blast", 16 * SCALE, 303 + SEED))
+# regression: odd b1 with b2 <= 2 made the tensor-core S2 zero a pad plane past its smem layout
+# (an illegal address for small b2; found by BLR_FUZZ_SCALE=10 BLR_FUZZ_SEED=7)
+REGRESSION = [(640, 528, 64, 264, 11, 2, 0), (640, 528, 48, 264, 11, 1, 0), (300, 840, 64, 256, 15, 2, 0)]
+
+
+@pytest.mark.parametrize("case", _cases("blast", 16 * SCALE, 303 + SEED) + REGRESSION)
 def test_fuzz_blast(cuda_lib, case):
     n, i, o, r, b1, b2, _ = case
     X = synth.make_x(n, i, seed=n + i).to(DEV)
