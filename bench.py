@@ -211,7 +211,7 @@ def run_reference(args, w):
     sample = f"{rows} token rows of {w.key} through all {len(w.layers)} layers per step (fp64 oracle)"
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{w.key}: {w.desc}", "rows_per_step": rows},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -612,7 +612,7 @@ def main():
         shards = [bdist.shard_rows(w.n, r, ws) for r in range(ws)]
         if rank == 0:
             print(json.dumps({"metric": METRIC, "value": None, "unit": "tokens/s", "n_gpus": ws, "dry_run": True,
-                              "scaling": "strong" if ws > 1 else "weak",
+                              "scaling": "strong",
                               "config": {"workload": f"{w.key}: {w.desc}", "n_tokens_total": w.n,
                                          "shards": shards}}), flush=True)
         if ws > 1:
@@ -649,7 +649,7 @@ def main():
     t_ms = r["t_ms"]
     line = {"metric": METRIC, "value": r["value"], "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
-            "scaling": "strong" if ws > 1 else "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{w.key}: {w.desc}", "n_tokens_total": w.n, "n_tokens_per_gpu": n,
                        "value_def": f"tokens/s through the BLR MLP; one step = {r['n_chains']} chain(s) x {w.n} tokens"
                                     + (f", token rows sharded contiguously over {ws} GPUs" if ws > 1 else ""),
