@@ -1397,7 +1397,10 @@ blr_status blr_monarch_matmul(const void* X, int64_t n_tok, int64_t d_in, int64_
                                 static_cast<uint64_t>(n_tok), static_cast<uint64_t>(b2)};
         const uint64_t cstr[4] = {static_cast<uint64_t>(r_blk) * 2, static_cast<uint64_t>(K2) * 2,
                                   static_cast<uint64_t>(K2 * comp) * 2, static_cast<uint64_t>(K2 * comp * n_tok) * 2};
-        const uint32_t cbox[5] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32, 1};
+        // 128-row cooperative stores (KParams::coop_store, BLR_COOP=0: per-warp 32-row boxes)
+        const char* ce = getenv("BLR_COOP");
+        p.coop_store = (p.c_box_w <= 64 && !(ce && ce[0] == '0')) ? 1 : 0;
+        const uint32_t cbox[5] = {static_cast<uint32_t>(p.c_box_w), 1, 1, p.coop_store ? 128u : 32u, 1};
         if (!encode(&tc, workspace, 5, cd, cstr, cbox, cs.mode)) return BLR_ERR_CUDA;
         // ---- phase 2: Y[t, k q + c] = sum_kk Z'[k][t][kk] U[k][c][kk]  (U is [N][K]: K-major B),
         //      planned before phase 1 is launched

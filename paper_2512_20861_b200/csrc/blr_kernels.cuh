@@ -1103,7 +1103,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         }
                         continue;
                     }
-                    if constexpr (KIND == KIND_GEMM && OUTF <= 1) {
+                    if constexpr ((KIND == KIND_GEMM && OUTF <= 1) || KIND == KIND_MONARCH_PROJ) {
                         if (p.coop_store) {
                             // the four warps of this column half stage their 32 rows of the chunk into one
                             // 128-row buffer and one thread stores it as ONE tensor box: a quarter of the
@@ -1127,7 +1127,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                 ptx::fence_async_smem();
                                 ptx::named_bar_sync(2 + half, 128);
                                 if (iss && !BLR_DBG_ON(p, 1)) {
-                                    ptx::tma_store_4d(&tmC, hbuf, n0 + c0, part, tc.g, m0);
+                                    if constexpr (KIND == KIND_MONARCH_PROJ) {
+                                        // Z'[k][t][l r' + rho] (the b2 <-> b1 permutation)
+                                        const int k = tc.n_blk * p.kb_per_tile + c0 / p.r_blk;
+                                        ptx::tma_store_5d(&tmC, hbuf, c0 % p.r_blk, tc.g, part, m0, k);
+                                    } else {
+                                        ptx::tma_store_4d(&tmC, hbuf, n0 + c0, part, tc.g, m0);
+                                    }
                                     ptx::bulk_commit();
                                 }
                             }
