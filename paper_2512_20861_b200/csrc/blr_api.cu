@@ -732,7 +732,9 @@ blr_status fused_launch(const DevInfo& d, int dev, cudaStream_t st, blr::FParams
         const uint64_t dims[4] = {static_cast<uint64_t>(p.n2), 1, static_cast<uint64_t>(p.g2), static_cast<uint64_t>(p.n_tok)};
         const uint64_t str[3] = {static_cast<uint64_t>(p.n2) * 2, static_cast<uint64_t>(p.n2) * 2,
                                  static_cast<uint64_t>(d_out) * 2};
-        const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, 32};
+        const char* ce = getenv("BLR_COOP");
+        p.coop_store = (p.c_box_w <= 64 && p.y_cs == 0 && !(ce && ce[0] == '0')) ? 1 : 0;
+        const uint32_t box[4] = {static_cast<uint32_t>(p.c_box_w), 1, 1, p.coop_store ? 128u : 32u};
         if (!encode(&tc, Y, 4, dims, str, box, pick_swz(p.c_box_w * 2).mode)) return BLR_ERR_CUDA;
     }
     const int smem = static_cast<int>(blr::fused_layout(p).total + SMEM_SLACK);

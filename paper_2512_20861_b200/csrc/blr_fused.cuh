@@ -47,6 +47,7 @@ struct FParams {
     int y_cs;
     long long y_rs;
     __nv_bfloat16* y;
+    int coop_store;  // 1: the four warps of a column half store a Y chunk's 128 rows as ONE tensor box
 };
 
 struct FLayout {
@@ -320,6 +321,28 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                 const int c = n0 + c0 + j;
                                 if (j < CW && c < p.n2) yb[static_cast<long long>(c) * p.y_cs] = __float2bfloat16_rn(fv[j]);
                             }
+                        }
+                        continue;
+                    }
+                    if (p.coop_store) {  // 128-row cooperative store (a quarter of the TMA store ops)
+                        const uint32_t hbuf = sbase + L.stg + half * 4u * p.stage_warp_bytes +
+                                              (nstore % p.stage_bufs) * (128u * row_bytes);
+                        ++nstore;
+                        const bool iss = (ew & 3) == 0 && lane == 0;
+                        if (iss) {
+                            if (p.stage_bufs == 2) ptx::bulk_wait_read<1>();
+                            else ptx::bulk_wait_read<0>();
+                        }
+                        ptx::named_bar_sync(2 + half, 128);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            if (j * 8 < CW)
+                                stage_row8(hbuf, row, j, row_bytes, p.c_swz, *reinterpret_cast<const float(*)[8]>(&fv[j * 8]), 0);
+                        ptx::fence_async_smem();
+                        ptx::named_bar_sync(2 + half, 128);
+                        if (iss) {
+                            ptx::tma_store_4d(&tmC, hbuf, n0 + c0, 0, kq, T * BM);
+                            ptx::bulk_commit();
                         }
                         continue;
                     }
