@@ -590,7 +590,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
-    ap.add_argument("--variants", default="C4M,C4X,C4F8,C4K,C2", help="comma-separated extra workloads (N = 1 only)")
+    ap.add_argument("--variants", default="C2,C4M,C4X,C4F8,C4K", help="comma-separated extra workloads (N = 1 only)")
     ap.add_argument("--eager", action="store_true", help="launch every step from the host (no CUDA graph)")
     ap.add_argument("--flush", default="write+read", choices=["write+read", "write"],
                     help="L2 flush between timed steps (see L2Flush)")
