@@ -16,6 +16,7 @@ import torch
 from oracle import oracle as orc
 from paper_2512_20861_b200 import synth
 from tests.parity import assert_parity, sample_rows, to64
+from tests.test_fp8_budget import FP8_ELEM, FP8_FROB
 
 pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda")
@@ -70,6 +71,12 @@ def test_fuzz_monarch(cuda_lib, case):
     rows = sample_rows(n, 24)
     ref = orc.monarch_forward(to64(X[rows]), to64(V), to64(U), b1, b2, vl)
     assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"monarch {case}")
+    # the transposed output order is the same values permuted, bit for bit
+    q = o // b2
+    Yt = cuda_lib.monarch_matmul(X.to(DEV), V.to(DEV), U.to(DEV), b1, b2, v_layout=vl,
+                                 out_order=cuda_lib.OUT_TRANSPOSED)
+    torch.cuda.synchronize()
+    assert torch.equal(Yt.view(n, q, b2).transpose(1, 2).reshape(n, o), Y), f"monarch transposed {case}"
 
 
 # regression: odd b1 with b2 <= 2 made the tensor-core S2 zero a pad plane past its smem layout
@@ -87,6 +94,14 @@ def test_fuzz_blast(cuda_lib, case):
     rows = sample_rows(n, 24)
     ref = orc.blast_forward(to64(X[rows].cpu()), to64(V), to64(S), to64(U))
     assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"blast {case}")
+    # FP8 first-stage intermediate: its own derived contract (tests/test_fp8_budget.py)
+    Y8 = cuda_lib.blast_matmul(X, V, S, U, fp8_intermediate=True)
+    torch.cuda.synchronize()
+    g = to64(Y8[torch.as_tensor(rows, device=DEV)])
+    nref = np.linalg.norm(ref)
+    if nref > 0:
+        assert np.linalg.norm(g - ref) / nref <= FP8_FROB, f"fp8z {case}"
+    assert np.all(np.abs(g - ref) <= FP8_ELEM * (1.0 + np.abs(ref))), f"fp8z elem {case}"
     # K-major storage: same function, bitwise, wherever the entry point applies
     Vt, Ut = cuda_lib.blast_kmajor_factors(V, U)
     try:
