@@ -1695,7 +1695,9 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
                                 static_cast<uint64_t>(b2)};
         const uint64_t cstr[3] = {static_cast<uint64_t>(r) * 2, static_cast<uint64_t>(r * comp) * 2,
                                   static_cast<uint64_t>(r * comp * n_tok) * 2};
-        const uint32_t cbox[4] = {static_cast<uint32_t>(R / 2), 1, 32, 1};
+        const char* ce = getenv("BLR_COOP");
+        p.coop_store = (ce && ce[0] == '0') ? 0 : 1;  // 128-row cooperative stores of Z''
+        const uint32_t cbox[4] = {static_cast<uint32_t>(R / 2), 1, p.coop_store ? 128u : 32u, 1};
         if (!encode(&tc, zpp, 4, cd, cstr, cbox, pick_swz(R).mode)) return BLR_ERR_CUDA;
         // ---- S3: Y_k = Z''_k U_k  (U is [b2][r][q]: MN-major B), planned before phase 1 launches
         GemmPrep g3;

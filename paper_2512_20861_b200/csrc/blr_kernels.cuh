@@ -915,9 +915,20 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 const uint32_t row_bytes = W * 2;
                 const uint32_t kstride = 32 * row_bytes;  // staging bytes per output block k
                 const int parts = p.out_lo_off > 0 ? 2 : 1;
+                // cooperative stores: the four warps of a column half stage [k][128 rows][W] together
+                // and one thread stores each k as ONE box (instead of four 32-row boxes)
+                const bool coop = p.coop_store != 0;
+                const bool iss = (ew & 3) == 0 && lane == 0;
+                const uint32_t kst = coop ? 4u * kstride : kstride;
+                const uint32_t sbuf = coop ? sbase + L.c_off + half * 4u * p.stage_warp_bytes + quarter * kstride : stg;
                 for (int part = 0; part < parts; ++part) {
-                    if (lane == 0) ptx::bulk_wait_read<0>();
-                    __syncwarp();
+                    if (coop) {
+                        if (iss) ptx::bulk_wait_read<0>();
+                        ptx::named_bar_sync(2 + half, 128);
+                    } else {
+                        if (lane == 0) ptx::bulk_wait_read<0>();
+                        __syncwarp();
+                    }
                     for (int sc = 0; sc < W / 8; ++sc) {
                         const int col = half * W + sc * 8;  // column within the tile
                         // output blocks k in groups of 8 (64 accumulator registers), inputs l in
@@ -962,7 +973,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                     float f[8];
 #pragma unroll
                                     for (int e = 0; e < 4; ++e) ptx::unpack_f32x2(acc2[k][e], f[2 * e], f[2 * e + 1]);
-                                    stage_row8(stg + (kb0 + k) * kstride, lane, sc, row_bytes, p.c_swz, f, part);
+                                    stage_row8(sbuf + (kb0 + k) * kst, lane, sc, row_bytes, p.c_swz, f, part);
                                 }
                             }
                         }
@@ -970,11 +981,21 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     }
                     if (trace && ew == 0 && lane == 0 && it == 0) trace[11] = clock64();
                     ptx::fence_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        for (int k = 0; k < p.b2; ++k)
-                            ptx::tma_store_4d(&tmC, stg + k * kstride, n0 + half * W, part, row0, k);
-                        ptx::bulk_commit();
+                    if (coop) {
+                        ptx::named_bar_sync(2 + half, 128);
+                        if (iss) {
+                            const uint32_t hb = sbase + L.c_off + half * 4u * p.stage_warp_bytes;
+                            for (int k = 0; k < p.b2; ++k)
+                                ptx::tma_store_4d(&tmC, hb + k * kst, n0 + half * W, part, m0, k);
+                            ptx::bulk_commit();
+                        }
+                    } else {
+                        __syncwarp();
+                        if (lane == 0) {
+                            for (int k = 0; k < p.b2; ++k)
+                                ptx::tma_store_4d(&tmC, stg + k * kstride, n0 + half * W, part, row0, k);
+                            ptx::bulk_commit();
+                        }
                     }
                 }
             } else {
