@@ -24,24 +24,27 @@ SCALE = int(os.environ.get("BLR_FUZZ_SCALE", "1"))   # longer one-off hunts: BLR
 SEED = int(os.environ.get("BLR_FUZZ_SEED", "0"))
 
 
+BIG = os.environ.get("BLR_FUZZ_BIG") == "1"   # one-off hunts at larger token counts / widths
+
+
 def _cases(method, count, seed):
     rng = np.random.default_rng(seed)
     out = []
     for _ in range(count):
-        n = int(rng.choice([1, 5, 16, 100, 200, 384, 640, 1000, 1300, 2500]))
+        n = int(rng.choice([1, 5, 16, 100, 200, 384, 640, 1000, 1300, 2500] + ([4100, 6000, 9000] if BIG else [])))
         if method == "lowrank":
-            i, o = (int(8 * rng.integers(8, 160)) for _ in range(2))
+            i, o = (int(8 * rng.integers(8, 512 if BIG else 160)) for _ in range(2))
             r = int(8 * rng.integers(2, 40))
             out.append((n, i, o, r, 1, 1, 0))
         elif method == "monarch":
             b1, b2 = int(rng.integers(1, 9)), int(rng.integers(1, 9))
-            p, q = (int(8 * rng.integers(2, 24)) for _ in range(2))
-            rb = int(8 * rng.integers(1, 5))
+            p, q = (int(8 * rng.integers(2, 64 if BIG else 24)) for _ in range(2))
+            rb = int(8 * rng.integers(1, 13 if BIG else 5))
             out.append((n, b1 * p, b2 * q, rb, b1, b2, int(rng.integers(0, 2))))
         else:
             b1, b2 = int(rng.integers(1, 17)), int(rng.integers(1, 17))
-            p, q = (int(8 * rng.integers(2, 24)) for _ in range(2))
-            r = int(8 * rng.integers(2, 48))
+            p, q = (int(8 * rng.integers(2, 64 if BIG else 24)) for _ in range(2))
+            r = int(8 * rng.integers(2, 160 if BIG else 48))
             out.append((n, b1 * p, b2 * q, r, b1, b2, 0))
     return out
 
