@@ -1526,6 +1526,18 @@ blr_status blast_pipe(const DevInfo& d, int dev, cudaStream_t st, const void* X,
     pa.r = static_cast<int>(r);
     pa.z_target = static_cast<unsigned int>(b1 * p1.tiles_n * 2);
     pa.tiles_pad = tiles_pad;
+    // L2 policy (BLR_PIPE_HINTS=0: none): the handed-over Z / Z'' evict-last, the streams that are
+    // read once (X, Y, Z after S2) evict-first, the weights evict-last
+    const char* he = getenv("BLR_PIPE_HINTS");
+    if (!(he && he[0] == '0')) {
+        p1.l2_a = 1;
+        p1.l2_b = 2;
+        p1.l2_out = 2;
+        pa.l2_z = 1;
+        pa.l2_zz = 2;
+        p3.l2_b = 2;
+        p3.l2_out = 1;
+    }
     pa.win = blr::S2_PIPE_WIN;
     if (const char* we = getenv("BLR_PIPE_WIN")) pa.win = std::max(1, atoi(we));
     if (p1.pipe_bp != nullptr) p1.pipe_bp_dist = std::max(p1.pipe_bp_dist, pa.win);

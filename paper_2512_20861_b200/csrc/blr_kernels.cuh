@@ -113,6 +113,8 @@ struct KParams {
                                 //   32 no accumulator hand-off, 64 no resident weight loads
     int fast_prod;              // 1: the lean GEMM producer loop (BLR_FASTPROD=0 selects the generic one)
     int coop_store;             // 1: 128-row cooperative output stores (one box per chunk per column half)
+    int l2_a, l2_b, l2_out;     // L2 cache-policy hints of the A / B loads and the output stores (lean
+                                // producer and GEMM-kind epilogues): 0 none, 1 evict_first, 2 evict_last
     int b_slab2;                // 1: MN-major B with two 64-column boxes per K block: a slab view of B (tmB2,
     int b_nslab;                //    b_nslab whole 64-column slabs) loads both boxes with ONE TMA op when the
                                 //    CTA's columns are two whole slabs (the per-SM TMA op rate)
@@ -445,6 +447,26 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     const int nslab = p.b_nslab;
                     const int ns = ptx::pin(n_steps);
                     const uint32_t tx_f = ptx::pin(tx);
+                    const int hint_a = p.l2_a, hint_b = p.l2_b;
+                    const uint64_t pol_a = ptx::l2_policy(hint_a), pol_b = ptx::l2_policy(hint_b);
+                    auto load3h = [&](uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2, int hint,
+                                      uint64_t pol) {
+                        if (hint == 0) {
+                            load3(dst, m, bar, c0, c1, c2);
+                        } else {
+                            if constexpr (PAIR == 2) ptx::tma_load_3d_pair_hint(dst, m, bar, c0, c1, c2, pol);
+                            else ptx::tma_load_3d_hint(dst, m, bar, c0, c1, c2, pol);
+                        }
+                    };
+                    auto load4h = [&](uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2, int c3,
+                                      int hint, uint64_t pol) {
+                        if (hint == 0) {
+                            load4(dst, m, bar, c0, c1, c2, c3);
+                        } else {
+                            if constexpr (PAIR == 2) ptx::tma_load_4d_pair_hint(dst, m, bar, c0, c1, c2, c3, pol);
+                            else ptx::tma_load_4d_hint(dst, m, bar, c0, c1, c2, c3, pol);
+                        }
+                    };
                     // B multicast across the mcs CTA pairs of a cluster (mcs > 1): this pair loads 1/mcs
                     // of every B box (K rows for MN-major, N rows for K-major) for all of them
                     uint16_t mc_mask = 0;
@@ -524,8 +546,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                             ptx::tma_load_3d(b_dst + q * box_b, &tmB, fb, nb0 + q * b_box_n, k0, sub);
                                         continue;
                                     }
-                                    if (a_blk_mode) load3(a_dst, &tmA, fb, 0, a_row0 + kb * 128, 0);
-                                    else load3(a_dst, &tmA, fb, part * a_lo_off + k0, a_c1, a_c2);
+                                    if (a_blk_mode) load3h(a_dst, &tmA, fb, 0, a_row0 + kb * 128, 0, hint_a, pol_a);
+                                    else load3h(a_dst, &tmA, fb, part * a_lo_off + k0, a_c1, a_c2, hint_a, pol_a);
                                     if (!b_res) {
                                         const uint32_t b_dst = b_st + j * b_stage_b;
                                         for (int h = 0; h < n_mma; ++h) {
@@ -548,13 +570,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                             if (b_mn) {
                                                 if (slab2 && (nh & 63) == 0 && (nh >> 6) + 2 <= nslab) {
                                                     // both 64-column boxes as one op: slab view (64, K, slab, g)
-                                                    load4(bh, &tmB2, fb, 0, k0, nh >> 6, tc.g);
+                                                    load4h(bh, &tmB2, fb, 0, k0, nh >> 6, tc.g, hint_b, pol_b);
                                                 } else {
                                                     for (int q = 0; q < b_boxes; ++q)
-                                                        load3(bh + q * box_b, &tmB, fb, nh + q * b_box_n, k0, tc.g);
+                                                        load3h(bh + q * box_b, &tmB, fb, nh + q * b_box_n, k0, tc.g, hint_b, pol_b);
                                                 }
                                             } else {
-                                                load3(bh, &tmB, fb, k0, nh, tc.g);
+                                                load3h(bh, &tmB, fb, k0, nh, tc.g, hint_b, pol_b);
                                             }
                                         }
                                     }
@@ -859,6 +881,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
         // a token tile's ready counter once its stores have landed, two tiles later (bulk groups of
         // the newer tile may still be in flight; their count bounds the wait)
         const bool sig_iss = OUTF >= 2 && p.pipe_sig != nullptr && (ew & 3) == 0 && lane == 0;
+        const uint64_t pol_out = ptx::l2_policy(p.l2_out);
         int sig_t[2] = {-1, -1};  // token tiles of the two previous tiles (oldest first)
         int sig_g = 0;            // bulk groups the previous tile committed
         auto sig_flush = [&](int keep_groups) {
@@ -1118,7 +1141,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             // a pair's second tile past n_tok is skipped: it would alias the next
                             // group's first tile)
                             const int cc = (n0 + c0) >> 3;
-                            ptx::tma_store_4d(&tmC, hbuf, 0, 0, cc, tc.g * p.o_tiles + m0 / BM);
+                            if (p.l2_out) ptx::tma_store_4d_hint(&tmC, hbuf, 0, 0, cc, tc.g * p.o_tiles + m0 / BM, pol_out);
+                            else ptx::tma_store_4d(&tmC, hbuf, 0, 0, cc, tc.g * p.o_tiles + m0 / BM);
                             ptx::bulk_commit();
                             ++sig_g;
                         }
@@ -1153,7 +1177,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                         const int k = tc.n_blk * p.kb_per_tile + c0 / p.r_blk;
                                         ptx::tma_store_5d(&tmC, hbuf, c0 % p.r_blk, tc.g, part, m0, k);
                                     } else {
-                                        ptx::tma_store_4d(&tmC, hbuf, n0 + c0, part, tc.g, m0);
+                                        if (p.l2_out) ptx::tma_store_4d_hint(&tmC, hbuf, n0 + c0, part, tc.g, m0, pol_out);
+                                        else ptx::tma_store_4d(&tmC, hbuf, n0 + c0, part, tc.g, m0);
                                     }
                                     ptx::bulk_commit();
                                 }
@@ -1486,6 +1511,7 @@ struct S2Pipe {
     unsigned int* sig_ctr;         // += 1 per item (T, c) once its Z'' panels are stored
     int win;                       // token tiles per window
     int dbg;                       // BLR_DEBUG_KNOBS builds: 1 no acquire waits, 2 no store-completion waits
+    int l2_in, l2_out;             // L2 hints of the Z loads / Z'' stores (0 none, 1 evict_first, 2 evict_last)
 };
 
 template <int MAXB2, bool FP8 = false>
@@ -1601,7 +1627,11 @@ __device__ __forceinline__ void s2_body(const CUtensorMap& tmZ, const CUtensorMa
                 ptx::mbar_arrive_expect_tx(a_full + 8 * s, static_cast<uint32_t>(b1 * (FP8 ? 1024 : 2048)));
                 // the b1 panels (l, T, c) in ONE tensor copy: Z viewed (64, 16, tiles*r/8, b1),
                 // box (64, 16, 1, b1) -> smem [l][2 KB] (fp8: 1-KB panels, 64-B rows)
-                ptx::tma_load_4d(base + L.a + s * L.a_bytes, &tmZ, a_full + 8 * s, 0, 0, (T + t0) * nchunks + c, 0);
+                if (rr && pipe->l2_in)
+                    ptx::tma_load_4d_hint(base + L.a + s * L.a_bytes, &tmZ, a_full + 8 * s, 0, 0, (T + t0) * nchunks + c, 0,
+                                          ptx::l2_policy(pipe->l2_in));
+                else
+                    ptx::tma_load_4d(base + L.a + s * L.a_bytes, &tmZ, a_full + 8 * s, 0, 0, (T + t0) * nchunks + c, 0);
             }
         }
         __syncwarp();
@@ -1726,7 +1756,11 @@ __device__ __forceinline__ void s2_body(const CUtensorMap& tmZ, const CUtensorMa
             ptx::named_bar_sync(1, 128);
             if (issuer) {
                 // panels (k, T, c) for all k in ONE tensor store (Z'' viewed like Z)
-                ptx::tma_store_4d(&tmZpp, base + L.c + cb * L.c_bytes, 0, 0, (T + t0o) * nchunks + c, 0);
+                if (rr && pipe->l2_out)
+                    ptx::tma_store_4d_hint(&tmZpp, base + L.c + cb * L.c_bytes, 0, 0, (T + t0o) * nchunks + c, 0,
+                                           ptx::l2_policy(pipe->l2_out));
+                else
+                    ptx::tma_store_4d(&tmZpp, base + L.c + cb * L.c_bytes, 0, 0, (T + t0o) * nchunks + c, 0);
                 ptx::bulk_commit();
                 if (rr) {  // item j - S2_SIG_LAG's stores have landed: signal its token tile
 #ifdef BLR_DEBUG_KNOBS
@@ -1813,6 +1847,7 @@ struct PipeArgs {
     uint32_t ticket_off;    // dynamic-smem byte offset of the role ticket
     int win;                // S2 role: token tiles per window
     int dbg;                // BLR_DEBUG_KNOBS builds: S2Pipe::dbg
+    int l2_z, l2_zz;        // S2 role's L2 hints: Z loads, Z'' stores
 };
 
 constexpr uint32_t PIPE_SMEM_ALIGN = 1024;
@@ -1846,6 +1881,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         sp.sig_ctr = pa.ctr + 1 + pa.tiles_pad;
         sp.win = pa.win;
         sp.dbg = pa.dbg;
+        sp.l2_in = pa.l2_z;
+        sp.l2_out = pa.l2_zz;
         // (320 threads: warps 8-9 of the S2 role only join its barriers)
         s2_body<16, false>(tmZ, tmZpp, pa.Z, pa.Zpp, pa.S, pa.n_tok, pa.b1, pa.b2, pa.r, 1, 0, 0, smem,
                            2 * (ticket - pa.n1) + static_cast<int>(crank), 2 * pa.n2, &sp);
