@@ -173,6 +173,8 @@ bool finish_plan(KParams& p, bool allow_resident, int stage_buf_bytes, int sms) 
     const int cols = p.n_sub * p.BN;
     if (cols > blr::TMEM_COLS) return false;
     p.acc_bufs = (2 * cols <= blr::TMEM_COLS) ? 2 : 1;
+    // wide tiles (48-KB stages): a 128-entry tile table leaves room for a fourth ring stage
+    if (p.n_mma == 2) p.tab_n = 128;
     // weight-stationary plans are opt-in (BLR_RESIDENT=1): with the lean producer, streamed CTA-pair
     // plans measured as fast or faster on every workload (C4 8.21 -> 7.61 ms, C3 0.93 -> 0.84 ms,
     // C2 / C4M / C5V-256 unchanged; in-process A/B)
@@ -300,9 +302,9 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     if (const char* pe = getenv("BLR_PLAN"); pe && pe[0] == '1')
         fprintf(stderr,
                 "[blr plan] kind=%d pair=%d mc=%d grid=%d tiles=%dx%dx%d BN=%d mma=%d bbox=%d kblk=%d kbox=%d stages=%d res=%d "
-                "cps=%d bufs=%d acc=%d cbox=%d smem=%d\n",
+                "cps=%d bufs=%d acc=%d cbox=%d split=%d smem=%d\n",
                 KIND, PAIR, p.mc, grid, p.tiles_m, p.groups, p.tiles_n, p.BN, p.n_mma, p.b_box_n, p.k_blocks, p.kbox, p.stages,
-                p.b_resident, p.cps, p.stage_bufs, p.acc_bufs, p.c_box_w, smem);
+                p.b_resident, p.cps, p.stage_bufs, p.acc_bufs, p.c_box_w, p.split_rel, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(blr::NUM_THREADS);
@@ -524,16 +526,26 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
             !plan_gemm(p, pair = 1, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, false, 1, !no_res))
             return BLR_ERR_UNSUPPORTED;
     }
-    // wide pair tiles (two MMAs per K step, <= 512 columns, single accumulator): half the operand
-    // bytes per MAC of a 256-column pair tile for streamed, long-K, wide-N phases (C4 gate S3,
-    // down S1); BLR_WIDE=0/1 overrides
+    // wide pair tiles (two MMAs of N = 256 per K step into one 512-column accumulator whose halves
+    // the epilogue frees separately, KParams::split_rel): 48 KB of operands per 128x512x64 MACs
+    // instead of 32 KB per 128x256x64, i.e. 25 % fewer L2 -> SM bytes per MAC.  Default where the
+    // tile is exactly 512 columns of whole 64-column slabs, the A operand is a plain K-major matrix
+    // (the per-half release), K is long enough for the tile's MMAs to cover its epilogue (>= 8 K
+    // blocks; C4 gate S1's 4 and ViT's 2 lose) and there are enough tiles for the halved tile count
+    // to fill the pairs evenly (>= 8 per pair): dense 65536x2048x11008 3.34 -> 2.96 ms, C4 down layer 3.85 -> 3.68 ms;
+    // C3's 4096-token phases lose (3-4 waves of wide tiles).  BLR_WIDE=0/1 overrides (1: any width).
     {
         const char* we = getenv("BLR_WIDE");
-        // measured no faster than 256-column pair tiles (C4 gate/down in-process A/B): opt-in only
-        const bool want = we && we[0] == '1' && !force_pair;
-        if (want && pair == 2 && out.col_stride == 0) {
+        const bool force = we && we[0] == '1';
+        const bool off = (we && we[0] == '0') || force_pair;
+        if (!off && pair == 2 && out.col_stride == 0 && N > 256 && (force || !a_blocked)) {
             KParams w;
-            if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, true)) p = w;
+            if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, true)) {
+                const int units = d.sm_count / 2;
+                const bool auto_ok = w.BN == 512 && b_mn_major && w.b_box_n == 64 && w.stages >= 4 && w.kbox == 1 &&
+                                     w.total_tiles >= 8 * units && w.k_blocks >= 8;
+                if (force || auto_ok) p = w;
+            }
         }
     }
     // B multicast across CTA pairs (cluster of 2 mc CTAs) for streamed pair plans with enough token
@@ -547,6 +559,13 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
             KParams w;
             if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, p.n_mma == 2, mc)) p = w;
         }
+    }
+    // wide tiles free their two MMA column halves separately (KParams::split_rel; BLR_SPLITREL=0 off)
+    {
+        const char* sr = getenv("BLR_SPLITREL");
+        p.split_rel = (p.n_mma == 2 && p.acc_bufs == 1 && !a_blocked && p.kbox == 1 && pair == 2 && !p.b_resident &&
+                       p.mc <= 1 && p.c_box_w <= 64 && p.stages >= 2 && !(sr && sr[0] == '0'))
+                          ? 1 : 0;
     }
     const int esz = 2;
     const Swz cs = pick_swz(p.c_box_w * esz);

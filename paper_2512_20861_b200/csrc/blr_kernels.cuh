@@ -127,6 +127,12 @@ struct KParams {
     int pipe_bp_dist;
     int no_trigger;                 // 1: never trigger the dependent grid early (its CTAs could take the SMs
                                     //    this grid's later CTAs need while the earlier ones wait on them)
+    int tab_n;                      // tile-table entries (0: TILE_TAB); wide plans take 128 so a fourth
+                                    // 48-KB ring stage fits
+    int split_rel;                  // wide tile, one accumulator: the epilogue frees the two MMA column
+                                    // halves separately (tempty_bar[0] / [1]); the next tile's K steps
+                                    // start on half 0 and hold their ring slots until half 1 is free,
+                                    // then catch up
 };
 
 struct SmemLayout {
@@ -136,6 +142,7 @@ struct SmemLayout {
 // threads in the prologue, so the single-thread producer / MMA loops and the epilogue do no
 // integer division per tile (the per-tile index arithmetic of one thread measured ~0.5 us).
 constexpr int TILE_TAB = 256;
+__host__ __device__ inline int tile_tab_n(const KParams& p) { return p.tab_n > 0 ? p.tab_n : TILE_TAB; }
 
 __host__ __device__ inline int kb_resident(const KParams& p) {  // resident B blocks (padded to kbox)
     return (p.kb_half + p.kbox - 1) / p.kbox * p.kbox;
@@ -157,7 +164,7 @@ __host__ __device__ inline SmemLayout smem_layout(const KParams& p) {
     L.tab_off = L.bar_off + 8 * (2 * MAX_STAGES + 6 + MAX_BRES) + 16;
     // tile-blocked A whose K is an odd number of 8-wide panels: a 2-KB zero panel above everything
     // else stands in for the missing half of the last K = 16 step (see the MMA issuer)
-    L.zero_off = (L.tab_off + TILE_TAB * 8 + 127) & ~127u;
+    L.zero_off = (L.tab_off + tile_tab_n(p) * 8 + 127) & ~127u;
     L.total = L.zero_off + ((p.a_blocked && (p.a_nchunks & 1)) ? 2048u : 0u);
     return L;
 }
@@ -240,7 +247,7 @@ __device__ __forceinline__ uint2 tile_pack(const TileCoord& c) {
 }
 // Coordinates of this CTA's tile `it` (< tile_count): from the table, else computed.
 __device__ __forceinline__ TileCoord tile_get(const KParams& p, const TileIter& t, uint32_t tab, int it) {
-    if (it < TILE_TAB) {
+    if (it < tile_tab_n(p)) {
         const uint2 e = ptx::ld_shared_v2u32(tab + 8u * it);
         TileCoord c;
         c.m_blk = static_cast<int>(e.x);
@@ -363,7 +370,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     const TileIter titer = tile_iter(p, PAIR, vblock, vgrid);
     const int ntiles = tile_count(p, titer);
     const uint32_t tile_tab = sbase + L.tab_off;  // explicit shared-window addressing (see s_tile)
-    for (int e = threadIdx.x; e < ntiles && e < TILE_TAB; e += NUM_THREADS)
+    for (int e = threadIdx.x; e < ntiles && e < tile_tab_n(p); e += NUM_THREADS)
         ptx::st_shared_v2u32(tile_tab + 8u * e, tile_pack(tile_coord(p, tile_at(p, titer, e))));
     if (p.a_blocked && (p.a_nchunks & 1)) {  // the zero panel (generic stores -> async proxy)
         for (uint32_t o = threadIdx.x * 16u; o < 2048u; o += NUM_THREADS * 16u)
@@ -740,6 +747,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             const uint32_t b_stage_h = p.b_stage_bytes;
             const uint32_t a_ks = a_kstep >> 4, b_ks = p.b_kstep >> 4, b_hh = p.b_half_bytes >> 4;
             const uint32_t d_half = static_cast<uint32_t>(p.BN / 2);
+            const bool split_h = KIND == KIND_GEMM && p.split_rel != 0;
             // K blocks issued as one unrolled burst of four K = 16 MMAs (all 8 panels valid).  Streamed
             // pair plans keep the per-step loop: the burst measured ~5% slower there at full size
             // (C4 gate S3 2.49 -> 2.62 ms, down S1 2.35 -> 2.49 ms, same box), while it speeds up
@@ -762,6 +770,77 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 }
                 if (!BLR_DBG_ON(p, 32)) ptx::mbar_wait(tempty_bar + 8 * acc, acc_phase ^ 1);
                 ptx::tc_fence_after();
+                if (split_h) {
+                    // wide tile, one accumulator, per-half release (KParams::split_rel): column half 0
+                    // is free (waited above).  Until the epilogue frees half 1, each K block issues
+                    // only its half-0 MMAs and keeps its ring slot; once half 1 is free the held
+                    // blocks' half-1 MMAs are issued in order and their slots released.  At most
+                    // stages - 1 slots are held, so the producer always has one to fill.
+                    bool h1 = false;
+                    int npend = 0, pst = 0, psi = 0;
+                    auto issue = [&](int st, int si, int h) {  // elected lane: one 64-K block of half h
+                        const uint32_t a_lo = a_lo0 + ((static_cast<uint32_t>(st) * a_blk) >> 4);
+                        const uint32_t b_lo = b_lo0 + ((static_cast<uint32_t>(st) * b_stage_h) >> 4) + (h ? b_hh : 0u);
+                        const uint32_t d = tmem_base + (h ? d_half : 0u);
+#pragma unroll
+                        for (int kk = 0; kk < BK / UMMA_K; ++kk) {
+                            const uint64_t ad = ptx::desc_make(a_lo + kk * a_ks, a_hi);
+                            const uint64_t bd = ptx::desc_make(b_lo + kk * b_ks, b_hi);
+                            const uint32_t acc1 = (si | kk) != 0 ? 1u : 0u;
+                            if constexpr (PAIR == 2) ptx::mma_bf16_pair(d, ad, bd, idesc, acc1);
+                            else ptx::mma_bf16(d, ad, bd, idesc, acc1);
+                        }
+                    };
+                    auto catch_up = [&]() {
+                        ptx::tc_fence_after();
+                        if (ptx::elect_one()) {
+                            int st = pst;
+                            for (int q = 0; q < npend; ++q) {
+                                issue(st, psi + q, 1);
+                                commit_slot(empty_bar + 8 * st);
+                                if (++st == p.stages) st = 0;
+                            }
+                        }
+                        __syncwarp();
+                        npend = 0;
+                        h1 = true;
+                    };
+                    const int max_pend = p.stages - 1;
+                    for (int si = 0; si < n_steps; ++si) {
+                        if (!h1 && npend >= max_pend) {
+                            ptx::mbar_wait(tempty_bar + 8, acc_phase ^ 1);
+                            catch_up();
+                        }
+                        ptx::mbar_wait(full_bar + 8 * stage, phase);
+                        if (!h1) {
+                            uint32_t ok = ptx::mbar_test_wait(tempty_bar + 8, acc_phase ^ 1) ? 1u : 0u;
+                            ok = __shfl_sync(0xffffffffu, ok, 0);
+                            if (ok) catch_up();
+                        }
+                        ptx::tc_fence_after();
+                        if (ptx::elect_one()) {
+                            issue(stage, si, 0);
+                            if (h1) {
+                                issue(stage, si, 1);
+                                commit_slot(empty_bar + 8 * stage);
+                            }
+                        }
+                        __syncwarp();
+                        if (!h1) {
+                            if (npend == 0) {
+                                pst = stage;
+                                psi = si;
+                            }
+                            ++npend;
+                        }
+                        ++mstep_tr;
+                        if (++stage == p.stages) { stage = 0; phase ^= 1; }
+                    }
+                    if (!h1) {
+                        ptx::mbar_wait(tempty_bar + 8, acc_phase ^ 1);
+                        catch_up();
+                    }
+                } else
                 for (int sub = 0; sub < p.n_sub; ++sub) {
                     const uint32_t d_tmem = tmem_base + acc * acc_stride + sub * p.BN;
                     for (int si = 0; si < n_steps; ++si) {
@@ -930,6 +1009,19 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             ptx::tc_fence_after();
             if (trace && ew == 0 && lane == 0 && it == 0) trace[10] = clock64();
             const uint32_t tbase = tmem_base + acc * acc_stride + lane_addr;
+            // per-half release (KParams::split_rel): column half 0 is freed as soon as this warp's
+            // chunks below BN/2 are in registers
+            const bool split_e = KIND == KIND_GEMM && p.split_rel != 0;
+            bool rel0 = false;
+            auto release_h0 = [&]() {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if constexpr (PAIR == 2) ptx::mbar_arrive_remote(tempty_bar, lead_rank);
+                    else ptx::mbar_arrive(tempty_bar);
+                }
+                rel0 = true;
+            };
 
             if constexpr (KIND == KIND_BLAST_PROJ) {
                 // Z''_k[t, rho] = sum_l S[l,k,rho] * Z_l[t, rho]   (Fig. 6 "s * z'")
@@ -1029,6 +1121,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                 const uint32_t row_bytes = CW * 2;
                 const uint32_t buf_bytes = 32 * row_bytes;
                 for (int c0 = half * CW; c0 < nvalid; c0 += 2 * CW) {
+                    if (split_e && !rel0 && c0 >= p.BN / 2) release_h0();
                     // TMEM -> registers: CW fp32 columns of this warp's 32 rows (mult. of 8; CW <= 64
                     // except for the unswizzled whole-r' Monarch chunks, staged 64 columns at a time)
                     float fv[64];
@@ -1252,11 +1345,13 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     sig_g = 0;
                 }
             }
+            if (split_e && !rel0) release_h0();
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-                if constexpr (PAIR == 2) ptx::mbar_arrive_remote(tempty_bar + 8 * acc, lead_rank);  // leader's barrier
-                else ptx::mbar_arrive(tempty_bar + 8 * acc);
+                const uint32_t tb = tempty_bar + 8 * (split_e ? 1 : acc);  // split: column half 1
+                if constexpr (PAIR == 2) ptx::mbar_arrive_remote(tb, lead_rank);  // leader's barrier
+                else ptx::mbar_arrive(tb);
             }
             if (++acc == p.acc_bufs) { acc = 0; acc_phase ^= 1; }
         }

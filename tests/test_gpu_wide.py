@@ -1,0 +1,63 @@
+"""Wide CTA-pair tiles (two MMAs of N = BN/2 per K step into one TMEM accumulator, BLR_WIDE=1) with
+the per-half accumulator release (KParams::split_rel: the epilogue frees column half 0 first, the
+next tile's K blocks start on half 0 and hold their ring slots until half 1 is free, then catch up).
+
+Against the fp64 oracle on ragged token / K / N tails, K shorter than the ring (the catch-up at the
+tile end), K much longer than the ring (the hold limit), and the BLAST split path whose S1 writes the
+tile-blocked fp16 Z.  The same products in the same K order as the default 256-column tiles, so the
+two plans must agree bit for bit (the MMA's K = 16 step sums do not depend on the tile's N)."""
+import pytest
+import torch
+
+from oracle import oracle as orc
+from paper_2512_20861_b200 import synth
+from tests.parity import assert_parity, sample_rows, to64
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda")
+
+
+def _lowrank(cuda_lib, X, V, U):
+    Y = cuda_lib.lowrank_matmul(X, V, U)
+    torch.cuda.synchronize()
+    return Y
+
+
+@pytest.mark.parametrize("split", ["1", "0"])
+@pytest.mark.parametrize("n,i,o,r", [
+    (1000, 64, 1104, 264),     # K = 64: one K block per tile (every tile ends with the catch-up)
+    (640, 520, 520, 512),      # ragged K tail, N = 520 (two wide tiles, the second mostly empty)
+    (2500, 1024, 1376, 320),   # long K for S1 (the hold limit), ragged rows
+    (257, 200, 784, 296),      # a CTA pair's second tile past n_tok
+])
+def test_wide_lowrank(cuda_lib, monkeypatch, split, n, i, o, r):
+    X = synth.make_x(n, i, seed=n + 1).to(DEV)
+    V, U = [t.to(DEV) for t in synth.lowrank_factors(i, o, r, seed=o + 1)]
+    Y0 = _lowrank(cuda_lib, X, V, U)
+    monkeypatch.setenv("BLR_WIDE", "1")
+    monkeypatch.setenv("BLR_SPLITREL", split)
+    Y = _lowrank(cuda_lib, X, V, U)
+    rows = sample_rows(n, 64)
+    ref = orc.lowrank_forward(to64(X[rows].cpu()), to64(V.cpu()), to64(U.cpu()))
+    assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"wide lowrank {n, i, o, r} split={split}")
+    assert torch.equal(Y, Y0), f"wide vs default tiles {n, i, o, r} split={split}"
+    # deterministic: the hand-over order depends on timing, the arithmetic must not
+    Y2 = _lowrank(cuda_lib, X, V, U)
+    assert torch.equal(Y2, Y)
+
+
+@pytest.mark.parametrize("n,b1,b2,r,p,q", [(1000, 16, 16, 272, 64, 88),
+                                           (4100, 4, 4, 1488, 176, 688)])   # C4 down-proj-like S1 (N = r)
+def test_wide_blast_split(cuda_lib, monkeypatch, n, b1, b2, r, p, q):
+    i, o = b1 * p, b2 * q
+    X = synth.make_x(n, i, seed=7).to(DEV)
+    V, S, U = [t.to(DEV) for t in synth.blast_factors(i, o, b1, b2, r, seed=7)]
+    monkeypatch.setenv("BLR_BLAST_PATH", "split")
+    Y0 = cuda_lib.blast_matmul(X, V, S, U)
+    monkeypatch.setenv("BLR_WIDE", "1")
+    Y = cuda_lib.blast_matmul(X, V, S, U)
+    torch.cuda.synchronize()
+    rows = sample_rows(n, 64)
+    ref = orc.blast_forward(to64(X[rows].cpu()), to64(V.cpu()), to64(S.cpu()), to64(U.cpu()))
+    assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"wide blast {n, b1, b2, r}")
+    assert torch.equal(Y, Y0)
