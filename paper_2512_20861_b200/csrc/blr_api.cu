@@ -302,9 +302,9 @@ blr_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
     if (const char* pe = getenv("BLR_PLAN"); pe && pe[0] == '1')
         fprintf(stderr,
                 "[blr plan] kind=%d pair=%d mc=%d grid=%d tiles=%dx%dx%d BN=%d mma=%d bbox=%d kblk=%d kbox=%d stages=%d res=%d "
-                "cps=%d bufs=%d acc=%d cbox=%d split=%d smem=%d\n",
+                "cps=%d bufs=%d acc=%d cbox=%d split=%d lastn=%d smem=%d\n",
                 KIND, PAIR, p.mc, grid, p.tiles_m, p.groups, p.tiles_n, p.BN, p.n_mma, p.b_box_n, p.k_blocks, p.kbox, p.stages,
-                p.b_resident, p.cps, p.stage_bufs, p.acc_bufs, p.c_box_w, p.split_rel, smem);
+                p.b_resident, p.cps, p.stage_bufs, p.acc_bufs, p.c_box_w, p.split_rel, p.last_nb, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(blr::NUM_THREADS);
@@ -559,6 +559,16 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
             KParams w;
             if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, p.n_mma == 2, mc)) p = w;
         }
+    }
+    // the last N tile's MMA covers only its valid columns (rounded up to 16): C4 gate S3's N = 688 is
+    // two 256-column tiles and one of 176 (KParams::last_nb; BLR_LASTN=0 off)
+    {
+        const char* ln = getenv("BLR_LASTN");
+        const int64_t last = N - static_cast<int64_t>(p.tiles_n - 1) * p.BN;
+        const int64_t lnb = rup(last, 16);
+        p.last_nb = (p.n_mma == 1 && !p.b_resident && p.mc <= 1 && p.tiles_n >= 1 && lnb < p.BN && lnb >= 16 &&
+                     !(ln && ln[0] == '0'))
+                        ? static_cast<int>(lnb) : 0;
     }
     // wide tiles free their two MMA column halves separately (KParams::split_rel; BLR_SPLITREL=0 off)
     {

@@ -129,6 +129,10 @@ struct KParams {
                                     //    this grid's later CTAs need while the earlier ones wait on them)
     int tab_n;                      // tile-table entries (0: TILE_TAB); wide plans take 128 so a fourth
                                     // 48-KB ring stage fits
+    int last_nb;                    // > 0: the last N tile's MMA is only last_nb columns wide (its valid
+                                    // columns rounded up to 16) and each CTA of a pair loads last_nb / 2
+                                    // of them: no MMA work on padding columns (C4 gate S3: 688 = 256 +
+                                    // 256 + 176)
     int split_rel;                  // wide tile, one accumulator: the epilogue frees the two MMA column
                                     // halves separately (tempty_bar[0] / [1]); the next tile's K steps
                                     // start on half 0 and hold their ring slots until half 1 is free,
@@ -480,6 +484,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     for (int j2 = 0; j2 < mcs; ++j2) mc_mask |= static_cast<uint16_t>(1u << (2 * j2 + crank));
                     const int mc_kr = BK / mcs;                              // MN-major: K rows per slice
                     const int mc_nr = ptx::pin(BNf / n_mma / PAIR / mcs);    // K-major: N rows per slice
+                    const int last_nb = ptx::pin(p.last_nb), last_blk = ptx::pin(p.tiles_n - 1);
                     for (int it = 0; it < ntiles; ++it) {
                         const TileCoord tc = tile_get(p, titer, tile_tab, it);
                         const int t128 = (tc.m_blk * mcs + static_cast<int>(pidx)) * PAIR + static_cast<int>(crank);
@@ -524,7 +529,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         }
                         const int a_row0 = (tc.g * a_tiles + t128) * a_nch * 16;  // tile-blocked A
                         const int a_c1 = a_gmid ? tc.g : m0, a_c2 = a_gmid ? m0 : tc.g;
-                        const int nb0 = tc.n_blk * BNf + static_cast<int>(crank) * bn_cta;  // half 0, this CTA
+                        const int nb0 = tc.n_blk * BNf + static_cast<int>(crank) *
+                                        ((last_nb > 0 && tc.n_blk == last_blk) ? last_nb / PAIR : bn_cta);  // half 0, this CTA
                         const int n_sub = KIND == KIND_BLAST_PROJ ? p.n_sub : 1;  // BLAST proj: the b1 sub-GEMMs l
                         for (int sub = 0; sub < n_sub; ++sub)
                         for (int si = 0; si < ns; ++si) {
@@ -661,8 +667,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                     if (!p.b_resident) {
                                         for (int h = 0; h < p.n_mma; ++h) {
                                             // this CTA's share of half h: columns n0h .. of the tile
+                                            const int share = (p.last_nb > 0 && tc.n_blk == p.tiles_n - 1)
+                                                                  ? p.last_nb / PAIR : p.BN / p.n_mma / PAIR;
                                             const int n0h = tc.n_blk * p.BN + h * (p.BN / p.n_mma) +
-                                                            static_cast<int>(crank) * (p.BN / p.n_mma / PAIR);
+                                                            static_cast<int>(crank) * share;
                                             const uint32_t bh = b_dst + h * p.b_half_bytes;
                                             if constexpr (PAIR == 2) {
                                                 if (mcs > 1) {
@@ -715,6 +723,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
         // Warp-wide schedule (uniform registers); one elected lane issues the MMAs and commits.
         if (leader) {
             const uint32_t idesc = ptx::idesc_bf16(BM * PAIR, p.BN / p.n_mma, p.b_mn_major);
+            const uint32_t idesc_last = p.last_nb > 0 ? ptx::idesc_bf16(BM * PAIR, p.last_nb, p.b_mn_major) : idesc;
             const uint16_t pair_mask = static_cast<uint16_t>(3u << (2 * pidx));
             const uint16_t all_mask = mcs > 1 ? static_cast<uint16_t>((1u << (2 * mcs)) - 1u) : pair_mask;
             auto commit = [&](uint32_t bar) {  // own pair (accumulator / resident-B hand-offs)
@@ -762,6 +771,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             int mstep_tr = 0;
             for (int it = 0; it < ntiles; ++it) {
                 const TileCoord tc = tile_get(p, titer, tile_tab, it);
+                const uint32_t idesc_t = (p.last_nb > 0 && tc.n_blk == p.tiles_n - 1) ? idesc_last : idesc;
                 bool fresh = false;  // first tile of a new resident slice: wait per B block
                 if (p.b_resident && tc.slice != cur_slice) {
                     cur_slice = tc.slice;
@@ -877,8 +887,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                         const uint64_t bd = ptx::desc_make(b_lo + kk * b_ks, b_hi);
                                         const uint32_t acc1 = accf | (kk != 0 ? 1u : 0u);
                                         if (BLR_DBG_ON(p, 8)) continue;  // debug: skip the MMA itself
-                                        if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc, acc1);
-                                        else ptx::mma_bf16(d_tmem, ad, bd, idesc, acc1);
+                                        if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc_t, acc1);
+                                        else ptx::mma_bf16(d_tmem, ad, bd, idesc_t, acc1);
                                         if (two_h) {  // second half: same A, B half 1, next TMEM columns
                                             const uint64_t bd2 = ptx::desc_make(b_lo + b_hh + kk * b_ks, b_hi);
                                             if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem + d_half, ad, bd2, idesc, acc1);
@@ -909,8 +919,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                     }
                                     const uint64_t bd = ptx::desc_make(b_lo0 + ((b_off + kk * p.b_kstep) >> 4), b_hi);
                                     if (BLR_DBG_ON(p, 8)) continue;  // debug: skip the MMA itself
-                                    if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
-                                    else ptx::mma_bf16(d_tmem, ad, bd, idesc, (si | j | kk) != 0);
+                                    if constexpr (PAIR == 2) ptx::mma_bf16_pair(d_tmem, ad, bd, idesc_t, (si | j | kk) != 0);
+                                    else ptx::mma_bf16(d_tmem, ad, bd, idesc_t, (si | j | kk) != 0);
                                     if (p.n_mma == 2) {  // second half: same A, B half 1, next TMEM columns
                                         const uint64_t bd2 = ptx::desc_make(
                                             b_lo0 + ((b_off + p.b_half_bytes + kk * p.b_kstep) >> 4), b_hi);

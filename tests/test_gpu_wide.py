@@ -61,3 +61,32 @@ def test_wide_blast_split(cuda_lib, monkeypatch, n, b1, b2, r, p, q):
     ref = orc.blast_forward(to64(X[rows].cpu()), to64(V.cpu()), to64(S.cpu()), to64(U.cpu()))
     assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"wide blast {n, b1, b2, r}")
     assert torch.equal(Y, Y0)
+
+
+@pytest.mark.parametrize("method,n,i,o,r,b", [
+    ("blast", 1000, 1024, 16 * 88, 272, 16),   # S3 N = q = 88 < 256: one narrow tile per group
+    ("blast", 2100, 512, 4 * 688, 320, 4),     # S3 N = 688 = 256 + 256 + 176 (C4 gate S3's split)
+    ("lowrank", 700, 520, 600, 264, 1),        # S3 N = 600 = 2 x 256 + 88 -> a 96-column last MMA
+    ("lowrank", 1300, 1000, 1032, 328, 1),     # N = 1032: a 16-column last tile (8 valid)
+])
+def test_last_tile_narrow_mma(cuda_lib, monkeypatch, method, n, i, o, r, b):
+    """The last N tile's MMA covers only its valid columns (KParams::last_nb, each CTA of a pair
+    loading half of them): the same dot products as the full-width MMA, bit for bit, and the oracle."""
+    X = synth.make_x(n, i, seed=3).to(DEV)
+    if method == "blast":
+        fac = [t.to(DEV) for t in synth.blast_factors(i, o, b, b, r, seed=3)]
+        run = lambda: cuda_lib.blast_matmul(X, *fac)  # noqa: E731
+    else:
+        fac = [t.to(DEV) for t in synth.lowrank_factors(i, o, r, seed=3)]
+        run = lambda: cuda_lib.lowrank_matmul(X, *fac)  # noqa: E731
+    monkeypatch.setenv("BLR_BLAST_PATH", "split")
+    Y = run()
+    monkeypatch.setenv("BLR_LASTN", "0")
+    Y0 = run()
+    torch.cuda.synchronize()
+    assert torch.equal(Y, Y0), f"last-tile MMA width {method} {n, i, o, r, b}"
+    rows = sample_rows(n, 48)
+    Xr = to64(X[rows].cpu())
+    fr = [to64(t.cpu()) for t in fac]
+    ref = orc.blast_forward(Xr, *fr) if method == "blast" else orc.lowrank_forward(Xr, *fr)
+    assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"last tile {method} {n, i, o, r, b}")
