@@ -500,6 +500,13 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
                         bool no_res = false) {
     KParams& p = g.p;
     int pair = 1;
+    // a tile-blocked A with an odd panel count adds a 2-KB zero panel to the smem layout (set on the
+    // plan only below): reserve it while planning, so no plan exceeds the opt-in limit with it
+    struct ReserveZero {
+        int add;
+        explicit ReserveZero(int a) : add(a) { t_smem_reserve += add; }
+        ~ReserveZero() { t_smem_reserve -= add; }
+    } reserve_zero((a_blocked && ((K / 8) & 1)) ? 2048 : 0);
     // CTA pairs by default from 256 tokens (BLR_PAIR=1: single CTAs, BLR_PAIR=0: the shape heuristic
     // below, BLR_PAIR=2: pairs)
     const char* pe = getenv("BLR_PAIR");
@@ -528,12 +535,13 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
     }
     // wide pair tiles (two MMAs of N = 256 per K step into one 512-column accumulator whose halves
     // the epilogue frees separately, KParams::split_rel): 48 KB of operands per 128x512x64 MACs
-    // instead of 32 KB per 128x256x64, i.e. 25 % fewer L2 -> SM bytes per MAC.  Default where the
-    // tile is exactly 512 columns of whole 64-column slabs, the A operand is a plain K-major matrix
-    // (the per-half release), K is long enough for the tile's MMAs to cover its epilogue (>= 8 K
-    // blocks; C4 gate S1's 4 and ViT's 2 lose) and there are enough tiles for the halved tile count
-    // to fill the pairs evenly (>= 8 per pair): dense 65536x2048x11008 3.34 -> 2.96 ms, C4 down layer 3.85 -> 3.68 ms;
-    // C3's 4096-token phases lose (3-4 waves of wide tiles).  BLR_WIDE=0/1 overrides (1: any width).
+    // instead of 32 KB per 128x256x64, i.e. 25 % fewer L2 -> SM bytes per MAC.  Default where each
+    // CTA's half of B is one TMA op (a 512-column tile of whole 64-column slabs of an MN-major B
+    // over a plain A), K is long enough for the tile's MMAs to cover its epilogue (>= 8
+    // K blocks; C4 gate S1's 4 and ViT's 2 lose) and there are enough tiles for the halved tile count
+    // to fill the pairs evenly (>= 8 per pair): dense 65536x2048x11008 3.34 -> 2.96 ms, C4 down layer
+    // 3.93 -> 3.83 ms; C3's 4096-token phases lose (3-4 waves of wide tiles).  BLR_WIDE=0/1
+    // overrides (1: any width).
     {
         const char* we = getenv("BLR_WIDE");
         const bool force = we && we[0] == '1';
@@ -542,8 +550,12 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
             KParams w;
             if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, true)) {
                 const int units = d.sm_count / 2;
-                const bool auto_ok = w.BN == 512 && b_mn_major && w.b_box_n == 64 && w.stages >= 4 && w.kbox == 1 &&
-                                     w.total_tiles >= 8 * units && w.k_blocks >= 8;
+                // MN-major B only, whole 64-column slabs per CTA half (BN = 512).  (K-major B, one box
+                // per half at any width, measured slower: C4K 7.90 -> 8.23 ms with 352-wide gate S3
+                // and 512-wide down S1 tiles; BLR_WIDE=1 forces it)
+                const bool b_ok = b_mn_major && w.BN == 512 && w.b_box_n == 64;
+                const bool auto_ok = b_ok && w.stages >= 4 && w.kbox == 1 && w.total_tiles >= 8 * units &&
+                                     w.k_blocks >= 8;
                 if (force || auto_ok) p = w;
             }
         }
@@ -573,7 +585,7 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
     // wide tiles free their two MMA column halves separately (KParams::split_rel; BLR_SPLITREL=0 off)
     {
         const char* sr = getenv("BLR_SPLITREL");
-        p.split_rel = (p.n_mma == 2 && p.acc_bufs == 1 && !a_blocked && p.kbox == 1 && pair == 2 && !p.b_resident &&
+        p.split_rel = (p.n_mma == 2 && p.acc_bufs == 1 && p.kbox == 1 && pair == 2 && !p.b_resident &&
                        p.mc <= 1 && p.c_box_w <= 64 && p.stages >= 2 && !(sr && sr[0] == '0'))
                           ? 1 : 0;
     }

@@ -789,12 +789,27 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     bool h1 = false;
                     int npend = 0, pst = 0, psi = 0;
                     auto issue = [&](int st, int si, int h) {  // elected lane: one 64-K block of half h
-                        const uint32_t a_lo = a_lo0 + ((static_cast<uint32_t>(st) * a_blk) >> 4);
+                        const uint32_t a_off = static_cast<uint32_t>(st) * a_blk;
+                        const uint32_t a_lo = a_lo0 + (a_off >> 4);
                         const uint32_t b_lo = b_lo0 + ((static_cast<uint32_t>(st) * b_stage_h) >> 4) + (h ? b_hh : 0u);
                         const uint32_t d = tmem_base + (h ? d_half : 0u);
+                        // tile-blocked A: only the K = 16 steps over valid panels, a half-valid last
+                        // step takes its second core matrix from the zero panel (as in the loop below)
+                        int n16 = BK / UMMA_K;
+                        bool half_last = false;
+                        if (p.a_blocked && si >= full_kb) {
+                            const int vp = min(8, max(0, p.a_nchunks - si * 8));
+                            n16 = (vp + 1) >> 1;
+                            half_last = (vp & 1) != 0;
+                        }
 #pragma unroll
                         for (int kk = 0; kk < BK / UMMA_K; ++kk) {
-                            const uint64_t ad = ptx::desc_make(a_lo + kk * a_ks, a_hi);
+                            if (kk >= n16) break;
+                            uint64_t ad = ptx::desc_make(a_lo + kk * a_ks, a_hi);
+                            if (half_last && kk == n16 - 1) {
+                                const uint32_t pa = a_base + a_off + kk * a_kstep;
+                                ad = ptx::smem_desc(pa, sbase + L.zero_off - pa, 128, 0);
+                            }
                             const uint64_t bd = ptx::desc_make(b_lo + kk * b_ks, b_hi);
                             const uint32_t acc1 = (si | kk) != 0 ? 1u : 0u;
                             if constexpr (PAIR == 2) ptx::mma_bf16_pair(d, ad, bd, idesc, acc1);

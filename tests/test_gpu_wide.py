@@ -90,3 +90,27 @@ def test_last_tile_narrow_mma(cuda_lib, monkeypatch, method, n, i, o, r, b):
     fr = [to64(t.cpu()) for t in fac]
     ref = orc.blast_forward(Xr, *fr) if method == "blast" else orc.lowrank_forward(Xr, *fr)
     assert_parity(Y[torch.as_tensor(rows, device=DEV)], ref, f"last tile {method} {n, i, o, r, b}")
+
+
+@pytest.mark.parametrize("n,b1,b2,r,p,q", [(1000, 16, 16, 272, 64, 88),    # r/8 = 34 panels: half-valid K tail
+                                           (2100, 4, 4, 1488, 176, 688),  # C4-like gate S3 (2 x 352 columns)
+                                           (300, 6, 6, 200, 128, 512)])   # r/8 = 25: odd panel count
+def test_wide_kmajor_blocked_a(cuda_lib, monkeypatch, n, b1, b2, r, p, q):
+    """K-major factor storage, wide tiles forced on every phase: S3's tile-blocked A goes through
+    the per-half-release MMA path with its partial-panel K tail (zero panel), bit for bit equal to
+    the paper-layout call and within the oracle's tolerance."""
+    i, o = b1 * p, b2 * q
+    X = synth.make_x(n, i, seed=9).to(DEV)
+    V, S, U = [t.to(DEV) for t in synth.blast_factors(i, o, b1, b2, r, seed=9)]
+    monkeypatch.setenv("BLR_BLAST_PATH", "split")
+    Y0 = cuda_lib.blast_matmul(X, V, S, U)
+    Vt, Ut = cuda_lib.blast_kmajor_factors(V, U)
+    monkeypatch.setenv("BLR_WIDE", "1")
+    Yk = cuda_lib.blast_matmul(X, Vt, S, Ut, kmajor=True)
+    Yw = cuda_lib.blast_matmul(X, V, S, U)
+    torch.cuda.synchronize()
+    assert torch.equal(Yk, Y0), f"kmajor wide {n, b1, b2, r}"
+    assert torch.equal(Yw, Y0), f"paper layout wide {n, b1, b2, r}"
+    rows = sample_rows(n, 48)
+    ref = orc.blast_forward(to64(X[rows].cpu()), to64(V.cpu()), to64(S.cpu()), to64(U.cpu()))
+    assert_parity(Yk[torch.as_tensor(rows, device=DEV)], ref, f"kmajor wide {n, b1, b2, r}")
