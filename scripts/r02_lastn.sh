@@ -1,4 +1,5 @@
 #!/bin/bash
+# (produced profiles/r02_lastn_ab.txt)
 # narrow last-N-tile MMA (KParams::last_nb): parity/bitwise tests + A/B against BLR_LASTN=0
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 timeout 600 python -m pytest tests/test_gpu_wide.py tests/test_gpu_fuzz.py -x -q > gpurun_out/lastn_tests.txt 2>&1

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (produced profiles/r02_wide_splitrel_ab.txt: in-process A/B of the wide tiles with the per-half release)
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 for c in C4 C4X C4F8; do
   BLR_PLAN=1 timeout 120 python scripts/ab.py $c "" --reps 1 2>&1 | grep "split=1" | sort | uniq > gpurun_out/wide3_plan_$c.txt

@@ -1,5 +1,6 @@
 #!/bin/bash
 # wide tiles over tile-blocked A (K-major factor storage): tests + A/B
+# (produced profiles/r02_wide_kmajor_ab.txt)
 python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
 timeout 600 python -m pytest tests/test_gpu_wide.py tests/test_gpu_pipe.py tests/test_gpu_fuzz.py -x -q > gpurun_out/wide4_tests.txt 2>&1
 echo "tests rc=$?" >> gpurun_out/wide4_tests.txt
