@@ -416,6 +416,11 @@ bool plan_gemm(KParams& p, int pair, const DevInfo& d, int a_gmid, int64_t n_tok
     p.n_mma = wide ? 2 : 1;
     if (wide) {  // N tiles of <= 512, halves multiples of 16 (per-CTA halves multiples of 8)
         p.BN = static_cast<int>(rup(cdiv(N, cdiv(N, 512)), 32));
+        // 512-column tiles whose last one holds at most one half (it then runs as half 0 alone,
+        // KParams::last_half): C4 gate S3's 688 = 512 + 176 instead of 2 x 352 (88-column per-CTA
+        // halves are 2-3 TMA boxes each; whole 64-column slabs are one)
+        const int64_t rem = N % 512;
+        if (N > 512 && rem > 0 && rem <= 256) p.BN = 512;
     } else {
         p.BN = choose_bn(N, K, p.tiles_m * groups, groups, d.sm_count / pair, pair, out.blocked != 0);
         if (pair == 2 && (p.BN / 2) % 8) p.BN = static_cast<int>(rup(p.BN, 32));
@@ -546,6 +551,8 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
         const char* we = getenv("BLR_WIDE");
         const bool force = we && we[0] == '1';
         const bool off = (we && we[0] == '0') || force_pair;
+        // (not over a tile-blocked A by default: C4 gate S3 as 512 + 176-column tiles measured slower,
+        // gate layer 4.06 -> 4.26 ms, as did 2 x 352 -- the 256-column tiles stay there)
         if (!off && pair == 2 && out.col_stride == 0 && N > 256 && (force || !a_blocked)) {
             KParams w;
             if (plan_gemm(w, pair, d, a_gmid, n_tok, K, groups, N, b_mn_major, out, comp, true)) {
@@ -588,6 +595,13 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
         p.split_rel = (p.n_mma == 2 && p.acc_bufs == 1 && p.kbox == 1 && pair == 2 && !p.b_resident &&
                        p.mc <= 1 && p.c_box_w <= 64 && p.stages >= 2 && !(sr && sr[0] == '0'))
                           ? 1 : 0;
+        // a wide plan's last N tile with <= BN/2 valid columns: half 0 alone, rup(valid, 16) wide
+        const int64_t last = N - static_cast<int64_t>(p.tiles_n - 1) * p.BN;
+        const char* lh = getenv("BLR_LASTHALF");
+        if (p.split_rel && last <= p.BN / 2 && !(lh && lh[0] == '0')) {
+            p.last_half = 1;
+            p.last_nb = static_cast<int>(rup(last, 16));
+        }
     }
     const int esz = 2;
     const Swz cs = pick_swz(p.c_box_w * esz);

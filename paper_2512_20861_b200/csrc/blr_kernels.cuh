@@ -133,6 +133,9 @@ struct KParams {
                                     // columns rounded up to 16) and each CTA of a pair loads last_nb / 2
                                     // of them: no MMA work on padding columns (C4 gate S3: 688 = 256 +
                                     // 256 + 176)
+    int last_half;                  // wide plan (split_rel): the last N tile holds <= BN/2 valid columns
+                                    // and runs as column half 0 alone, last_nb wide (C4 gate S3: 688 =
+                                    // 512 + 176): its B half 1 is neither loaded nor multiplied
     int split_rel;                  // wide tile, one accumulator: the epilogue frees the two MMA column
                                     // halves separately (tempty_bar[0] / [1]); the next tile's K steps
                                     // start on half 0 and hold their ring slots until half 1 is free,
@@ -458,6 +461,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     const int nslab = p.b_nslab;
                     const int ns = ptx::pin(n_steps);
                     const uint32_t tx_f = ptx::pin(tx);
+                    const uint32_t tx_lh = ptx::pin(p.kbox * (a_blk + b_bytes / 2) * PAIR);  // single-half last tile
+                    const bool last_half = p.last_half != 0;
                     const int hint_a = p.l2_a, hint_b = p.l2_b;
                     const uint64_t pol_a = ptx::l2_policy(hint_a), pol_b = ptx::l2_policy(hint_b);
                     auto load3h = [&](uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2, int hint,
@@ -531,6 +536,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         const int a_c1 = a_gmid ? tc.g : m0, a_c2 = a_gmid ? m0 : tc.g;
                         const int nb0 = tc.n_blk * BNf + static_cast<int>(crank) *
                                         ((last_nb > 0 && tc.n_blk == last_blk) ? last_nb / PAIR : bn_cta);  // half 0, this CTA
+                        const bool lh = last_half && tc.n_blk == last_blk;  // half 0 only
+                        const int n_mma_t = lh ? 1 : n_mma;
                         const int n_sub = KIND == KIND_BLAST_PROJ ? p.n_sub : 1;  // BLAST proj: the b1 sub-GEMMs l
                         for (int sub = 0; sub < n_sub; ++sub)
                         for (int si = 0; si < ns; ++si) {
@@ -539,7 +546,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             const uint32_t a_st = a_base + stage * (a_blk * kbox);
                             const uint32_t b_st = b_base + stage * (b_stage_b * kbox);
                             if (ptx::elect_one()) {
-                                if (leader) ptx::mbar_arrive_expect_tx(fb, tx_f);
+                                if (leader) ptx::mbar_arrive_expect_tx(fb, lh ? tx_lh : tx_f);
                                 for (int j = 0; j < kbox; ++j) {
                                     const int kb = si * kbox + j;
                                     const int part = (a_lo_off > 0 && kb >= kb_half) ? 1 : 0;
@@ -563,7 +570,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                     else load3h(a_dst, &tmA, fb, part * a_lo_off + k0, a_c1, a_c2, hint_a, pol_a);
                                     if (!b_res) {
                                         const uint32_t b_dst = b_st + j * b_stage_b;
-                                        for (int h = 0; h < n_mma; ++h) {
+                                        for (int h = 0; h < n_mma_t; ++h) {
                                             const int nh = nb0 + h * bn_h;
                                             const uint32_t bh = b_dst + h * b_half_b;
                                             if constexpr (PAIR == 2) {
@@ -642,7 +649,9 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         const uint32_t a_st = a_base + stage * (a_blk * p.kbox);
                         const uint32_t b_st = b_base + stage * (p.b_stage_bytes * p.kbox);
                         if (ptx::elect_one()) {
-                            if (leader) ptx::mbar_arrive_expect_tx(fb, tx);  // (tile-blocked A: always full tiles)
+                            const bool lh_g = p.last_half && tc.n_blk == p.tiles_n - 1;  // single-half last tile
+                            if (leader)
+                                ptx::mbar_arrive_expect_tx(fb, lh_g ? p.kbox * (a_blk + b_bytes / 2) * PAIR : tx);  // (tile-blocked A: always full tiles)
                             if (trace && nstep_tr < 32) trace[64 + nstep_tr] = clock64();
                             for (int j = 0; j < p.kbox; ++j) {
                                 const int kb = si * p.kbox + j;
@@ -665,7 +674,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                                     else
                                         load3(a_dst, &tmA, fb, part * p.a_lo_off + k0, m0, tc.g);
                                     if (!p.b_resident) {
-                                        for (int h = 0; h < p.n_mma; ++h) {
+                                        for (int h = 0; h < (lh_g ? 1 : p.n_mma); ++h) {
                                             // this CTA's share of half h: columns n0h .. of the tile
                                             const int share = (p.last_nb > 0 && tc.n_blk == p.tiles_n - 1)
                                                                   ? p.last_nb / PAIR : p.BN / p.n_mma / PAIR;
@@ -786,7 +795,10 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     // only its half-0 MMAs and keeps its ring slot; once half 1 is free the held
                     // blocks' half-1 MMAs are issued in order and their slots released.  At most
                     // stages - 1 slots are held, so the producer always has one to fill.
-                    bool h1 = false;
+                    // (a single-half last tile, KParams::last_half: half 0 alone, last_nb columns wide)
+                    const bool lh = p.last_half && tc.n_blk == p.tiles_n - 1;
+                    const uint32_t idesc_h = lh ? idesc_last : idesc;
+                    bool h1 = lh;
                     int npend = 0, pst = 0, psi = 0;
                     auto issue = [&](int st, int si, int h) {  // elected lane: one 64-K block of half h
                         const uint32_t a_off = static_cast<uint32_t>(st) * a_blk;
@@ -812,8 +824,8 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                             }
                             const uint64_t bd = ptx::desc_make(b_lo + kk * b_ks, b_hi);
                             const uint32_t acc1 = (si | kk) != 0 ? 1u : 0u;
-                            if constexpr (PAIR == 2) ptx::mma_bf16_pair(d, ad, bd, idesc, acc1);
-                            else ptx::mma_bf16(d, ad, bd, idesc, acc1);
+                            if constexpr (PAIR == 2) ptx::mma_bf16_pair(d, ad, bd, idesc_h, acc1);
+                            else ptx::mma_bf16(d, ad, bd, idesc_h, acc1);
                         }
                     };
                     auto catch_up = [&]() {
@@ -846,7 +858,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                         if (ptx::elect_one()) {
                             issue(stage, si, 0);
                             if (h1) {
-                                issue(stage, si, 1);
+                                if (!lh) issue(stage, si, 1);
                                 commit_slot(empty_bar + 8 * stage);
                             }
                         }
