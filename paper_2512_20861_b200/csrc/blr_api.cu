@@ -842,8 +842,9 @@ bool encode_x_blocked(CUtensorMap* m, const void* X, int64_t n_tok, int64_t b1, 
 // Small n runs the weight-streaming tensor-core decode stages of blr_decode_tc.cuh
 // up to a per-method token count where they measured faster than the tcgen05 prefill path
 // (scripts/decode_bench.py, profiles/r02_decode.txt, profiles/r02_small_n.txt): low rank n <= 16,
-// Monarch n <= 256, BLAST n <= 8 (n <= 2048 when the tcgen05 path would be the S1+S2-fused
-// projection); n > 16 runs as independent 16-token chunks.  BLR_DECODE=1 forces the path for
+// Monarch n <= 256, BLAST n <= 16 (n <= 2048 when the tcgen05 path would be the S1+S2-fused
+// projection; Llama-7B BLAST at n = 12 / 16: 34.7 / 36.0 us vs 39.8 us, profiles/r02_decode.txt);
+// n > 16 runs as independent 16-token chunks.  BLR_DECODE=1 forces the path for
 // every n <= DECODE_MAX_TOKENS, BLR_DECODE_MAXN=m for n <= m, BLR_DECODE=0 disables it.
 bool use_decode(int64_t n_tok, int64_t default_max) {
     if (n_tok > blr::DTC_MAX_N) return false;
@@ -1675,9 +1676,9 @@ blr_status blast_impl(const void* X, int64_t n_tok, int64_t d_in, int64_t d_out,
     // small n: the weight-streaming kernels; up to 2048 tokens where the tcgen05 alternative is the
     // S1+S2-fused projection, whose parallelism is the handful of 128-token tiles (C1, C5 ViT-B)
     // K-major factors (blr_blast_matmul_kmajor): the split tensor-core path only
-    if (kmaj && (use_decode(n_tok, blast_fused(b1, r) ? 2048 : 8) || blast_fused(b1, r) || comp_factor(r) != 1 || fp8z))
+    if (kmaj && (use_decode(n_tok, blast_fused(b1, r) ? 2048 : 16) || blast_fused(b1, r) || comp_factor(r) != 1 || fp8z))
         return BLR_ERR_UNSUPPORTED;
-    if (use_decode(n_tok, blast_fused(b1, r) ? 2048 : 8)) {  // fp32 Z [b1][n][r] (unless fused away), Z'' [b2][n][r]
+    if (use_decode(n_tok, blast_fused(b1, r) ? 2048 : 16)) {  // fp32 Z [b1][n][r] (unless fused away), Z'' [b2][n][r]
         float* z = static_cast<float*>(workspace);
         float* zp2 = z + b1 * n_tok * r;
         int cs = 0, units = 0;

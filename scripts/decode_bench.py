@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LAYERS = [("lowrank", "Llama-7B", "gate_up_proj"), ("monarch", "Llama-7B", "gate_up_proj"),
           ("blast", "Llama-7B", "gate_up_proj"), ("blast", "Llama-7B", "down_proj"),
           ("lowrank", "GPT2-S", "c_fc"), ("blast", "GPT2-S", "c_fc")]
-NS = [1, 8, 16]
+NS = [int(x) for x in os.environ.get("DECODE_NS", "1,8,16").split(",")]
 
 
 def measure():
