@@ -515,7 +515,14 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
     // CTA pairs by default from 256 tokens (BLR_PAIR=1: single CTAs, BLR_PAIR=0: the shape heuristic
     // below, BLR_PAIR=2: pairs)
     const char* pe = getenv("BLR_PAIR");
-    const int force = force_pair ? force_pair : pe ? atoi(pe) : 2;
+    int force = force_pair ? force_pair : pe ? atoi(pe) : 2;
+    // ... except short-K phases (<= 4 K blocks) of small problems: single CTAs give twice the tiles
+    // and no pair coupling there (GPT2-S / ViT-B / Llama-3.2-1B q_o BLAST S3, K = r <= 256: per layer
+    // 4-9 % faster, in-process A/B); BLR_SHORTK_PAIR=1 keeps pairs
+    if (!force_pair && !pe && cdiv(K, blr::BK) <= 4 && n_tok < 32768) {
+        const char* sk = getenv("BLR_SHORTK_PAIR");
+        if (!(sk && sk[0] == '1')) force = 1;
+    }
     if (force == 2 && n_tok >= 256) {
         pair = 2;
     } else if (force != 1) {
