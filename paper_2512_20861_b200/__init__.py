@@ -56,9 +56,12 @@ def load():
                                        ctypes.c_int, vp, vp, sz, vp]
     lib.blr_blast_matmul.argtypes = [vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp]
     lib.blr_blast_matmul_fp8z.argtypes = lib.blr_blast_matmul.argtypes
-    lib.blr_blast_matmul_kmajor.argtypes = lib.blr_blast_matmul.argtypes
-    for fn in ("blr_lowrank_matmul", "blr_monarch_matmul", "blr_blast_matmul", "blr_blast_matmul_fp8z",
-               "blr_blast_matmul_kmajor"):
+    fns = ["blr_lowrank_matmul", "blr_monarch_matmul", "blr_blast_matmul", "blr_blast_matmul_fp8z"]
+    # (an older build loaded through BLR_LIB for an A/B may predate the K-major entry point)
+    if path == LIB_PATH or hasattr(lib, "blr_blast_matmul_kmajor"):
+        lib.blr_blast_matmul_kmajor.argtypes = lib.blr_blast_matmul.argtypes
+        fns.append("blr_blast_matmul_kmajor")
+    for fn in fns:
         getattr(lib, fn).restype = ctypes.c_int
     lib.blr_lowrank_workspace_size.argtypes = [i64, i64, i64, i64]
     lib.blr_monarch_workspace_size.argtypes = [i64, i64, i64, i64, i64, i64]

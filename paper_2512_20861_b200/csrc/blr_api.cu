@@ -519,7 +519,9 @@ blr_status gemm_prepare(GemmPrep& g, const DevInfo& d, const void* A, int a_gmid
     // ... except short-K phases (<= 4 K blocks) of small problems: single CTAs give twice the tiles
     // and no pair coupling there (GPT2-S / ViT-B / Llama-3.2-1B q_o BLAST S3, K = r <= 256: per layer
     // 4-9 % faster, in-process A/B); BLR_SHORTK_PAIR=1 keeps pairs
-    if (!force_pair && !pe && cdiv(K, blr::BK) <= 4 && n_tok < 32768) {
+    // and problems of <= 2048 tokens (<= 16 token tiles: DiT-XL/2 at 1 and 8 images 47 -> 45 us and
+    // 70 -> 66 us; BLR_PAIR=2 forces pairs)
+    if (!force_pair && !pe && ((cdiv(K, blr::BK) <= 4 && n_tok < 32768) || n_tok <= 2048)) {
         const char* sk = getenv("BLR_SHORTK_PAIR");
         if (!(sk && sk[0] == '1')) force = 1;
     }
