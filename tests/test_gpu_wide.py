@@ -114,3 +114,26 @@ def test_wide_kmajor_blocked_a(cuda_lib, monkeypatch, n, b1, b2, r, p, q):
     rows = sample_rows(n, 48)
     ref = orc.blast_forward(to64(X[rows].cpu()), to64(V.cpu()), to64(S.cpu()), to64(U.cpu()))
     assert_parity(Yk[torch.as_tensor(rows, device=DEV)], ref, f"kmajor wide {n, b1, b2, r}")
+
+
+from tests.test_gpu_fuzz import _cases  # noqa: E402  (the fuzz's seeded shape generator)
+
+
+@pytest.mark.parametrize("case", _cases("lowrank", 10, 4242) + _cases("blast", 10, 4343))
+def test_wide_forced_fuzz(cuda_lib, monkeypatch, case):
+    """Every GEMM phase forced onto the wide tiles (BLR_WIDE=1: any width, tile-blocked A too, the
+    per-half release, single-half last tiles) over the fuzz's random shapes: bit for bit the default
+    plans' result (same products, same K order)."""
+    n, i, o, r, b1, b2, _ = case
+    X = synth.make_x(n, i, seed=n + i).to(DEV)
+    if b1 == 1 and b2 == 1:
+        fac = [t.to(DEV) for t in synth.lowrank_factors(i, o, r, seed=o + r)]
+        run = lambda: cuda_lib.lowrank_matmul(X, *fac)  # noqa: E731
+    else:
+        fac = [t.to(DEV) for t in synth.blast_factors(i, o, b1, b2, r, seed=o + r)]
+        run = lambda: cuda_lib.blast_matmul(X, *fac)  # noqa: E731
+    Y0 = run()
+    monkeypatch.setenv("BLR_WIDE", "1")
+    Y = run()
+    torch.cuda.synchronize()
+    assert torch.equal(Y, Y0), f"forced wide {case}"
