@@ -41,8 +41,12 @@ enum Kind : int { KIND_GEMM = 0, KIND_MONARCH_PROJ = 1, KIND_BLAST_PROJ = 2 };
 // Debug switches that skip kernel stages (timing experiments only; the results are then wrong).
 // Compiled in only with -DBLR_DEBUG_KNOBS; release builds ignore KParams::dbg entirely.
 #ifdef BLR_DEBUG_KNOBS
+constexpr bool kGenericProducer = true;
 #define BLR_DBG_ON(p, bit) (((p).dbg & (bit)) != 0)
 #else
+// release builds carry only the lean producer loop: the smaller kernel measured faster on small
+// problems, whose short launches start with a cold instruction cache (DiT-XL/2 one image 45 -> 42 us)
+constexpr bool kGenericProducer = false;
 #define BLR_DBG_ON(p, bit) false
 #endif
 
@@ -438,7 +442,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             int bp_ok = -1;    // highest token tile cleared by back-pressure
             bool fast_done = false;
             {
-                if (trace == nullptr && p.fast_prod) {
+                if (!kGenericProducer || (trace == nullptr && p.fast_prod)) {
                     // Lean producer for the GEMM kind: every parameter the K loop needs is hoisted
                     // into registers and every per-tile coordinate computed once per tile, so a K
                     // block costs a barrier wait, an expect_tx and its TMA issues.  (The generic loop
@@ -608,6 +612,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     }
                 }
             }
+#ifdef BLR_DEBUG_KNOBS  // the generic producer loop (BLR_FASTPROD=0, per-step trace stamps): debug builds only
             for (int it = 0; !fast_done && it < ntiles; ++it) {
                 const TileCoord tc = tile_get(p, titer, tile_tab, it);
                 const int m0 = ((tc.m_blk * mcs + static_cast<int>(pidx)) * PAIR + static_cast<int>(crank)) * BM;
@@ -726,6 +731,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
                     }
                 }
             }
+#endif
         }
     } else if (warp == 1) {
         // ===================================================== MMA issuer ===================
