@@ -343,7 +343,11 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
     const int mcs = (PAIR == 2 && p.mc > 1) ? p.mc : 1;
     const uint32_t lead_rank = cl_rank & ~1u;
     const bool leader = crank == 0;
+#ifdef BLR_DEBUG_KNOBS
     unsigned long long* trace = p.trace ? p.trace + vblock * 128 : nullptr;
+#else
+    unsigned long long* const trace = nullptr;  // per-CTA timeline stamps: debug builds only
+#endif
     // trace stamps: [0] %globaltimer at entry, [8] %clock64 at entry; every other stamp is a
     // %clock64 value (cheap; converted on the host with the SM clock)
     if (trace && threadIdx.x == 0) {

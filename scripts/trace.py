@@ -1,4 +1,6 @@
 """Intra-kernel timeline: per-CTA %globaltimer stamps for each GEMM-kernel launch of one layer call.
+(Needs a debug build of the GEMM kernels' trace stamps: BLR_NVCC_EXTRA=-DBLR_DEBUG_KNOBS before
+__graft_entry__.build(); release builds compile the stamps out.)
 stamps: 0 entry, 1 setup done, 2 after griddepcontrol.wait, 3 MMA got first stage, 4 last MMA commit,
 5 epilogue done (warp 2), 6 bulk stores drained, 7 exit."""
 import ctypes, os, sys

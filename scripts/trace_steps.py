@@ -1,4 +1,6 @@
 """Per-stage timeline of one CTA of a GEMM launch (debug trace stamps, clock64): producer issue
+(Needs a debug build of the GEMM kernels' trace stamps: BLR_NVCC_EXTRA=-DBLR_DEBUG_KNOBS before
+__graft_entry__.build(); release builds compile the stamps out.)
 time and MMA start time of the first 32 ring steps, to tell a load-latency-bound mainloop (MMA
 start = issue + latency, gaps > the MMA time) from an MMA-bound one.
     python scripts/trace_steps.py blast Llama-7B gate_up_proj 65536 <launch index> [cta]"""
