@@ -158,7 +158,11 @@ __global__ void __launch_bounds__(DTC_THREADS)
     auto group_of = [&](int u) { return EPI == 2 ? static_cast<int>(blockIdx.x) * d.n_units + u : gz; };
 
     const int cta_lin = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+#ifdef BLR_DEBUG_KNOBS
     unsigned long long* tr = (d.trace && cta_lin < 2048) ? d.trace + cta_lin * 16 : nullptr;
+#else
+    unsigned long long* const tr = nullptr;  // timeline stamps: debug builds only (scripts/dtc_trace.py)
+#endif
     if (tr && threadIdx.x == 0) tr[0] = ptx::globaltimer();
     if (threadIdx.x == 0) {
         for (int s = 0; s < d.stages; ++s) {

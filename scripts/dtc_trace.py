@@ -1,4 +1,6 @@
 """Timeline of the tensor-core decode launches (debug globaltimer stamps per CTA, ns):
+(Needs a debug build: BLR_NVCC_EXTRA=-DBLR_DEBUG_KNOBS before __graft_entry__.build(); release builds
+compile the stamps out.)
     python scripts/dtc_trace.py METHOD N
 stamps: 0 start, 1 producer go, 2 consumer past wait, 3 A staged, 8.. first ring stages landed,
 4 mainloop done, 5 after cluster sync 1, 6 reduce done, 7 end."""
