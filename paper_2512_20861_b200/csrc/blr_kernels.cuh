@@ -775,7 +775,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             const uint32_t b_stage_h = p.b_stage_bytes;
             const uint32_t a_ks = a_kstep >> 4, b_ks = p.b_kstep >> 4, b_hh = p.b_half_bytes >> 4;
             const uint32_t d_half = static_cast<uint32_t>(p.BN / 2);
-            const bool split_h = KIND == KIND_GEMM && p.split_rel != 0;
+            const bool split_h = KIND == KIND_GEMM && PAIR == 2 && p.split_rel != 0;  // (wide plans are pair plans)
             // K blocks issued as one unrolled burst of four K = 16 MMAs (all 8 panels valid).  Streamed
             // pair plans keep the per-step loop: the burst measured ~5% slower there at full size
             // (C4 gate S3 2.49 -> 2.62 ms, down S1 2.35 -> 2.49 ms, same box), while it speeds up
@@ -1058,7 +1058,7 @@ __device__ __forceinline__ void gemm_body(const CUtensorMap& tmA, const CUtensor
             const uint32_t tbase = tmem_base + acc * acc_stride + lane_addr;
             // per-half release (KParams::split_rel): column half 0 is freed as soon as this warp's
             // chunks below BN/2 are in registers
-            const bool split_e = KIND == KIND_GEMM && p.split_rel != 0;
+            const bool split_e = KIND == KIND_GEMM && PAIR == 2 && p.split_rel != 0;
             bool rel0 = false;
             auto release_h0 = [&]() {
                 ptx::tc_fence_before();
